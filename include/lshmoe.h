@@ -1,0 +1,188 @@
+/*
+ * lshmoe.h — C ABI of the B200-native LSH-MoE compressed expert-parallel dispatch/combine path.
+ *
+ * The operations follow Algorithm 1 of "LSH-MoE" (arXiv 2411.08446, App. A,
+ * L513-543, cited P:Lnnn).  One MoE layer on one rank is, in order:
+ *
+ *   lshmoe_hash      Alg. 1 L5   IDX_i <- LSH(X_i), cross-polytope hash Eq. 3
+ *   lshmoe_compress  Alg. 1 L3, L5-L12  dispatch X into X_i by zeta, divide each X_i
+ *                    into clusters by bucket, centroid = Mean (§2.3)
+ *   lshmoe_dispatch  Alg. 1 L14  Input <- all-to-all(C)
+ *   lshmoe_expert_ffn Alg. 1 L15 Output <- Expert(Input)   [harness utility]
+ *   lshmoe_combine   Alg. 1 L16  E(C) <- all-to-all(Output)
+ *   lshmoe_restore   Alg. 1 L17-19 residual compensation Eq. 4-5,
+ *                    summed over the k gated experts as in Eq. 2
+ *
+ * Conventions (all functions):
+ *  - Every function returns an lshmoe_status; nothing throws.  On a non-OK status
+ *    lshmoe_last_error() returns a thread-local message.
+ *  - Pointers are DEVICE pointers unless marked [host].  The caller owns and allocates every
+ *    buffer (e.g. torch tensors); the library never allocates device memory on the hot path.
+ *    Only lshmoe_comm_init allocates (NCCL communicator + a small pinned host plan buffer).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are stream-ordered and
+ *    asynchronous, except lshmoe_rotation (pure host), lshmoe_dispatch at world > 1 (one host
+ *    synchronisation to learn the all-to-all-v counts), lshmoe_comm_* and
+ *    lshmoe_check_device_error.
+ *  - Matrices are row-major.  Token rows (x, centroids, recv, y) must be 16-byte aligned with
+ *    pitch d * sizeof(dtype); f32 needs d % 4 == 0, bf16 needs d % 64 == 0 (the tcgen05 hash
+ *    tiles K and N in multiples of 64) — else LSHMOE_EUNSUPPORTED.
+ *  - Routed copies: copy id c = t*k + s is slot s of token t; zeta (`experts`) is int32 [n, k]
+ *    with ids in [0, num_experts) distinct within a row.  Ids out of range raise the
+ *    device error word (see LSHMOE_EDEVICE).
+ *  - Determinism: every output is a deterministic function of the inputs, independent of the
+ *    stream, the world size w and repeated runs.
+ *  - Aliasing: y may alias x in lshmoe_restore; at world == 1 recv may equal centroids and
+ *    returned may equal expert_out (the exchange is then skipped).  Nothing else may alias.
+ */
+#ifndef LSHMOE_H_
+#define LSHMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSHMOE_ABI_VERSION 1
+#define LSHMOE_UNIQUE_ID_BYTES 128
+#define LSHMOE_MAX_Q 16
+
+typedef enum {
+  LSHMOE_OK = 0,
+  LSHMOE_EINVAL = 1,       /* host-detected bad argument: n < 0, d < 1, q < 1, k < 1, k > E,
+                              E % world != 0, NULL required pointer, misaligned pointer,
+                              capacity / workspace smaller than required */
+  LSHMOE_EUNSUPPORTED = 2, /* valid but outside the kernels' envelope: bf16 with d % 64 != 0,
+                              f32 with d % 4 != 0, d > 32767 (int16 codes), q > LSHMOE_MAX_Q,
+                              n * k >= 2^31 */
+  LSHMOE_ECUDA = 3,        /* CUDA runtime / launch error */
+  LSHMOE_ENCCL = 4,        /* NCCL error, including ncclCommGetAsyncError */
+  LSHMOE_EDEVICE = 5       /* device-side validation failed (expert id outside [0, E));
+                              latched in a device error word, reported by the next call that
+                              synchronises (lshmoe_dispatch at world > 1, lshmoe_check_device_error) */
+} lshmoe_status;
+
+typedef enum { LSHMOE_F32 = 0, LSHMOE_BF16 = 1 } lshmoe_dtype;   /* token = wire = output dtype */
+
+typedef void* lshmoe_stream;                                     /* cudaStream_t */
+typedef struct lshmoe_comm lshmoe_comm;
+
+int lshmoe_abi_version(void);
+const char* lshmoe_last_error(void);
+
+/* Synchronises `stream`, reads and clears the device error word.  LSHMOE_EDEVICE if a kernel
+   latched an error since the last check. */
+lshmoe_status lshmoe_check_device_error(lshmoe_stream stream);
+
+/* ---- a1: random rotations (Eq. 3, "R is a random rotation matrix"; reading R3) ------
+   Writes q row-major d x d matrices R_j (y = R_j x) to out [host] (q*d*d elements of dtype).
+   Recipe (DESIGN.md §3 R3): SplitMix64 counter stream seeded with
+   rotation_seed ^ (0x9E3779B97F4A7C15 * (j+1)), Irwin-Hall(12) approximately-Gaussian G_j,
+   modified Gram-Schmidt over the columns of G_j in fp64 with left-to-right sums and no FMA,
+   R_j = Q_j^T, rounded fp64 -> fp32 (RNE) -> bf16 (RNE) for bf16.  Pure host function,
+   deterministic, bit-identical to the independent oracle (tests/test_abi_rotation.py). */
+lshmoe_status lshmoe_rotation(int d, int q, uint64_t rotation_seed, lshmoe_dtype dtype, void* out);
+
+/* ---- a2: cross-polytope hash, Eq. 3 --------------------------------------------
+   x [n, d] dtype, rotation [q, d, d] dtype (from lshmoe_rotation) -> codes int16 [n, q]:
+   code_tj = sign(y_i*) * (i*+1), i* = argmax_i |y_i|, y = R_j x_t (reading R1); ties to the
+   smallest i, a zero winner is '+' (reading R2).  bf16: tcgen05 tensor cores, bf16 x bf16
+   products, fp32 accumulation; f32: SIMT fp32 FMA (reading R19).  Hashed once per token, shared
+   by its k routed copies (reading R6).  n == 0 is a no-op. */
+lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d,
+                          const void* rotation, int q, int16_t* codes, lshmoe_stream stream);
+
+/* ---- a3-a5: group by expert, bucketize, centroid means -------------------------------------
+   Bytes of device workspace lshmoe_compress needs for these sizes. */
+lshmoe_status lshmoe_compress_workspace(int64_t n, int k, int num_experts, int q, int d,
+                                        lshmoe_dtype dtype, size_t* bytes /* [host] out */);
+
+/* Inputs: x [n, d] dtype; codes int16 [n, q] (from lshmoe_hash); experts (zeta) int32 [n, k].
+   Outputs (capacity n*k rows — no token is ever dropped, reading R20):
+     bucket      int32 [n, k]    global centroid row of routed copy (t, s)
+     perm        int32 [n*k]     copy ids grouped by centroid row, ascending within a row (R8)
+     row_start   int32 [n*k+1]   perm offsets of each row; the first m+1 entries are valid
+     expert_rows int32 [E]       m_e = number of centroids of expert e
+     num_rows    int32 [1]       m = sum_e m_e
+     centroids   dtype [n*k, d]  c~ = RNE(mean) in send layout: expert-major, rows of expert e
+                                 at [sum_{e'<e} m_e', ...), local bucket ids in first-appearance
+                                 order of the (t, s)-ordered group (reading R7)
+     centroids_f32 float [n*k, d] nullable: the fp32 means before rounding (parity tier 2)
+   Bucket key = the q-tuple of codes (AND-composite, reading R4); clustering is per
+   (rank, expert) group (Alg. 1 L4-L6, reading R5).  Centroid = fp32 sum in a fixed order
+   divided once by the count (reading R10).  Stream-ordered; no host synchronisation. */
+lshmoe_status lshmoe_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d,
+                              const int16_t* codes, int q,
+                              const int32_t* experts, int k, int num_experts,
+                              int32_t* bucket, int32_t* perm, int32_t* row_start,
+                              int32_t* expert_rows, int32_t* num_rows,
+                              void* centroids, float* centroids_f32,
+                              void* workspace, size_t workspace_bytes, lshmoe_stream stream);
+
+/* ---- a6/a8 communicator ----------------------------------------------------------------------
+   Expert placement: rank p owns experts [p*E/w, (p+1)*E/w).  NCCL over NVLink; the
+   bootstrap id travels over torch.distributed.  world == 1 needs no id (pass NULL). */
+lshmoe_status lshmoe_get_unique_id(uint8_t* id /* [host] LSHMOE_UNIQUE_ID_BYTES */);
+lshmoe_status lshmoe_comm_init(const uint8_t* id /* [host] */, int world, int rank,
+                               lshmoe_comm** out /* [host] */);
+lshmoe_status lshmoe_comm_destroy(lshmoe_comm* comm);
+/* The counts of the last dispatch on this comm: counts [host] int32 [world, E], entry (p, e) =
+   expert_rows[e] of rank p.  Only valid at world > 1 after lshmoe_dispatch. */
+lshmoe_status lshmoe_comm_last_counts(const lshmoe_comm* comm, int32_t* counts, int num_experts);
+
+/* ---- a6: dispatch, Alg. 1 L14: send only the centroids ------------------------------
+   centroids [m, d] in compress's send layout; expert_rows [E] device.  recv [recv_capacity, d]
+   receives, on rank p, the rows of p's local experts ordered by (local expert, source rank,
+   local bucket) (reading R24); recv_rows int32 [E/w, w] device out = rows per (local expert,
+   source).  world > 1: all-gathers the counts (ncclAllGather), synchronises `stream` once to
+   read them, then one grouped ncclSend/ncclRecv all-to-all-v; checks the device error word.
+   world == 1 (comm may be NULL): a device-side copy bounded by the device count (skipped when
+   recv == centroids); no host synchronisation.  recv_total [host] (nullable) receives the row
+   count at world > 1 (left untouched at world == 1). */
+lshmoe_status lshmoe_dispatch(lshmoe_comm* comm, const void* centroids, lshmoe_dtype dtype, int d,
+                              const int32_t* expert_rows, int num_experts,
+                              void* recv, int64_t recv_capacity, int32_t* recv_rows,
+                              int64_t* recv_total, lshmoe_stream stream);
+
+/* ---- a7: expert FFN on the received centroids, Alg. 1 L15 [harness utility] --------
+   out = W2 relu(W1 in + b1) + b2 per local expert, rows segmented by recv_rows
+   [E_local, world].  W1 [E_local, d_ffn, d], b1 [E_local, d_ffn], W2 [E_local, d, d_ffn],
+   b2 [E_local, d] in dtype; hidden [capacity, d_ffn] dtype is scratch; capacity >= rows
+   received.  bf16: tcgen05 GEMMs, fp32 accumulation, hidden rounded to bf16; f32: SIMT. */
+lshmoe_status lshmoe_expert_ffn(const void* in, lshmoe_dtype dtype, int d, int d_ffn,
+                                const int32_t* recv_rows, int experts_local, int world,
+                                const void* W1, const void* b1, const void* W2, const void* b2,
+                                void* hidden, int64_t capacity, void* out, lshmoe_stream stream);
+
+/* ---- a8: combine, Alg. 1 L16: exact reverse of the last dispatch on `comm` ----------
+   expert_out laid out like recv; returned [m, d] receives E(c~) in the centroids' layout. */
+lshmoe_status lshmoe_combine(lshmoe_comm* comm, const void* expert_out, lshmoe_dtype dtype, int d,
+                             const int32_t* expert_rows, int num_experts, void* returned,
+                             int64_t returned_capacity, lshmoe_stream stream);
+
+/* ---- a9: residual-based error compensation, Eq. 4-5, Alg. 1 L17-19 -------------
+   y_t = sum_s g_ts * (returned[b_ts] + (x_t - centroids[b_ts])), b = bucket [n, k], g = gate_weight
+   float [n, k] or NULL (g = 1, Eq. 2 unweighted, reading R13).  The residual is taken against
+   the centroid as transmitted (reading R11), so identity experts restore k*x exactly.  fp32
+   math, y rounded (RNE) to dtype. */
+lshmoe_status lshmoe_restore(const void* x, const void* centroids, const void* returned,
+                             lshmoe_dtype dtype, int64_t n, int d, const int32_t* bucket, int k,
+                             const float* gate_weight, void* y, lshmoe_stream stream);
+
+/* ---- uncompressed expert-parallel baseline (§2.2): same machinery, no LSH ---------
+   lshmoe_permute: rows of x copied into send [n*k, d] grouped by expert (ascending (t, s)
+   within an expert), slot int32 [n, k] = send row of copy (t, s), expert_rows [E] = n_e.
+   lshmoe_unpermute: y_t = sum_s g_ts * returned[slot_ts].  Workspace: lshmoe_compress_workspace. */
+lshmoe_status lshmoe_permute(const void* x, lshmoe_dtype dtype, int64_t n, int d,
+                             const int32_t* experts, int k, int num_experts,
+                             int32_t* slot, int32_t* expert_rows, void* send,
+                             void* workspace, size_t workspace_bytes, lshmoe_stream stream);
+lshmoe_status lshmoe_unpermute(const void* returned, lshmoe_dtype dtype, int64_t n, int d,
+                               const int32_t* slot, int k, const float* gate_weight, void* y,
+                               lshmoe_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSHMOE_H_ */

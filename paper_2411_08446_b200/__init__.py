@@ -1,0 +1,303 @@
+"""paper_2411_08446_b200 — B200-native LSH-MoE compressed expert-parallel dispatch/combine.
+
+Thin Python binding over the C ABI of ``liblshmoe.so`` (include/lshmoe.h).  Every function below
+only marshals arguments (torch tensors -> device pointers, the current CUDA stream) and calls the
+same-named C entry point; every step of the path runs in the library's sm_100a kernels.  There is
+no CPU fallback: importing this package fails loudly if the library is missing.
+
+Steps (Alg. 1): hash -> compress -> dispatch -> expert_ffn -> combine -> restore.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "liblshmoe.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(or python paper_2411_08446_b200/build.py) — there is no CPU fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+OK, EINVAL, EUNSUPPORTED, ECUDA, ENCCL, EDEVICE = range(6)
+F32, BF16 = 0, 1
+UNIQUE_ID_BYTES = 128
+_STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSUPPORTED", 3: "ECUDA", 4: "ENCCL", 5: "EDEVICE"}
+
+_vp, _i64, _i32, _u64, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64, ctypes.c_size_t
+
+_SIGS = {
+    "lshmoe_abi_version": ([], _i32),
+    "lshmoe_last_error": ([], ctypes.c_char_p),
+    "lshmoe_check_device_error": ([_vp], _i32),
+    "lshmoe_rotation": ([_i32, _i32, _u64, _i32, _vp], _i32),
+    "lshmoe_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp], _i32),
+    "lshmoe_compress_workspace": ([_i64, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
+    "lshmoe_compress": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                         _vp, _sz, _vp], _i32),
+    "lshmoe_get_unique_id": ([_vp], _i32),
+    "lshmoe_comm_init": ([_vp, _i32, _i32, ctypes.POINTER(_vp)], _i32),
+    "lshmoe_comm_destroy": ([_vp], _i32),
+    "lshmoe_comm_last_counts": ([_vp, _vp, _i32], _i32),
+    "lshmoe_dispatch": ([_vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp, ctypes.POINTER(_i64), _vp], _i32),
+    "lshmoe_expert_ffn": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp], _i32),
+    "lshmoe_combine": ([_vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp], _i32),
+    "lshmoe_restore": ([_vp, _vp, _vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _vp], _i32),
+    "lshmoe_permute": ([_vp, _i32, _i64, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp], _i32),
+    "lshmoe_unpermute": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _vp], _i32),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+
+class LshmoeError(RuntimeError):
+    def __init__(self, status: int, fn: str):
+        self.status = status
+        msg = _lib.lshmoe_last_error().decode(errors="replace")
+        super().__init__(f"{fn}: {_STATUS.get(status, status)}: {msg}")
+
+
+def _check(st: int, fn: str):
+    if st != OK:
+        raise LshmoeError(st, fn)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.bfloat16:
+        return BF16
+    raise TypeError(f"unsupported dtype {t.dtype} (float32 | bfloat16)")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("lshmoe kernels take CUDA tensors (no CPU fallback)")
+
+
+def abi_version() -> int:
+    return _lib.lshmoe_abi_version()
+
+
+# ---- a1 --------------------------------------------------------------------------------------
+def rotation(d: int, q: int, seed: int, dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
+    """q row-major d x d rotations (host tensor [q, d, d]) from the library's recipe (Eq. 3)."""
+    out = torch.empty((q, d, d), dtype=dtype)
+    _check(_lib.lshmoe_rotation(d, q, seed & (2 ** 64 - 1), _dt(out), _ptr(out)), "lshmoe_rotation")
+    return out
+
+
+# ---- a2 --------------------------------------------------------------------------------------
+def hash(x: torch.Tensor, R: torch.Tensor, codes: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:  # noqa: A001
+    """Cross-polytope codes int16 [n, q] of x [n, d] under rotations R [q, d, d] (Eq. 3)."""
+    _require_cuda(x, R)
+    n, d = x.shape
+    q = R.shape[0]
+    if R.dtype != x.dtype or R.shape[1:] != (d, d):
+        raise ValueError("R must be [q, d, d] in x's dtype")
+    if codes is None:
+        codes = torch.empty((n, q), dtype=torch.int16, device=x.device)
+    _check(_lib.lshmoe_hash(_ptr(x), _dt(x), n, d, _ptr(R), q, _ptr(codes), _stream(stream)), "lshmoe_hash")
+    return codes
+
+
+# ---- a3-a5 -----------------------------------------------------------------------------------
+@dataclass
+class Compressed:
+    bucket: torch.Tensor       # int32 [n, k]
+    perm: torch.Tensor         # int32 [n*k]
+    row_start: torch.Tensor    # int32 [n*k+1]
+    expert_rows: torch.Tensor  # int32 [E]
+    num_rows: torch.Tensor     # int32 [1]
+    centroids: torch.Tensor    # dtype [n*k, d] (first m rows valid)
+    centroids_f32: Optional[torch.Tensor]
+
+
+def compress_workspace_bytes(n: int, k: int, E: int, q: int, d: int, dtype: torch.dtype) -> int:
+    b = ctypes.c_size_t(0)
+    _check(_lib.lshmoe_compress_workspace(n, k, E, q, d, F32 if dtype == torch.float32 else BF16, ctypes.byref(b)),
+           "lshmoe_compress_workspace")
+    return b.value
+
+
+def alloc_compressed(n: int, k: int, E: int, d: int, dtype: torch.dtype, device, with_f32: bool = False) -> Compressed:
+    nk = n * k
+    i32 = dict(dtype=torch.int32, device=device)
+    return Compressed(torch.empty((n, k), **i32), torch.empty(nk, **i32), torch.empty(nk + 1, **i32),
+                      torch.empty(E, **i32), torch.empty(1, **i32),
+                      torch.empty((nk, d), dtype=dtype, device=device),
+                      torch.empty((nk, d), dtype=torch.float32, device=device) if with_f32 else None)
+
+
+def compress(x: torch.Tensor, codes: torch.Tensor, experts: torch.Tensor, num_experts: int,
+             out: Optional[Compressed] = None, workspace: Optional[torch.Tensor] = None,
+             with_f32: bool = False, stream=None) -> Compressed:
+    """Group routed copies by expert, bucket by composite key, centroid means (Alg. 1 L3-L12)."""
+    _require_cuda(x, codes, experts)
+    n, d = x.shape
+    k = experts.shape[1]
+    q = codes.shape[1]
+    if out is None:
+        out = alloc_compressed(n, k, num_experts, d, x.dtype, x.device, with_f32)
+    wsb = compress_workspace_bytes(n, k, num_experts, q, d, x.dtype)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(max(wsb, 16), dtype=torch.uint8, device=x.device)
+    _check(_lib.lshmoe_compress(_ptr(x), _dt(x), n, d, _ptr(codes), q, _ptr(experts), k, num_experts,
+                                _ptr(out.bucket), _ptr(out.perm), _ptr(out.row_start), _ptr(out.expert_rows),
+                                _ptr(out.num_rows), _ptr(out.centroids), _ptr(out.centroids_f32),
+                                _ptr(workspace), workspace.numel(), _stream(stream)), "lshmoe_compress")
+    return out
+
+
+# ---- a6 / a8 ---------------------------------------------------------------------------------
+class Comm:
+    """NCCL communicator owned by the library (world == 1 needs no NCCL)."""
+
+    def __init__(self, world: int = 1, rank: int = 0, unique_id: Optional[bytes] = None):
+        self.world, self.rank = world, rank
+        h = ctypes.c_void_p()
+        idbuf = None
+        if world > 1:
+            if unique_id is None or len(unique_id) != UNIQUE_ID_BYTES:
+                raise ValueError("world > 1 needs the 128-byte unique id from rank 0")
+            idbuf = (ctypes.c_uint8 * UNIQUE_ID_BYTES).from_buffer_copy(unique_id)
+        _check(_lib.lshmoe_comm_init(idbuf, world, rank, ctypes.byref(h)), "lshmoe_comm_init")
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * UNIQUE_ID_BYTES)()
+        _check(_lib.lshmoe_get_unique_id(buf), "lshmoe_get_unique_id")
+        return bytes(buf)
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "Comm":
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        if world == 1:
+            return cls(1, 0)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(world, rank, obj[0])
+
+    @property
+    def handle(self):
+        return self._h
+
+    def last_counts(self, num_experts: int) -> torch.Tensor:
+        out = torch.empty((self.world, num_experts), dtype=torch.int32)
+        _check(_lib.lshmoe_comm_last_counts(self._h, _ptr(out), num_experts), "lshmoe_comm_last_counts")
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.lshmoe_comm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dispatch(comm: Optional[Comm], centroids: torch.Tensor, expert_rows: torch.Tensor, num_experts: int,
+             recv: torch.Tensor, recv_rows: torch.Tensor, stream=None) -> Optional[int]:
+    """Centroid all-to-all-v (Alg. 1 L14).  Returns the received row count at world > 1, else None."""
+    _require_cuda(centroids, expert_rows, recv, recv_rows)
+    d = centroids.shape[1]
+    tot = ctypes.c_int64(-1)
+    _check(_lib.lshmoe_dispatch(comm.handle if comm else None, _ptr(centroids), _dt(centroids), d, _ptr(expert_rows),
+                                num_experts, _ptr(recv), recv.shape[0], _ptr(recv_rows), ctypes.byref(tot),
+                                _stream(stream)), "lshmoe_dispatch")
+    return tot.value if tot.value >= 0 else None
+
+
+def combine(comm: Optional[Comm], expert_out: torch.Tensor, expert_rows: torch.Tensor, num_experts: int,
+            returned: torch.Tensor, stream=None) -> torch.Tensor:
+    """Reverse all-to-all-v (Alg. 1 L16): E(c~) back into the centroid layout."""
+    _require_cuda(expert_out, expert_rows, returned)
+    d = expert_out.shape[1]
+    _check(_lib.lshmoe_combine(comm.handle if comm else None, _ptr(expert_out), _dt(expert_out), d, _ptr(expert_rows),
+                               num_experts, _ptr(returned), returned.shape[0], _stream(stream)), "lshmoe_combine")
+    return returned
+
+
+# ---- a7 --------------------------------------------------------------------------------------
+def expert_ffn(inp: torch.Tensor, recv_rows: torch.Tensor, W1: torch.Tensor, b1: torch.Tensor, W2: torch.Tensor,
+               b2: torch.Tensor, out: Optional[torch.Tensor] = None, hidden: Optional[torch.Tensor] = None,
+               stream=None) -> torch.Tensor:
+    """E_e(x) = W2 relu(W1 x + b1) + b2 over rows segmented by recv_rows [E_local, world] (Alg. 1 L15)."""
+    _require_cuda(inp, recv_rows, W1, b1, W2, b2)
+    cap, d = inp.shape
+    E_local, d_ffn, _ = W1.shape
+    world = recv_rows.shape[1] if recv_rows.dim() == 2 else 1
+    if out is None:
+        out = torch.empty_like(inp)
+    if hidden is None:
+        hidden = torch.empty((cap, d_ffn), dtype=inp.dtype, device=inp.device)
+    _check(_lib.lshmoe_expert_ffn(_ptr(inp), _dt(inp), d, d_ffn, _ptr(recv_rows), E_local, world, _ptr(W1), _ptr(b1),
+                                  _ptr(W2), _ptr(b2), _ptr(hidden), cap, _ptr(out), _stream(stream)),
+           "lshmoe_expert_ffn")
+    return out
+
+
+# ---- a9 --------------------------------------------------------------------------------------
+def restore(x: torch.Tensor, centroids: torch.Tensor, returned: torch.Tensor, bucket: torch.Tensor,
+            gate_weight: Optional[torch.Tensor] = None, y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """y_t = sum_s g_ts (E(c~)[b_ts] + x_t - c~[b_ts])  (Eq. 4-5 + Eq. 2)."""
+    _require_cuda(x, centroids, returned, bucket, gate_weight)
+    n, d = x.shape
+    k = bucket.shape[1]
+    if y is None:
+        y = torch.empty_like(x)
+    _check(_lib.lshmoe_restore(_ptr(x), _ptr(centroids), _ptr(returned), _dt(x), n, d, _ptr(bucket), k,
+                               _ptr(gate_weight), _ptr(y), _stream(stream)), "lshmoe_restore")
+    return y
+
+
+# ---- uncompressed baseline -------------------------------------------------------------------
+def permute(x: torch.Tensor, experts: torch.Tensor, num_experts: int, send: torch.Tensor, slot: torch.Tensor,
+            expert_rows: torch.Tensor, workspace: torch.Tensor, stream=None):
+    _require_cuda(x, experts, send, slot, expert_rows, workspace)
+    n, d = x.shape
+    k = experts.shape[1]
+    _check(_lib.lshmoe_permute(_ptr(x), _dt(x), n, d, _ptr(experts), k, num_experts, _ptr(slot), _ptr(expert_rows),
+                               _ptr(send), _ptr(workspace), workspace.numel(), _stream(stream)), "lshmoe_permute")
+
+
+def unpermute(returned: torch.Tensor, slot: torch.Tensor, y: torch.Tensor, gate_weight=None, stream=None):
+    _require_cuda(returned, slot, y, gate_weight)
+    n, d = y.shape
+    k = slot.shape[1]
+    _check(_lib.lshmoe_unpermute(_ptr(returned), _dt(y), n, d, _ptr(slot), k, _ptr(gate_weight), _ptr(y),
+                                 _stream(stream)), "lshmoe_unpermute")
+    return y
+
+
+def check_device_error(stream=None):
+    _check(_lib.lshmoe_check_device_error(_stream(stream)), "lshmoe_check_device_error")

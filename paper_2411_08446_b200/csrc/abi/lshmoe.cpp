@@ -1,0 +1,182 @@
+// C-ABI surface of liblshmoe.so: argument validation, error reporting and dispatch to the
+// sm_100a kernel launchers.  See include/lshmoe.h for the contract of every entry point.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "lshmoe_internal.h"
+
+namespace lshmoe {
+
+static thread_local std::string g_last_error;
+
+lshmoe_status set_error(lshmoe_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+lshmoe_status cuda_status(int err, const char* what) {
+  if (err == 0) return LSHMOE_OK;
+  return set_error(LSHMOE_ECUDA, std::string(what) + ": " + cudaGetErrorString(static_cast<cudaError_t>(err)));
+}
+
+}  // namespace lshmoe
+
+using namespace lshmoe;
+
+#define REQUIRE(cond, st, msg)                                  \
+  do {                                                          \
+    if (!(cond)) return set_error((st), std::string(__func__) + ": " + (msg)); \
+  } while (0)
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static size_t dsize(lshmoe_dtype t) { return t == LSHMOE_F32 ? 4 : 2; }
+
+static lshmoe_status check_token_shape(const char* fn, lshmoe_dtype dtype, int64_t n, int d) {
+  if (dtype != LSHMOE_F32 && dtype != LSHMOE_BF16) return set_error(LSHMOE_EINVAL, std::string(fn) + ": bad dtype");
+  if (n < 0) return set_error(LSHMOE_EINVAL, std::string(fn) + ": n < 0 (S:L146)");
+  if (d < 1) return set_error(LSHMOE_EINVAL, std::string(fn) + ": d < 1 (S:L51)");
+  if (d > 32767) return set_error(LSHMOE_EUNSUPPORTED, std::string(fn) + ": d > 32767 does not fit int16 codes");
+  if (dtype == LSHMOE_BF16 && d % 64 != 0)
+    return set_error(LSHMOE_EUNSUPPORTED, std::string(fn) + ": bf16 path needs d % 64 == 0");
+  if (dtype == LSHMOE_F32 && d % 4 != 0)
+    return set_error(LSHMOE_EUNSUPPORTED, std::string(fn) + ": f32 path needs d % 4 == 0");
+  return LSHMOE_OK;
+}
+
+extern "C" {
+
+int lshmoe_abi_version(void) { return LSHMOE_ABI_VERSION; }
+
+const char* lshmoe_last_error(void) { return g_last_error.c_str(); }
+
+lshmoe_status lshmoe_check_device_error(lshmoe_stream stream) {
+  int v = 0;
+  int err = read_and_clear_device_error(&v, stream);
+  if (err) return cuda_status(err, "lshmoe_check_device_error");
+  if (v) return set_error(LSHMOE_EDEVICE, "device error word set: expert id outside [0, E) (S:L312)");
+  return LSHMOE_OK;
+}
+
+lshmoe_status lshmoe_rotation(int d, int q, uint64_t seed, lshmoe_dtype dtype, void* out) {
+  REQUIRE(d >= 1, LSHMOE_EINVAL, "d < 1 (S:L51)");
+  REQUIRE(q >= 1, LSHMOE_EINVAL, "q < 1");
+  REQUIRE(out != nullptr, LSHMOE_EINVAL, "out is NULL");
+  REQUIRE(dtype == LSHMOE_F32 || dtype == LSHMOE_BF16, LSHMOE_EINVAL, "bad dtype");
+  REQUIRE(d <= 32767, LSHMOE_EUNSUPPORTED, "d > 32767");
+  return rotation_host(d, q, seed, dtype, out);
+}
+
+lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, const void* rotation, int q,
+                          int16_t* codes, lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, dtype, n, d);
+  if (st) return st;
+  REQUIRE(q >= 1, LSHMOE_EINVAL, "q < 1");
+  REQUIRE(q <= LSHMOE_MAX_Q, LSHMOE_EUNSUPPORTED, "q > LSHMOE_MAX_Q");
+  if (n == 0) return LSHMOE_OK;
+  REQUIRE(x && rotation && codes, LSHMOE_EINVAL, "NULL pointer");
+  REQUIRE(aligned16(x) && aligned16(rotation), LSHMOE_EINVAL, "x / rotation must be 16-byte aligned");
+  int err;
+  if (dtype == LSHMOE_F32) {
+    REQUIRE(d <= 384, LSHMOE_EUNSUPPORTED, "f32 (SIMT) hash supports d <= 384");
+    err = launch_hash_f32(static_cast<const float*>(x), n, d, static_cast<const float*>(rotation), q, codes, stream);
+  } else {
+    err = launch_hash_bf16(x, n, d, rotation, q, codes, stream);
+  }
+  return cuda_status(err, "lshmoe_hash");
+}
+
+lshmoe_status lshmoe_compress_workspace(int64_t n, int k, int E, int q, int d, lshmoe_dtype dtype, size_t* bytes) {
+  (void)q;
+  (void)dtype;
+  REQUIRE(bytes != nullptr, LSHMOE_EINVAL, "bytes is NULL");
+  REQUIRE(n >= 0 && k >= 1 && E >= 1 && d >= 1, LSHMOE_EINVAL, "bad sizes");
+  REQUIRE(n * k < (int64_t(1) << 31), LSHMOE_EUNSUPPORTED, "n * k >= 2^31");
+  *bytes = compress_workspace_layout(n, k, E, d, nullptr, nullptr);
+  return LSHMOE_OK;
+}
+
+lshmoe_status lshmoe_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int16_t* codes, int q,
+                              const int32_t* experts, int k, int E, int32_t* bucket, int32_t* perm,
+                              int32_t* row_start, int32_t* expert_rows, int32_t* num_rows, void* centroids,
+                              float* centroids_f32, void* workspace, size_t workspace_bytes, lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, dtype, n, d);
+  if (st) return st;
+  REQUIRE(q >= 1, LSHMOE_EINVAL, "q < 1");
+  REQUIRE(q <= LSHMOE_MAX_Q, LSHMOE_EUNSUPPORTED, "q > LSHMOE_MAX_Q");
+  REQUIRE(k >= 1 && E >= 1, LSHMOE_EINVAL, "k < 1 or E < 1");
+  REQUIRE(k <= E, LSHMOE_EINVAL, "k > E (S:L228)");
+  REQUIRE(n * k < (int64_t(1) << 31), LSHMOE_EUNSUPPORTED, "n * k >= 2^31");
+  REQUIRE(row_start && expert_rows && num_rows, LSHMOE_EINVAL, "NULL output pointer");
+  if (n > 0) {
+    REQUIRE(x && codes && experts && bucket && perm && centroids, LSHMOE_EINVAL, "NULL pointer");
+    REQUIRE(aligned16(x) && aligned16(centroids) && (!centroids_f32 || aligned16(centroids_f32)),
+            LSHMOE_EINVAL, "x / centroids must be 16-byte aligned");
+  }
+  size_t need = compress_workspace_layout(n, k, E, d, nullptr, nullptr);
+  REQUIRE(workspace_bytes >= need, LSHMOE_EINVAL, "workspace too small (see lshmoe_compress_workspace)");
+  REQUIRE(need == 0 || (workspace && aligned16(workspace)), LSHMOE_EINVAL, "workspace NULL or misaligned");
+  CompressWs ws;
+  compress_workspace_layout(n, k, E, d, workspace, &ws);
+  int err = launch_compress(x, dtype, n, d, codes, q, experts, k, E, bucket, perm, row_start, expert_rows, num_rows,
+                            centroids, centroids_f32, ws, stream);
+  return cuda_status(err, "lshmoe_compress");
+}
+
+lshmoe_status lshmoe_restore(const void* x, const void* ct, const void* ret, lshmoe_dtype dtype, int64_t n, int d,
+                             const int32_t* bucket, int k, const float* g, void* y, lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, dtype, n, d);
+  if (st) return st;
+  REQUIRE(k >= 1, LSHMOE_EINVAL, "k < 1");
+  if (n == 0) return LSHMOE_OK;
+  REQUIRE(x && ct && ret && bucket && y, LSHMOE_EINVAL, "NULL pointer");
+  REQUIRE(aligned16(x) && aligned16(ct) && aligned16(ret) && aligned16(y), LSHMOE_EINVAL, "rows must be 16-byte aligned");
+  return cuda_status(launch_restore(x, ct, ret, dtype, n, d, bucket, k, g, y, stream), "lshmoe_restore");
+}
+
+lshmoe_status lshmoe_expert_ffn(const void* in, lshmoe_dtype dtype, int d, int d_ffn, const int32_t* recv_rows,
+                                int experts_local, int world, const void* W1, const void* b1, const void* W2,
+                                const void* b2, void* hidden, int64_t capacity, void* out, lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, dtype, capacity, d);
+  if (st) return st;
+  REQUIRE(d_ffn >= 1 && experts_local >= 1 && world >= 1, LSHMOE_EINVAL, "bad sizes");
+  if (dtype == LSHMOE_BF16) REQUIRE(d_ffn % 64 == 0, LSHMOE_EUNSUPPORTED, "bf16 FFN needs d_ffn % 64 == 0");
+  if (dtype == LSHMOE_F32) REQUIRE(d_ffn % 4 == 0, LSHMOE_EUNSUPPORTED, "f32 FFN needs d_ffn % 4 == 0");
+  if (capacity == 0) return LSHMOE_OK;
+  REQUIRE(in && recv_rows && W1 && b1 && W2 && b2 && hidden && out, LSHMOE_EINVAL, "NULL pointer");
+  REQUIRE(aligned16(in) && aligned16(hidden) && aligned16(out) && aligned16(W1) && aligned16(W2),
+          LSHMOE_EINVAL, "operands must be 16-byte aligned");
+  return cuda_status(launch_expert_ffn(in, dtype, d, d_ffn, recv_rows, experts_local, world, W1, b1, W2, b2, hidden,
+                                       capacity, out, stream),
+                     "lshmoe_expert_ffn");
+}
+
+lshmoe_status lshmoe_permute(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int32_t* experts, int k, int E,
+                             int32_t* slot, int32_t* expert_rows, void* send, void* workspace, size_t workspace_bytes,
+                             lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, dtype, n, d);
+  if (st) return st;
+  REQUIRE(k >= 1 && E >= 1 && k <= E, LSHMOE_EINVAL, "bad k / E");
+  REQUIRE(n * k < (int64_t(1) << 31), LSHMOE_EUNSUPPORTED, "n * k >= 2^31");
+  REQUIRE(expert_rows, LSHMOE_EINVAL, "NULL expert_rows");
+  if (n > 0) REQUIRE(x && experts && slot && send && aligned16(x) && aligned16(send), LSHMOE_EINVAL, "bad pointer");
+  size_t need = compress_workspace_layout(n, k, E, d, nullptr, nullptr);
+  REQUIRE(workspace_bytes >= need, LSHMOE_EINVAL, "workspace too small");
+  CompressWs ws;
+  compress_workspace_layout(n, k, E, d, workspace, &ws);
+  return cuda_status(launch_permute(x, dtype, n, d, experts, k, E, slot, expert_rows, send, ws, stream), "lshmoe_permute");
+}
+
+lshmoe_status lshmoe_unpermute(const void* returned, lshmoe_dtype dtype, int64_t n, int d, const int32_t* slot, int k,
+                               const float* g, void* y, lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, dtype, n, d);
+  if (st) return st;
+  REQUIRE(k >= 1, LSHMOE_EINVAL, "k < 1");
+  if (n == 0) return LSHMOE_OK;
+  REQUIRE(returned && slot && y && aligned16(returned) && aligned16(y), LSHMOE_EINVAL, "bad pointer");
+  return cuda_status(launch_unpermute(returned, dtype, n, d, slot, k, g, y, stream), "lshmoe_unpermute");
+}
+
+}  // extern "C"

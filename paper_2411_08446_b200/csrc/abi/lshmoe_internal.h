@@ -1,0 +1,61 @@
+// Internal declarations shared by the C-ABI layer (csrc/abi) and the kernel launchers
+// (csrc/kernels).  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "../../../include/lshmoe.h"
+
+namespace lshmoe {
+
+// ---- errors -------------------------------------------------------------------------------
+lshmoe_status set_error(lshmoe_status st, const std::string& msg);
+lshmoe_status cuda_status(int cuda_err, const char* what);   // ECUDA with cudaGetErrorString
+
+// ---- host ---------------------------------------------------------------------------------
+lshmoe_status rotation_host(int d, int q, uint64_t seed, lshmoe_dtype dtype, void* out);
+
+// ---- launchers (csrc/kernels/*.cu); all return cudaError_t as int -------------------------
+int launch_hash_f32(const float* x, int64_t n, int d, const float* R, int q, int16_t* codes, void* stream);
+int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int16_t* codes, void* stream);
+
+struct CompressWs {            // carved from the caller's workspace by compress_workspace_layout
+  int32_t* table;              // [table_size] hash table of representative copy ids
+  int64_t table_size;          // power of two
+  int32_t* rep;                // [nk]
+  uint32_t* keys[2];           // [nk] radix keys (ping-pong)
+  int32_t* vals[2];            // [nk] radix values (ping-pong)
+  int32_t* rowid;              // [nk] centroid row of each first copy
+  int32_t* hist;               // [256 * nblocks_max]
+  float* partial;              // [2 * n_items * d] centroid partial sums of rows spanning items
+  int64_t n_items;
+  size_t bytes;
+};
+size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, CompressWs* ws);
+
+int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int16_t* codes, int q,
+                    const int32_t* experts, int k, int E, int32_t* bucket, int32_t* perm,
+                    int32_t* row_start, int32_t* expert_rows, int32_t* num_rows, void* centroids,
+                    float* centroids_f32, const CompressWs& ws, void* stream);
+
+int launch_permute(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int32_t* experts, int k,
+                   int E, int32_t* slot, int32_t* expert_rows, void* send, const CompressWs& ws, void* stream);
+int launch_unpermute(const void* returned, lshmoe_dtype dtype, int64_t n, int d, const int32_t* slot, int k,
+                     const float* g, void* y, void* stream);
+
+int launch_restore(const void* x, const void* ct, const void* ret, lshmoe_dtype dtype, int64_t n, int d,
+                   const int32_t* bucket, int k, const float* g, void* y, void* stream);
+
+// Copies rows [0, sum(counts[0..E))) of src to dst (d columns) and counts -> counts_out.
+int launch_local_exchange(const void* src, void* dst, int64_t capacity_rows, int row_bytes,
+                          const int32_t* counts, int E, int32_t* counts_out, void* stream);
+
+int launch_expert_ffn(const void* in, lshmoe_dtype dtype, int d, int d_ffn, const int32_t* recv_rows,
+                      int experts_local, int world, const void* W1, const void* b1, const void* W2,
+                      const void* b2, void* hidden, int64_t capacity, void* out, void* stream);
+
+int read_and_clear_device_error(int* value, void* stream);
+int device_sm_count();
+
+}  // namespace lshmoe

@@ -1,0 +1,106 @@
+// a1: random rotation matrices R_j of the cross-polytope hash (Eq. 3, PAPER.md P:L228:
+// "R is a random rotation matrix").  The paper fixes no distribution or recipe (DESIGN.md
+// reading R3); this file fixes one that is bit-reproducible across implementations:
+//   SplitMix64 counter stream -> Irwin-Hall(12) approximately-Gaussian G_j (no libm)
+//   -> modified Gram-Schmidt over the columns of G_j in fp64, every sum left-to-right, no FMA
+//      (this translation unit is compiled with -ffp-contract=off)
+//   -> R_j = Q_j^T -> RNE fp64 -> fp32 (-> RNE bf16).
+// Right-looking MGS: after q_i is fixed, every later column is reduced against it; the inner
+// loop runs over columns j (independent, vectorisable) while the k-sum order stays sequential.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "lshmoe_internal.h"
+
+namespace lshmoe {
+
+static inline uint64_t splitmix64_at(uint64_t state0, uint64_t i /* 1-based */) {
+  uint64_t z = state0 + i * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static inline uint16_t f32_to_bf16_rne(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+// G (row-major d x d, G[r*d + c]) of hash j.
+static void gaussian_matrix(int d, uint64_t state0, std::vector<double>& G) {
+  const size_t nn = static_cast<size_t>(d) * d;
+  G.resize(nn);
+  const double scale = 1.0 / 9007199254740992.0;  // 2^-53
+  for (size_t e = 0; e < nn; ++e) {
+    double g = 0.0;
+    for (int i = 0; i < 12; ++i) {
+      const uint64_t z = splitmix64_at(state0, 12 * e + i + 1);
+      const double u = static_cast<double>(z >> 11) * scale;
+      g = (i == 0) ? u : g + u;
+    }
+    G[e] = g - 6.0;
+  }
+}
+
+// Q (row-major, columns orthonormal) from G by right-looking modified Gram-Schmidt.
+static void mgs_columns(int d, std::vector<double>& A /* in: G, destroyed */, std::vector<double>& Q) {
+  Q.assign(static_cast<size_t>(d) * d, 0.0);
+  std::vector<double> r(d), qi(d);
+  for (int i = 0; i < d; ++i) {
+    double ss = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double v = A[static_cast<size_t>(k) * d + i];
+      const double p = v * v;
+      ss = (k == 0) ? p : ss + p;
+    }
+    const double nrm = std::sqrt(ss);
+    for (int k = 0; k < d; ++k) {
+      qi[k] = A[static_cast<size_t>(k) * d + i] / nrm;
+      Q[static_cast<size_t>(k) * d + i] = qi[k];
+    }
+    if (i + 1 == d) break;
+    // r_j = sum_k qi[k] * A[k][j], sequential in k, for all j > i.
+    for (int k = 0; k < d; ++k) {
+      const double qk = qi[k];
+      const double* row = &A[static_cast<size_t>(k) * d];
+      if (k == 0) {
+        for (int j = i + 1; j < d; ++j) r[j] = qk * row[j];
+      } else {
+        for (int j = i + 1; j < d; ++j) r[j] = r[j] + qk * row[j];
+      }
+    }
+    for (int k = 0; k < d; ++k) {
+      const double qk = qi[k];
+      double* row = &A[static_cast<size_t>(k) * d];
+      for (int j = i + 1; j < d; ++j) row[j] = row[j] - qk * r[j];
+    }
+  }
+}
+
+lshmoe_status rotation_host(int d, int q, uint64_t seed, lshmoe_dtype dtype, void* out) {
+  std::vector<double> G, Q;
+  const size_t nn = static_cast<size_t>(d) * d;
+  for (int j = 0; j < q; ++j) {
+    const uint64_t state0 = seed ^ (0x9E3779B97F4A7C15ull * static_cast<uint64_t>(j + 1));
+    gaussian_matrix(d, state0, G);
+    mgs_columns(d, G, Q);
+    // R_j[i][k] = Q[k][i]
+    if (dtype == LSHMOE_F32) {
+      float* o = static_cast<float*>(out) + j * nn;
+      for (int i = 0; i < d; ++i)
+        for (int k = 0; k < d; ++k) o[static_cast<size_t>(i) * d + k] = static_cast<float>(Q[static_cast<size_t>(k) * d + i]);
+    } else {
+      uint16_t* o = static_cast<uint16_t*>(out) + j * nn;
+      for (int i = 0; i < d; ++i)
+        for (int k = 0; k < d; ++k)
+          o[static_cast<size_t>(i) * d + k] = f32_to_bf16_rne(static_cast<float>(Q[static_cast<size_t>(k) * d + i]));
+    }
+  }
+  return LSHMOE_OK;
+}
+
+}  // namespace lshmoe

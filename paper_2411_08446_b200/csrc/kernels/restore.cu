@@ -1,0 +1,144 @@
+// a9: residual-based error compensation (Eq. 4-5; Alg. 1 L17-19,
+// P:L536-538) summed over the k gated experts as in Eq. 2:
+//     y_t = sum_s g_ts * (E(c~)[b_ts] + (x_t - c~[b_ts]))
+// The residual x - c~ is never materialised: it is recomputed here from x and the transmitted
+// centroid (reading R11), saving a write + read of n*k*d elements.  Flat 128-bit streaming: one
+// thread per 16-byte chunk of an output row; c~ / E(c~) rows are gathers (mostly L2 hits).
+// Also: the baseline un-permute and the world == 1 local exchange.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "../abi/lshmoe_internal.h"
+#include "common.cuh"
+
+namespace lshmoe {
+
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(256) restore_kernel(const T* x /* y may alias x */, const T* __restrict__ ct,
+                                                      const T* __restrict__ ret, int64_t n, int d,
+                                                      const int32_t* __restrict__ bucket, int k,
+                                                      const float* __restrict__ g, T* y) {
+  constexpr int VN = Vec<T>::N;
+  const int cpr = d / VN;
+  const int64_t total = n * cpr;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / cpr;
+    const int ch = static_cast<int>(i - t * cpr);
+    float xv[VN], acc[VN];
+    Vec<T>::load(x + t * d + ch * VN, xv);
+    for (int s = 0; s < k; ++s) {
+      const int64_t b = bucket[t * k + s];
+      float cv[VN], rv[VN];
+      Vec<T>::load(ct + b * d + ch * VN, cv);
+      Vec<T>::load(ret + b * d + ch * VN, rv);
+      const float gw = g ? g[t * k + s] : 1.0f;
+#pragma unroll
+      for (int v = 0; v < VN; ++v) {
+        float term = rv[v] + (xv[v] - cv[v]);       // E(c~) + Delta  (Eq. 5)
+        if (g) term = gw * term;
+        acc[v] = (s == 0) ? term : acc[v] + term;   // Eq. 2 sum over the k experts
+      }
+    }
+    Vec<T>::store(y + t * d + ch * VN, acc);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) unpermute_kernel(const T* __restrict__ ret, int64_t n, int d,
+                                                        const int32_t* __restrict__ slot, int k,
+                                                        const float* __restrict__ g, T* __restrict__ y) {
+  constexpr int VN = Vec<T>::N;
+  const int cpr = d / VN;
+  const int64_t total = n * cpr;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / cpr;
+    const int ch = static_cast<int>(i - t * cpr);
+    float acc[VN];
+    for (int s = 0; s < k; ++s) {
+      const int64_t b = slot[t * k + s];
+      float rv[VN];
+      Vec<T>::load(ret + b * d + ch * VN, rv);
+      const float gw = g ? g[t * k + s] : 1.0f;
+#pragma unroll
+      for (int v = 0; v < VN; ++v) {
+        const float term = g ? gw * rv[v] : rv[v];
+        acc[v] = (s == 0) ? term : acc[v] + term;
+      }
+    }
+    Vec<T>::store(y + t * d + ch * VN, acc);
+  }
+}
+
+// world == 1 "all-to-all": copy the sum(counts) valid rows (device count) and the counts.
+__global__ void __launch_bounds__(256) local_exchange_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                             int64_t capacity_rows, int row_bytes,
+                                                             const int32_t* __restrict__ counts, int E,
+                                                             int32_t* __restrict__ counts_out) {
+  __shared__ int64_t rows_s;
+  if (threadIdx.x == 0) {
+    int64_t r = 0;
+    for (int e = 0; e < E; ++e) r += counts[e];
+    rows_s = r < capacity_rows ? r : capacity_rows;
+  }
+  if (counts_out && blockIdx.x == 0)
+    for (int e = threadIdx.x; e < E; e += blockDim.x) counts_out[e] = counts[e];
+  __syncthreads();
+  if (!dst) return;
+  const int64_t total = rows_s * (row_bytes / 16);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+int grid_for(int64_t work) {
+  const int64_t g = (work + 255) / 256;
+  const int64_t cap = 16 * static_cast<int64_t>(device_sm_count());
+  return static_cast<int>(std::max<int64_t>(1, std::min(g, cap)));
+}
+
+}  // namespace
+
+int launch_restore(const void* x, const void* ct, const void* ret, lshmoe_dtype dtype, int64_t n, int d,
+                   const int32_t* bucket, int k, const float* g, void* y, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == LSHMOE_BF16) {
+    using T = __nv_bfloat16;
+    restore_kernel<T><<<grid_for(n * (d / 8)), 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(ct),
+                                                             static_cast<const T*>(ret), n, d, bucket, k, g,
+                                                             static_cast<T*>(y));
+  } else {
+    restore_kernel<float><<<grid_for(n * (d / 4)), 256, 0, st>>>(static_cast<const float*>(x),
+                                                                 static_cast<const float*>(ct),
+                                                                 static_cast<const float*>(ret), n, d, bucket, k, g,
+                                                                 static_cast<float*>(y));
+  }
+  return cudaGetLastError();
+}
+
+int launch_unpermute(const void* ret, lshmoe_dtype dtype, int64_t n, int d, const int32_t* slot, int k, const float* g,
+                     void* y, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == LSHMOE_BF16) {
+    using T = __nv_bfloat16;
+    unpermute_kernel<T><<<grid_for(n * (d / 8)), 256, 0, st>>>(static_cast<const T*>(ret), n, d, slot, k, g,
+                                                               static_cast<T*>(y));
+  } else {
+    unpermute_kernel<float><<<grid_for(n * (d / 4)), 256, 0, st>>>(static_cast<const float*>(ret), n, d, slot, k, g,
+                                                                   static_cast<float*>(y));
+  }
+  return cudaGetLastError();
+}
+
+int launch_local_exchange(const void* src, void* dst, int64_t capacity_rows, int row_bytes, const int32_t* counts,
+                          int E, int32_t* counts_out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = dst ? 8 * device_sm_count() : 1;
+  local_exchange_kernel<<<grid, 256, 0, st>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), capacity_rows,
+                                              row_bytes, counts, E, counts_out);
+  return cudaGetLastError();
+}
+
+}  // namespace lshmoe

@@ -1,0 +1,103 @@
+"""GPU parity of a2, lshmoe_hash (Eq. 3), against the oracle's fp64 codes.
+
+Tier 1 (BASELINE.json): codes bit-exact except tokens whose oracle top-two margin is below 1e-5
+relative, which are reported (count printed) and allowed to differ."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from helpers import CONFIGS, NEAR_TIE, f64, make_case, small_cfg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_2411_08446_b200 as L
+    assert torch.cuda.is_available()
+    return L
+
+
+def _check_codes(L, case, label):
+    X = case.X.cuda()
+    R = case.R_lib.cuda()
+    codes = L.hash(X, R)
+    torch.cuda.synchronize()
+    got = codes.cpu().numpy()
+    mism = got != case.codes
+    near = case.margins < NEAR_TIE
+    bad = mism & ~near
+    print(f"[hash {label}] n={X.shape[0]} d={X.shape[1]} q={R.shape[0]} mismatches={int(mism.sum())} "
+          f"(near-ties in oracle: {int(near.sum())}, mismatches outside near-tie band: {int(bad.sum())})")
+    assert not bad.any(), np.argwhere(bad)[:10]
+    assert np.all(got != 0) and np.all(np.abs(got) <= X.shape[1])
+    return got
+
+
+@pytest.mark.parametrize("cfgname", ["C1"])
+def test_hash_f32_config(L, cfgname):
+    case = make_case(L, CONFIGS[cfgname], seed=0, sanitize=False)
+    _check_codes(L, case, cfgname)
+
+
+@pytest.mark.parametrize("n,d,q", [(1000, 128, 3), (1, 64, 1), (127, 64, 2), (129, 192, 2), (300, 256, 4),
+                                   (777, 384, 2)])
+def test_hash_bf16_shapes(L, n, d, q):
+    cfg = small_cfg(n=n, d=d, q=q)
+    case = make_case(L, cfg, seed=1, sanitize=False)
+    _check_codes(L, case, f"bf16 n={n} d={d}")
+
+
+@pytest.mark.parametrize("n,d,q", [(300, 64, 2), (50, 8, 3)])
+def test_hash_f32_shapes(L, n, d, q):
+    cfg = small_cfg(n=n, d=d, q=q, dtype="f32")
+    case = make_case(L, cfg, seed=2, sanitize=False)
+    _check_codes(L, case, f"f32 n={n} d={d}")
+
+
+def test_hash_c2_full_size(L):
+    """BASELINE.json configs[1] at full size (16K tokens, d=768, q=6) in the bench's launch config."""
+    case = make_case(L, CONFIGS["C2"], seed=0, sanitize=False)
+    _check_codes(L, case, "C2")
+
+
+def test_hash_d1024(L):
+    cfg = CONFIGS["C3"].with_(n=4096, q=2)
+    case = make_case(L, cfg, seed=0, sanitize=False)
+    _check_codes(L, case, "d=1024")
+
+
+def test_hash_duplicates_and_special_rows(L):
+    """Identical rows at different tile positions hash identically; the zero row hashes to +1;
+    a negated row hashes to the negated code (when not a near tie)."""
+    cfg = small_cfg(n=700, d=256, q=3)
+    case = make_case(L, cfg, seed=3, sanitize=True)
+    X = case.X.clone()
+    X[5] = 0
+    for dst in (130, 257, 384, 699):
+        X[dst] = X[17]
+    X[300] = -X[17]
+    codes = L.hash(X.cuda(), case.R_lib.cuda()).cpu().numpy()
+    assert np.all(codes[5] == 1)
+    for dst in (130, 257, 384, 699):
+        assert np.array_equal(codes[dst], codes[17])
+    assert np.array_equal(codes[300], -codes[17])
+
+
+def test_hash_identity_rotation_examples(L, golden):
+    """SPEC's worked examples through the GPU with R = I (f32 path)."""
+    xs = [c["x"] + [0.0] for c in golden["cp_hash_identity_rotation"]["cases"]]   # pad d=3 -> 4
+    X = torch.tensor(xs, dtype=torch.float32).cuda()
+    R = torch.eye(4, dtype=torch.float32)[None].cuda()
+    codes = L.hash(X, R).cpu().numpy()[:, 0]
+    assert list(codes) == [c["code"] for c in golden["cp_hash_identity_rotation"]["cases"]]
+
+
+def test_hash_scale_invariance(L):
+    cfg = small_cfg(n=512, d=128, q=2, dtype="f32")
+    case = make_case(L, cfg, seed=4, sanitize=True)
+    R = case.R_lib.cuda()
+    a = L.hash(case.X.cuda(), R)
+    b = L.hash((case.X * 4.0).cuda(), R)       # exact power-of-two scaling
+    assert torch.equal(a, b)

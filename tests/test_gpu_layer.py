@@ -1,0 +1,187 @@
+"""GPU parity of a6-a9 (dispatch, expert FFN, combine, restore) and of the whole layer
+(Alg. 1) against the oracle, plus the uncompressed baseline (Eq. 2)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from helpers import (CONFIGS, experts_for, f64, make_case, oracle_experts, row_rel_err, small_cfg,
+                     stack_experts)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_2411_08446_b200 as L
+    return L
+
+
+def _tdt(dtype):
+    return torch.float32 if dtype == "f32" else torch.bfloat16
+
+
+# ---- a9 restore ------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype,k,weighted", [("bf16", 1, False), ("bf16", 2, True), ("f32", 2, False), ("f32", 1, True)])
+def test_restore_matches_oracle(L, dtype, k, weighted):
+    rng = np.random.default_rng(1)
+    n, d, m = 999, 128, 300
+    dt = _tdt(dtype)
+    X = torch.from_numpy(rng.standard_normal((n, d))).to(dt)
+    Ct = torch.from_numpy(rng.standard_normal((m, d))).to(dt)
+    ret = torch.from_numpy(rng.standard_normal((m, d))).to(dt)
+    bucket = torch.from_numpy(rng.integers(0, m, (n, k)).astype(np.int32))
+    g = torch.from_numpy(rng.random((n, k)).astype(np.float32)) if weighted else None
+    y = L.restore(X.cuda(), Ct.cuda(), ret.cuda(), bucket.cuda(), None if g is None else g.cuda())
+    ref = O.restore(f64(X), f64(Ct), f64(ret), bucket.numpy(), None if g is None else f64(g))
+    got = f64(y)
+    if dtype == "bf16":
+        r = O.round_to_dtype(ref, "bf16")
+        assert np.all(np.abs(got - r) <= O.ulp_bf16(r))          # at most 1 ulp from the RNE of the exact
+        print(f"[restore bf16 k={k}] exact-match fraction {np.mean(got == r):.5f}")
+    else:
+        assert row_rel_err(got, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_restore_identity_expert_exact(L, k):
+    """ret = c~ (identity expert) => y = k x (Eq. 4-5 algebra).  In the kernel's fp32
+    arithmetic this is exact wherever x - c~ is exact in fp32 (bf16 operands whose exponents differ
+    by <= 16); everywhere else it is within 1 bf16 ulp."""
+    cfg = small_cfg(n=800, k=k, E=4, q=3, d=128)
+    case = make_case(L, cfg, seed=3, sanitize=False)
+    out = L.compress(case.X.cuda(), torch.from_numpy(case.codes).cuda(), case.zeta.cuda(), 4)
+    y = f64(L.restore(case.X.cuda(), out.centroids, out.centroids, out.bucket))
+    want = k * f64(case.X)
+    ct = f64(out.centroids)[out.bucket.cpu().numpy()]                 # [n, k, d]
+    xs = f64(case.X)[:, None, :]
+    exact = np.all((xs - ct).astype(np.float32).astype(np.float64) == xs - ct, axis=1)
+    assert np.array_equal(y[exact], want[exact])
+    assert np.all(np.abs(y - want) <= O.ulp_bf16(want) + 1e-30)
+    print(f"[restore identity k={k}] exact-eligible fraction {exact.mean():.6f}")
+
+
+def test_restore_in_place(L):
+    rng = np.random.default_rng(2)
+    X = torch.from_numpy(rng.standard_normal((64, 64))).to(torch.bfloat16).cuda()
+    Ct = torch.from_numpy(rng.standard_normal((10, 64))).to(torch.bfloat16).cuda()
+    b = torch.from_numpy(rng.integers(0, 10, (64, 1)).astype(np.int32)).cuda()
+    y0 = L.restore(X, Ct, Ct, b)
+    X2 = X.clone()
+    L.restore(X2, Ct, Ct, b, y=X2)
+    assert torch.equal(X2, y0)
+
+
+# ---- a7 expert FFN -----------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype,d,d_ffn,E_local,world", [("bf16", 128, 256, 3, 1), ("bf16", 768, 3072, 4, 2),
+                                                          ("f32", 64, 256, 2, 1), ("bf16", 64, 192, 2, 3)])
+def test_expert_ffn_matches_oracle(L, dtype, d, d_ffn, E_local, world):
+    cfg = small_cfg(d=d, d_ffn=d_ffn, E=E_local, dtype=dtype)
+    ex = experts_for(cfg, 0)
+    rng = np.random.default_rng(3)
+    rows = rng.integers(0, 300, (E_local, world)).astype(np.int32)
+    rows[0, 0] = 0                                           # an empty segment
+    total = int(rows.sum())
+    cap = total + 37
+    dt = _tdt(dtype)
+    inp = torch.from_numpy(rng.standard_normal((cap, d))).to(dt)
+    W1, b1, W2, b2 = stack_experts(ex, range(E_local), "cuda")
+    out = L.expert_ffn(inp.cuda(), torch.from_numpy(rows).cuda(), W1, b1, W2, b2)
+    got = f64(out[:total])
+    oex = oracle_experts(ex)
+    ref = np.zeros((total, d))
+    pos = 0
+    for e in range(E_local):
+        c = int(rows[e].sum())
+        ref[pos:pos + c] = O.expert_ffn(f64(inp[pos:pos + c]), *oex[e])
+        pos += c
+    err = row_rel_err(got, ref)
+    print(f"[ffn {dtype} d={d} dff={d_ffn}] row-max-rel err {err:.3e}")
+    assert err <= (2e-2 if dtype == "bf16" else 1e-5)
+
+
+# ---- a6 / a8 at world 1 ---------------------------------------------------------------------------
+def test_dispatch_combine_world1_roundtrip(L):
+    rng = np.random.default_rng(4)
+    E, d, m = 6, 128, 500
+    er = rng.multinomial(m, np.ones(E) / E).astype(np.int32)
+    C = torch.from_numpy(rng.standard_normal((m + 20, d))).to(torch.bfloat16).cuda()
+    recv = torch.zeros_like(C)
+    rr = torch.empty((E, 1), dtype=torch.int32, device="cuda")
+    L.dispatch(None, C, torch.from_numpy(er).cuda(), E, recv, rr)
+    assert torch.equal(recv[:m], C[:m]) and torch.all(recv[m:] == 0)
+    assert np.array_equal(rr.cpu().numpy()[:, 0], er)
+    back = torch.zeros_like(C)
+    L.combine(None, recv, torch.from_numpy(er).cuda(), E, back)
+    assert torch.equal(back[:m], C[:m])
+    comm = L.Comm(1, 0)
+    L.dispatch(comm, C, torch.from_numpy(er).cuda(), E, C, rr)     # aliased: pass-through
+    comm.close()
+
+
+# ---- the whole layer --------------------------------------------------------------------------------
+def run_layer(L, case, ex_stacked, E):
+    X = case.X.cuda()
+    n, d = X.shape
+    k = case.zeta.shape[1]
+    codes = L.hash(X, case.R_lib.cuda())
+    out = L.compress(X, codes, case.zeta.cuda(), E)
+    recv = torch.empty_like(out.centroids)
+    rr = torch.empty((E, 1), dtype=torch.int32, device="cuda")
+    L.dispatch(None, out.centroids, out.expert_rows, E, recv, rr)
+    eo = L.expert_ffn(recv, rr, *ex_stacked)
+    ret = torch.empty_like(out.centroids)
+    L.combine(None, eo, out.expert_rows, E, ret)
+    y = L.restore(X, out.centroids, ret, out.bucket, None if case.g is None else case.g.cuda())
+    torch.cuda.synchronize()
+    return codes, out, y
+
+
+@pytest.mark.parametrize("cfgname,tol", [("C1", 1e-5), ("C2", 2e-2)])
+def test_layer_end_to_end(L, cfgname, tol):
+    cfg = CONFIGS[cfgname]
+    case = make_case(L, cfg, seed=0, sanitize=True)
+    ex = experts_for(cfg, 0)
+    codes, out, y = run_layer(L, case, stack_experts(ex, range(cfg.E), "cuda"), cfg.E)
+    assert np.array_equal(codes.cpu().numpy(), case.codes)          # sanitised: no near ties
+    res = O.lsh_layer(f64(case.X), case.zeta.numpy(), case.R64, oracle_experts(ex), cfg.E, cfg.dtype)
+    b = res.buckets[0]
+    assert int(out.num_rows.item()) == b.m
+    assert np.array_equal(out.bucket.cpu().numpy(), b.bucket)
+    err = row_rel_err(f64(y), res.y[0])
+    print(f"[layer {cfgname}] replaced near-tie tokens={case.replaced} ratio={res.ratio:.4f} y row-rel err={err:.3e}")
+    assert err <= tol
+
+
+def test_layer_weighted_top2(L):
+    cfg = small_cfg(n=2000, k=2, E=4, q=3, d=128, d_ffn=256)
+    case = make_case(L, cfg, seed=11, sanitize=True, with_weights=True)
+    ex = experts_for(cfg, 11)
+    _, out, y = run_layer(L, case, stack_experts(ex, range(4), "cuda"), 4)
+    res = O.lsh_layer(f64(case.X), case.zeta.numpy(), case.R64, oracle_experts(ex), 4, "bf16", g=f64(case.g))
+    assert row_rel_err(f64(y), res.y[0]) <= 2e-2
+
+
+# ---- uncompressed baseline (Eq. 2) ----------------------------------------------------------------
+def test_baseline_permute_unpermute(L):
+    cfg = small_cfg(n=1500, k=2, E=4, q=2, d=128, d_ffn=256)
+    case = make_case(L, cfg, seed=12, sanitize=False)
+    ex = experts_for(cfg, 12)
+    X = case.X.cuda()
+    n, k, E = 1500, 2, 4
+    send = torch.empty((n * k, 128), dtype=torch.bfloat16, device="cuda")
+    slot = torch.empty((n, k), dtype=torch.int32, device="cuda")
+    er = torch.empty(E, dtype=torch.int32, device="cuda")
+    ws = torch.empty(L.compress_workspace_bytes(n, k, E, 2, 128, torch.bfloat16), dtype=torch.uint8, device="cuda")
+    L.permute(X, case.zeta.cuda(), E, send, slot, er, ws)
+    rr = er.view(E, 1).clone()
+    eo = L.expert_ffn(send, rr, *stack_experts(ex, range(E), "cuda"))
+    y = torch.empty_like(X)
+    L.unpermute(eo, slot, y)
+    ref = O.moe_dense(f64(case.X), case.zeta.numpy(), oracle_experts(ex))
+    assert row_rel_err(f64(y), ref) <= 2e-2
+    grp = O.group_by_expert(case.zeta.numpy(), E)
+    assert np.array_equal(er.cpu().numpy(), [len(g) for g in grp])
+    flat = np.concatenate([np.array(g) for g in grp])
+    s = slot.cpu().numpy().reshape(-1)
+    assert np.array_equal(s[flat], np.arange(n * k))
