@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Benchmark of the LSH-MoE compressed expert-parallel layer (Alg. 1) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl lsh|reference]
+
+A step = one pass of the whole hot path over one batch per rank: hash (tcgen05) -> compress
+(bucket + centroid) -> dispatch (all-to-all of centroids) -> expert FFN -> combine -> restore.
+Workload per rank = BASELINE.json configs[1] (C2, RoBERTa-MoE-shaped, 16K tokens/GPU, bf16);
+weak scaling over N ranks (one process per GPU, experts partitioned across ranks).  Inputs are
+seeded synthetic (lshmoe_inputs).  L2 is flushed (256 MiB write) between timed steps, outside the
+timed events.  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (the tier's reference arm) on the same workload/metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer dispatch+combine tokens/s (LSH-compressed EP layer: hash, compress, all-to-all, expert FFN, all-to-all, restore)"
+UNIT = "tokens/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="C2")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--q", type=int, default=None, help="override the number of hash functions")
+    p.add_argument("--impl", default="lsh", choices=["lsh", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-uncompressed", action="store_true")
+    p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--profile", action="store_true", help="minimal run for ncu: warmup + steps eager, no extras")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained"), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the hash kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_hash_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Polls SM clock and throttle reasons via NVML during the timed region."""
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        N = self.N
+        names = {getattr(N, k): k for k in dir(N) if k.startswith("nvmlClocksEventReason") or k.startswith("nvmlClocksThrottleReason")}
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4,
+                "hw_power_brake_slowdown": 0x80}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, b in bits.items():
+                    if r & b:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------------
+def run_reference(args, cfg):
+    """The oracle (CPU, fp64, NumPy) as it stands, timed on the host cores: each step = Alg. 1 on a
+    bounded sample of rank 0's tokens of the same workload."""
+    import numpy as np
+    import torch
+
+    import oracle as O
+    from lshmoe_inputs import make_experts, make_rank_inputs, rotation_seed
+    X, zeta, _ = make_rank_inputs(cfg, args.seed, 0)
+    ex = make_experts(cfg, args.seed)
+    oex = {e: tuple(t.to(torch.float64).numpy() for t in v) for e, v in ex.items()}
+    R64 = O.to_stored(O.rotation(cfg.d, cfg.q, rotation_seed(args.seed), cfg.dtype), cfg.dtype)
+    X64 = X.to(torch.float64).numpy()
+    z = zeta.numpy()
+    sample = min(cfg.n, 2048)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.lsh_layer(X64[:sample], z[:sample], R64, oex, cfg.E, cfg.dtype)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    value = sample / (ms / 1e3)
+    cores = len(os.sched_getaffinity(0))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg, args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"Alg. 1 on the first {sample} of rank 0's {cfg.n} tokens per step (fp64 NumPy oracle, "
+                                       f"rotation generation excluded)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, world):
+    return {"workload": f"{cfg.name}: {cfg.note}", "tokens_per_gpu": cfg.n, "d_model": cfg.d, "experts": cfg.E,
+            "experts_per_gpu": cfg.E // world, "top_k": cfg.k, "hash_functions": cfg.q, "d_ffn": cfg.d_ffn,
+            "parallelism": f"ep{world}", "l2": "flushed between timed steps (256 MiB write, outside the events)"}
+
+
+def cpu_baseline(cfg, seed, X, zeta, ex):
+    import numpy as np
+    import torch
+
+    import oracle as O
+    from lshmoe_inputs import rotation_seed
+    R64 = O.to_stored(O.rotation(cfg.d, cfg.q, rotation_seed(seed), cfg.dtype), cfg.dtype)
+    oex = {e: tuple(t.to(torch.float64).numpy() for t in v) for e, v in ex.items()}
+    X64 = X.to(torch.float64).numpy()
+    z = zeta.numpy()
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.lsh_layer(X64, z, R64, oex, cfg.E, cfg.dtype)
+        reps += 1
+        if time.perf_counter() - t0 > 10.0 or reps >= 5:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": cfg.n / dt, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": f"{reps} full step(s) of rank 0 (all {cfg.n} tokens, Alg. 1 incl. expert FFN) in fp64 NumPy; "
+                      f"rotation generation excluded"}
+
+
+# ---------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    from lshmoe_inputs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.q:
+        cfg = cfg.with_(q=args.q)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, cfg)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_08446_b200 as L
+    from lshmoe_inputs import make_experts, make_rank_inputs, rotation_seed
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    assert cfg.E % world == 0, "experts must split evenly over ranks"
+    E_local = cfg.E // world
+    comm = L.Comm.from_process_group() if world > 1 else None
+
+    # ---- inputs (seeded synthetic, per rank) and buffers ----
+    X_cpu, zeta_cpu, _ = make_rank_inputs(cfg, args.seed, rank)
+    ex = make_experts(cfg, args.seed, range(rank * E_local, (rank + 1) * E_local))
+    W1, b1, W2, b2 = (torch.stack([ex[e][i] for e in sorted(ex)]).to(dev).contiguous() for i in range(4))
+    R = L.rotation(cfg.d, cfg.q, rotation_seed(args.seed), X_cpu.dtype).to(dev)
+    X = X_cpu.to(dev)
+    zeta = zeta_cpu.to(dev)
+    n, k, d = cfg.n, cfg.k, cfg.d
+    nk = n * k
+    codes = torch.empty((n, cfg.q), dtype=torch.int16, device=dev)
+    comp = L.alloc_compressed(n, k, cfg.E, d, X.dtype, dev)
+    ws = torch.empty(L.compress_workspace_bytes(n, k, cfg.E, cfg.q, d, X.dtype), dtype=torch.uint8, device=dev)
+    cap = nk * world
+    recv = comp.centroids if world == 1 else torch.empty((cap, d), dtype=X.dtype, device=dev)
+    rr = torch.empty((E_local, world), dtype=torch.int32, device=dev)
+    hid = torch.empty((cap, cfg.d_ffn), dtype=X.dtype, device=dev)
+    eo = torch.empty((cap, d), dtype=X.dtype, device=dev)
+    ret = eo if world == 1 else torch.empty((nk, d), dtype=X.dtype, device=dev)
+    y = torch.empty_like(X)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)     # 256 MiB > 126 MB L2
+    stream = torch.cuda.Stream(device=dev)          # non-default stream (graph capture needs one)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, zeta_cpu, X, zeta, R, codes, comp,
+                  ws, cap, recv, rr, hid, eo, ret, y, flush, stream, W1, b1, W2, b2, dist)
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.close()
+        dist.destroy_process_group()
+
+
+def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, zeta_cpu, X, zeta, R, codes, comp, ws,
+              cap, recv, rr, hid, eo, ret, y, flush, stream, W1, b1, W2, b2, dist):
+    import torch
+    from lshmoe_inputs import make_experts
+    n, k, d = cfg.n, cfg.k, cfg.d
+    nk = n * k
+
+    def stage_calls():
+        return [
+            lambda: L.hash(X, R, codes),
+            lambda: L.compress(X, codes, zeta, cfg.E, out=comp, workspace=ws),
+            lambda: L.dispatch(comm, comp.centroids, comp.expert_rows, cfg.E, recv, rr),
+            lambda: L.expert_ffn(recv, rr, W1, b1, W2, b2, out=eo, hidden=hid),
+            lambda: L.combine(comm, eo, comp.expert_rows, cfg.E, ret),
+            lambda: L.restore(X, comp.centroids, ret, comp.bucket, y=y),
+        ]
+
+    stages = stage_calls()
+    stage_names = ["hash", "compress", "dispatch", "expert_ffn", "combine", "restore"]
+
+    def step():
+        for f in stages:
+            f()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    L.check_device_error()
+
+    if args.profile:
+        for _ in range(args.steps):
+            flush.zero_()
+            step()
+        barrier()
+        return
+
+    # ---- per-stage breakdown (eager, CUDA events on the launching stream) ----
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(args.steps)]
+    barrier()
+    for s in range(args.steps):
+        flush.zero_()
+        ev[s][0].record(stream)
+        for i, f in enumerate(stages):
+            f()
+            ev[s][i + 1].record(stream)
+    barrier()
+    stage_ms = {nm: statistics.mean(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(args.steps))
+                for i, nm in enumerate(stage_names)}
+    eager_ms = statistics.mean(ev[s][0].elapsed_time(ev[s][-1]) for s in range(args.steps))
+    hash_ms = stage_ms["hash"]
+
+    # ---- headline: whole step, CUDA graph replay at world 1 (no host sync inside the step) ----
+    use_graph = world == 1 and not args.no_graph
+    run = step
+    if use_graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step()
+        run = g.replay
+        for _ in range(3):
+            run()
+    l0 = L.kernel_launches()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    with ClockSampler(local_rank) as clk:
+        for s in range(args.steps):
+            flush.zero_()
+            evs[s][0].record(stream)
+            run()
+            evs[s][1].record(stream)
+        barrier()
+    launches = L.kernel_launches() - l0
+    per_step = [a.elapsed_time(b) for a, b in evs]
+    ms = max_over_ranks(sum(per_step) / len(per_step))
+    if use_graph:   # kernels inside a replayed graph are not re-counted on the host
+        l1 = L.kernel_launches()
+        step()
+        torch.cuda.synchronize()
+        launches_per_step = L.kernel_launches() - l1
+    else:
+        launches_per_step = launches // args.steps
+    m = int(comp.num_rows.item())
+    ratio = m / nk
+
+    # ---- e2e: pinned host inputs -> device, the step, result -> host, all inside the events ----
+    X_h = X_cpu.pin_memory()
+    z_h = zeta_cpu.pin_memory()
+    y_h = torch.empty(y.shape, dtype=y.dtype).pin_memory()
+
+    def e2e_step():
+        X.copy_(X_h, non_blocking=True)
+        zeta.copy_(z_h, non_blocking=True)
+        step()
+        y_h.copy_(y, non_blocking=True)
+
+    e2e_run = e2e_step
+    if use_graph:
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=stream):
+            e2e_step()
+        e2e_run = g2.replay
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    for s in range(args.steps):
+        flush.zero_()
+        e2e_ev[s][0].record(stream)
+        e2e_run()
+        e2e_ev[s][1].record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in e2e_ev))
+    h2d = X_h.numel() * X_h.element_size() + z_h.numel() * z_h.element_size()
+    d2h = y_h.numel() * y_h.element_size()
+
+    # ---- context: uncompressed expert-parallel baseline on the same machinery ----
+    unc = None
+    if not args.no_uncompressed:
+        send = torch.empty((nk, d), dtype=X.dtype, device=dev)
+        slot = torch.empty((n, k), dtype=torch.int32, device=dev)
+        er = torch.empty(cfg.E, dtype=torch.int32, device=dev)
+        urecv = send if world == 1 else torch.empty((cap, d), dtype=X.dtype, device=dev)
+        uret = eo if world == 1 else torch.empty((nk, d), dtype=X.dtype, device=dev)
+        yb = torch.empty_like(X)
+
+        def base_step():
+            L.permute(X, zeta, cfg.E, send, slot, er, ws)
+            L.dispatch(comm, send, er, cfg.E, urecv, rr)
+            L.expert_ffn(urecv, rr, W1, b1, W2, b2, out=eo, hidden=hid)
+            L.combine(comm, eo, er, cfg.E, uret)
+            L.unpermute(uret, slot, yb)
+
+        for _ in range(3):
+            base_step()
+        brun = base_step
+        if use_graph:
+            g3 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g3, stream=stream):
+                base_step()
+            brun = g3.replay
+        bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        for s in range(args.steps):
+            flush.zero_()
+            bev[s][0].record(stream)
+            brun()
+            bev[s][1].record(stream)
+        barrier()
+        bms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in bev))
+        unc = {"ms_per_step": bms, "tokens_per_s": world * n / (bms / 1e3),
+               "what": "permute -> all-to-all of every routed token -> expert FFN on n*k rows -> all-to-all -> unpermute",
+               "speedup_of_lsh": bms / ms}
+
+    L.check_device_error()
+    pk = peaks()
+    flops = 2.0 * n * cfg.q * d * d
+    achieved = flops / (hash_ms / 1e3) / 1e12
+    roof = {"bound": "tensor", "kernel": "tc_gemm_kernel<ArgmaxEpi> (lshmoe_hash)", "achieved": achieved,
+            "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops"],
+            "traffic": ncu_traffic(),
+            "per_launch": {"flops": flops, "algorithmic_bytes": n * d * 2 + cfg.q * d * d * 2 + n * cfg.q * 2,
+                           "avg_ms": hash_ms},
+            "peak_source": pk["source"] + " bf16 dense (burst) — cuBLAS bf16 GEMM",
+            "frac_of_sustained": achieved / pk["bf16_tflops_sustained"] if pk.get("bf16_tflops_sustained") else None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.seed, X_cpu, zeta_cpu, make_experts(cfg, args.seed))
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": world * n / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32",
+                "data": "synthetic (seeded Zipf mixture tokens, linear top-k gate, random experts)",
+                "config": workload_config(cfg, world),
+                "compression_ratio": ratio, "centroids": m, "routed_copies": nk,
+                "gpu_launches": launches_per_step * args.steps, "gpu_launches_per_step": launches_per_step,
+                "cuda_graph": use_graph,
+                "stages_ms": stage_ms, "eager_ms_per_step": eager_ms,
+                "roofline": roof,
+                "e2e": {"value": world * n / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "clocks": clk.summary(),
+                "uncompressed_baseline": unc,
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -70,6 +70,9 @@ typedef struct lshmoe_comm lshmoe_comm;
 
 int lshmoe_abi_version(void);
 const char* lshmoe_last_error(void);
+/* Cumulative number of CUDA kernels this library has launched in this process (all threads);
+   the bench reports the per-step difference as "gpu_launches". */
+int64_t lshmoe_kernel_launches(void);
 
 /* Synchronises `stream`, reads and clears the device error word.  LSHMOE_EDEVICE if a kernel
    latched an error since the last check. */

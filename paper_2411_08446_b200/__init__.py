@@ -34,6 +34,7 @@ _vp, _i64, _i32, _u64, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctyp
 
 _SIGS = {
     "lshmoe_abi_version": ([], _i32),
+    "lshmoe_kernel_launches": ([], _i64),
     "lshmoe_last_error": ([], ctypes.c_char_p),
     "lshmoe_check_device_error": ([_vp], _i32),
     "lshmoe_rotation": ([_i32, _i32, _u64, _i32, _vp], _i32),
@@ -101,6 +102,11 @@ def _require_cuda(*ts):
 
 def abi_version() -> int:
     return _lib.lshmoe_abi_version()
+
+
+def kernel_launches() -> int:
+    """Cumulative count of kernels the library launched in this process."""
+    return _lib.lshmoe_kernel_launches()
 
 
 # ---- a1 --------------------------------------------------------------------------------------

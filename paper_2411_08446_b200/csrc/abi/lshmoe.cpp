@@ -2,6 +2,7 @@
 // sm_100a kernel launchers.  See include/lshmoe.h for the contract of every entry point.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -11,6 +12,9 @@
 namespace lshmoe {
 
 static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 lshmoe_status set_error(lshmoe_status st, const std::string& msg) {
   g_last_error = msg;
@@ -49,6 +53,8 @@ static lshmoe_status check_token_shape(const char* fn, lshmoe_dtype dtype, int64
 extern "C" {
 
 int lshmoe_abi_version(void) { return LSHMOE_ABI_VERSION; }
+
+int64_t lshmoe_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* lshmoe_last_error(void) { return g_last_error.c_str(); }
 

@@ -56,6 +56,7 @@ int launch_expert_ffn(const void* in, lshmoe_dtype dtype, int d, int d_ffn, cons
                       const void* b2, void* hidden, int64_t capacity, void* out, void* stream);
 
 int read_and_clear_device_error(int* value, void* stream);
+void count_launches(int n);   // kernels launched by this library (lshmoe_kernel_launches)
 int device_sm_count();
 
 }  // namespace lshmoe

@@ -262,6 +262,7 @@ void radix_pass(const RadixIO& io, int n, int shift, int32_t* hist, int32_t* exp
   radix_upsweep<KM><<<nb, kRT, 0, st>>>(io, n, shift, hist, nb);
   radix_scan<<<1, kRadix, 0, st>>>(hist, nb, expert_rows, num_rows, E);
   radix_downsweep<KM, OM><<<nb, kRT, 0, st>>>(io, n, shift, hist, nb);
+  count_launches(3);
 }
 
 // ---- centroid ---------------------------------------------------------------------------------
@@ -521,6 +522,7 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
   const uint32_t mask = static_cast<uint32_t>(ws.table_size - 1);
   insert_kernel<<<tgrid, 256, 0, st>>>(codes, q, experts, k, E, nk, ws.table, mask);
   lookup_kernel<<<tgrid, 256, 0, st>>>(codes, q, experts, k, E, nk, ws.table, mask, ws.rep, ws.keys[0]);
+  count_launches(2);
   // 3. firsts in (expert, position) order -> rowid, m_e, m
   RadixIO io{};
   io.E = E;
@@ -563,6 +565,7 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
     centroid_kernel<<<cgrid, 256, 0, st>>>(a);
     centroid_fixup_kernel<<<cgrid, 256, 0, st>>>(a);
   }
+  count_launches(2);
   return cudaGetLastError();
 }
 
@@ -585,6 +588,7 @@ int launch_permute(const void* x, lshmoe_dtype dtype, int64_t n, int d, const in
   const int grid = static_cast<int>(std::min<int64_t>((chunks + 255) / 256, 16 * device_sm_count()));
   gather_rows_kernel<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(x), row_bytes, k, ws.vals[1], nk,
                                            static_cast<uint8_t*>(send));
+  count_launches(1);
   return cudaGetLastError();
 }
 

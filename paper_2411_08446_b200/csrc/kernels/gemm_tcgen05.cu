@@ -361,6 +361,7 @@ int launch_tc(const CUtensorMap& a, const CUtensorMap& b, int K, const Sched& s,
     configured = true;
   }
   kern<<<grid, kThreads, Cfg<BN>::kSmem, st>>>(a, b, K, s, e);
+  count_launches(1);
   return cudaGetLastError();
 }
 

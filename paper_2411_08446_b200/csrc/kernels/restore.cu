@@ -115,6 +115,7 @@ int launch_restore(const void* x, const void* ct, const void* ret, lshmoe_dtype 
                                                                  static_cast<const float*>(ret), n, d, bucket, k, g,
                                                                  static_cast<float*>(y));
   }
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -129,6 +130,7 @@ int launch_unpermute(const void* ret, lshmoe_dtype dtype, int64_t n, int d, cons
     unpermute_kernel<float><<<grid_for(n * (d / 4)), 256, 0, st>>>(static_cast<const float*>(ret), n, d, slot, k, g,
                                                                    static_cast<float*>(y));
   }
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -138,6 +140,7 @@ int launch_local_exchange(const void* src, void* dst, int64_t capacity_rows, int
   const int grid = dst ? 8 * device_sm_count() : 1;
   local_exchange_kernel<<<grid, 256, 0, st>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), capacity_rows,
                                               row_bytes, counts, E, counts_out);
+  count_launches(1);
   return cudaGetLastError();
 }
 

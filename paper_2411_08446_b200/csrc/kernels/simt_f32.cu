@@ -94,6 +94,7 @@ int launch_hash_f32(const float* x, int64_t n, int d, const float* R, int q, int
   }
   dim3 grid(static_cast<unsigned>((n + kTok - 1) / kTok), q);
   hash_f32_kernel<<<grid, kTok, smem, static_cast<cudaStream_t>(stream)>>>(x, static_cast<int>(n), d, R, q, codes);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -117,6 +118,7 @@ int launch_expert_ffn(const void* in, lshmoe_dtype dtype, int d, int d_ffn, cons
   ffn_f32_layer_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(hidden), d_ffn, d, recv_rows, E_local, world,
                                             static_cast<const float*>(W2), static_cast<const float*>(b2),
                                             static_cast<float*>(out), capacity, 0);
+  count_launches(2);
   return cudaGetLastError();
 }
 
