@@ -228,7 +228,8 @@ def main():
     ws = torch.empty(L.compress_workspace_bytes(n, k, cfg.E, cfg.q, d, X.dtype), dtype=torch.uint8, device=dev)
     cap = nk * world
     recv = comp.centroids if world == 1 else torch.empty((cap, d), dtype=X.dtype, device=dev)
-    rr = torch.empty((E_local, world), dtype=torch.int32, device=dev)
+    # world 1: recv aliases the centroids and recv_rows [E, 1] aliases expert_rows (no copies)
+    rr = comp.expert_rows.view(cfg.E, 1) if world == 1 else torch.empty((E_local, world), dtype=torch.int32, device=dev)
     hid = torch.empty((cap, cfg.d_ffn), dtype=X.dtype, device=dev)
     eo = torch.empty((cap, d), dtype=X.dtype, device=dev)
     ret = eo if world == 1 else torch.empty((nk, d), dtype=X.dtype, device=dev)
@@ -309,6 +310,8 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 for i, nm in enumerate(stage_names)}
     eager_ms = statistics.mean(ev[s][0].elapsed_time(ev[s][-1]) for s in range(args.steps))
     hash_ms = stage_ms["hash"]
+    compress_phases = L.compress_phase_times(ws)   # last eager step, CTA 0's view (us)
+    compress_cta = L.compress_cta_times(ws)
 
     # ---- headline: whole step, CUDA graph replay at world 1 (no host sync inside the step) ----
     use_graph = world == 1 and not args.no_graph
@@ -381,14 +384,15 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
         send = torch.empty((nk, d), dtype=X.dtype, device=dev)
         slot = torch.empty((n, k), dtype=torch.int32, device=dev)
         er = torch.empty(cfg.E, dtype=torch.int32, device=dev)
+        brr = er.view(cfg.E, 1) if world == 1 else torch.empty((E_local, world), dtype=torch.int32, device=dev)
         urecv = send if world == 1 else torch.empty((cap, d), dtype=X.dtype, device=dev)
         uret = eo if world == 1 else torch.empty((nk, d), dtype=X.dtype, device=dev)
         yb = torch.empty_like(X)
 
         def base_step():
             L.permute(X, zeta, cfg.E, send, slot, er, ws)
-            L.dispatch(comm, send, er, cfg.E, urecv, rr)
-            L.expert_ffn(urecv, rr, W1, b1, W2, b2, out=eo, hidden=hid)
+            L.dispatch(comm, send, er, cfg.E, urecv, brr)
+            L.expert_ffn(urecv, brr, W1, b1, W2, b2, out=eo, hidden=hid)
             L.combine(comm, eo, er, cfg.E, uret)
             L.unpermute(uret, slot, yb)
 
@@ -439,6 +443,10 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 "gpu_launches": launches_per_step * args.steps, "gpu_launches_per_step": launches_per_step,
                 "cuda_graph": use_graph,
                 "stages_ms": stage_ms, "eager_ms_per_step": eager_ms,
+                "compress_phases_us": dict(zip(["insert", "firsts_hist", "firsts_scatter", "row_lo_hist",
+                                                "row_lo_scatter", "row_hi_hist", "row_hi_scatter", "centroid",
+                                                "fixup"], compress_phases)),
+                "compress_centroid_cta_us": compress_cta,
                 "roofline": roof,
                 "e2e": {"value": world * n / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},

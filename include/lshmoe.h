@@ -92,9 +92,15 @@ lshmoe_status lshmoe_rotation(int d, int q, uint64_t rotation_seed, lshmoe_dtype
    code_tj = sign(y_i*) * (i*+1), i* = argmax_i |y_i|, y = R_j x_t (reading R1); ties to the
    smallest i, a zero winner is '+' (reading R2).  bf16: tcgen05 tensor cores, bf16 x bf16
    products, fp32 accumulation; f32: SIMT fp32 FMA (reading R19).  Hashed once per token, shared
-   by its k routed copies (reading R6).  n == 0 is a no-op. */
+   by its k routed copies (reading R6).  n == 0 is a no-op.
+   workspace: device buffer of lshmoe_hash_workspace() bytes (0 for f32 or d <= 256: may be NULL).
+   It must be zero-filled before its first use and not written by anyone else afterwards: it holds
+   per-tile arrival counters that every call leaves at zero, plus scratch.  A caller allocates it
+   once (e.g. torch.zeros) and reuses it, on one stream at a time. */
+lshmoe_status lshmoe_hash_workspace(int64_t n, int d, int q, lshmoe_dtype dtype, size_t* bytes /* [host] */);
 lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d,
-                          const void* rotation, int q, int16_t* codes, lshmoe_stream stream);
+                          const void* rotation, int q, int16_t* codes,
+                          void* workspace, size_t workspace_bytes, lshmoe_stream stream);
 
 /* ---- a3-a5: group by expert, bucketize, centroid means -------------------------------------
    Bytes of device workspace lshmoe_compress needs for these sizes. */
@@ -141,7 +147,8 @@ lshmoe_status lshmoe_comm_last_counts(const lshmoe_comm* comm, int32_t* counts, 
    source).  world > 1: all-gathers the counts (ncclAllGather), synchronises `stream` once to
    read them, then one grouped ncclSend/ncclRecv all-to-all-v; checks the device error word.
    world == 1 (comm may be NULL): a device-side copy bounded by the device count (skipped when
-   recv == centroids); no host synchronisation.  recv_total [host] (nullable) receives the row
+   recv == centroids; the recv_rows copy is skipped when recv_rows == expert_rows, whose [E, 1]
+   layout is identical); no host synchronisation.  recv_total [host] (nullable) receives the row
    count at world > 1 (left untouched at world == 1). */
 lshmoe_status lshmoe_dispatch(lshmoe_comm* comm, const void* centroids, lshmoe_dtype dtype, int d,
                               const int32_t* expert_rows, int num_experts,

@@ -38,7 +38,8 @@ _SIGS = {
     "lshmoe_last_error": ([], ctypes.c_char_p),
     "lshmoe_check_device_error": ([_vp], _i32),
     "lshmoe_rotation": ([_i32, _i32, _u64, _i32, _vp], _i32),
-    "lshmoe_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp], _i32),
+    "lshmoe_hash_workspace": ([_i64, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
+    "lshmoe_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _sz, _vp], _i32),
     "lshmoe_compress_workspace": ([_i64, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
     "lshmoe_compress": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                          _vp, _sz, _vp], _i32),
@@ -118,7 +119,31 @@ def rotation(d: int, q: int, seed: int, dtype: torch.dtype = torch.bfloat16) -> 
 
 
 # ---- a2 --------------------------------------------------------------------------------------
-def hash(x: torch.Tensor, R: torch.Tensor, codes: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:  # noqa: A001
+def hash_workspace_bytes(n: int, d: int, q: int, dtype: torch.dtype) -> int:
+    b = ctypes.c_size_t(0)
+    _check(_lib.lshmoe_hash_workspace(n, d, q, F32 if dtype == torch.float32 else BF16, ctypes.byref(b)),
+           "lshmoe_hash_workspace")
+    return b.value
+
+
+_HASH_WS = {}
+
+
+def hash_workspace(n: int, d: int, q: int, dtype: torch.dtype, device) -> Optional[torch.Tensor]:
+    """A zero-filled hash workspace (kept zero-filled by the kernel), cached per device and size."""
+    nbytes = hash_workspace_bytes(n, d, q, dtype)
+    if nbytes == 0:
+        return None
+    key = (str(device), nbytes)
+    ws = _HASH_WS.get(key)
+    if ws is None:
+        ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        _HASH_WS[key] = ws
+    return ws
+
+
+def hash(x: torch.Tensor, R: torch.Tensor, codes: Optional[torch.Tensor] = None,  # noqa: A001
+         workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """Cross-polytope codes int16 [n, q] of x [n, d] under rotations R [q, d, d] (Eq. 3)."""
     _require_cuda(x, R)
     n, d = x.shape
@@ -127,7 +152,11 @@ def hash(x: torch.Tensor, R: torch.Tensor, codes: Optional[torch.Tensor] = None,
         raise ValueError("R must be [q, d, d] in x's dtype")
     if codes is None:
         codes = torch.empty((n, q), dtype=torch.int16, device=x.device)
-    _check(_lib.lshmoe_hash(_ptr(x), _dt(x), n, d, _ptr(R), q, _ptr(codes), _stream(stream)), "lshmoe_hash")
+    if workspace is None:
+        workspace = hash_workspace(n, d, q, x.dtype, x.device)
+    wsb = 0 if workspace is None else workspace.numel()
+    _check(_lib.lshmoe_hash(_ptr(x), _dt(x), n, d, _ptr(R), q, _ptr(codes), _ptr(workspace), wsb, _stream(stream)),
+           "lshmoe_hash")
     return codes
 
 
@@ -141,6 +170,33 @@ class Compressed:
     num_rows: torch.Tensor     # int32 [1]
     centroids: torch.Tensor    # dtype [n*k, d] (first m rows valid)
     centroids_f32: Optional[torch.Tensor]
+
+
+def compress_phase_times(workspace: torch.Tensor) -> list:
+    """Diagnostics: CTA 0's globaltimer stamps (ns) left in the workspace by the last compress:
+    start, then the exit of each grid barrier, then CTA 0's end.  Returns successive deltas (us)."""
+    raw = workspace[8:64].cpu().view(torch.int32).numpy().astype("int64") & 0xFFFFFFFF
+    out = []
+    for a, b in zip(raw[:-1], raw[1:]):
+        if b == 0xFFFFFFFF:
+            break
+        out.append(round(((int(b) - int(a)) & 0xFFFFFFFF) / 1e3, 2))
+    return out
+
+
+def compress_cta_times(workspace: torch.Tensor) -> dict:
+    """Diagnostics: per-CTA centroid-phase durations (us) from the last compress."""
+    raw = workspace[256:256 + 8192].cpu().view(torch.int32).numpy().astype("int64") & 0xFFFFFFFF
+    st, en = raw[0::2], raw[1::2]
+    ok = (st != 0xFFFFFFFF) & (en != 0xFFFFFFFF)
+    if not ok.any():
+        return {}
+    st, en = st[ok], en[ok]
+    dur = ((en - st) & 0xFFFFFFFF) / 1e3
+    t0 = st.min()
+    return {"ctas": int(ok.sum()), "dur_min": float(dur.min()), "dur_med": float(sorted(dur)[len(dur) // 2]),
+            "dur_max": float(dur.max()), "start_spread": float((st.max() - t0) / 1e3),
+            "end_max": float((en.max() - t0) / 1e3)}
 
 
 def compress_workspace_bytes(n: int, k: int, E: int, q: int, d: int, dtype: torch.dtype) -> int:

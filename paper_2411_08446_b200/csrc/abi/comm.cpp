@@ -108,9 +108,10 @@ lshmoe_status lshmoe_dispatch(lshmoe_comm* c, const void* centroids, lshmoe_dtyp
   if (!centroids || !expert_rows || !recv || !recv_rows) return set_error(LSHMOE_EINVAL, "lshmoe_dispatch: NULL pointer");
   const size_t row_bytes = static_cast<size_t>(d) * (dtype == LSHMOE_F32 ? 4 : 2);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (world == 1) {
+  if (world == 1) {   // recv_rows [E, 1] == expert_rows: alias it to skip the copy
     int err = launch_local_exchange(centroids, recv == centroids ? nullptr : recv, recv_capacity,
-                                    static_cast<int>(row_bytes), expert_rows, E, recv_rows, stream);
+                                    static_cast<int>(row_bytes), expert_rows, E,
+                                    recv_rows == expert_rows ? nullptr : recv_rows, stream);
     return cuda_status(err, "lshmoe_dispatch (local)");
   }
   lshmoe_status st = ensure_capacity(c, E);

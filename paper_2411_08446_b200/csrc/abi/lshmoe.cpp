@@ -75,8 +75,15 @@ lshmoe_status lshmoe_rotation(int d, int q, uint64_t seed, lshmoe_dtype dtype, v
   return rotation_host(d, q, seed, dtype, out);
 }
 
+lshmoe_status lshmoe_hash_workspace(int64_t n, int d, int q, lshmoe_dtype dtype, size_t* bytes) {
+  REQUIRE(bytes != nullptr, LSHMOE_EINVAL, "bytes is NULL");
+  REQUIRE(n >= 0 && d >= 1 && q >= 1, LSHMOE_EINVAL, "bad sizes");
+  *bytes = dtype == LSHMOE_BF16 ? hash_workspace_bytes(n, d, q) : 0;
+  return LSHMOE_OK;
+}
+
 lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, const void* rotation, int q,
-                          int16_t* codes, lshmoe_stream stream) {
+                          int16_t* codes, void* workspace, size_t workspace_bytes, lshmoe_stream stream) {
   lshmoe_status st = check_token_shape(__func__, dtype, n, d);
   if (st) return st;
   REQUIRE(q >= 1, LSHMOE_EINVAL, "q < 1");
@@ -89,7 +96,10 @@ lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, c
     REQUIRE(d <= 384, LSHMOE_EUNSUPPORTED, "f32 (SIMT) hash supports d <= 384");
     err = launch_hash_f32(static_cast<const float*>(x), n, d, static_cast<const float*>(rotation), q, codes, stream);
   } else {
-    err = launch_hash_bf16(x, n, d, rotation, q, codes, stream);
+    const size_t need = hash_workspace_bytes(n, d, q);
+    REQUIRE(workspace_bytes >= need, LSHMOE_EINVAL, "workspace too small (see lshmoe_hash_workspace)");
+    REQUIRE(need == 0 || (workspace && aligned16(workspace)), LSHMOE_EINVAL, "workspace NULL or misaligned");
+    err = launch_hash_bf16(x, n, d, rotation, q, codes, workspace, stream);
   }
   return cuda_status(err, "lshmoe_hash");
 }

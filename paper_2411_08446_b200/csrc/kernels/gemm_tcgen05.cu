@@ -1,6 +1,8 @@
 // tcgen05 tensor-core kernels (sm_100a): one warp-specialised, persistent TN-GEMM mainloop
-// (TMA -> shared memory ring -> single-thread tcgen05.mma -> double-buffered TMEM accumulator)
-// with two epilogues:
+// (TMA -> shared-memory ring -> single-thread tcgen05.mma -> double-buffered TMEM accumulator),
+// either per CTA (cta_group::1, M = 128) or per CTA pair (cluster of 2, cta_group::2, M = 256: each
+// CTA stages its 128 A rows and half of the B tile, so per-SM shared-memory traffic per MMA drops
+// from 12 KB to 8 KB), with two epilogues:
 //
 //  * ArgmaxEpi — a2, the cross-polytope hash of Eq. 3.  Y = X R_j^T is a
 //    dense contraction [n, d] x [d, d] per hash j; each 128-token x BN-coordinate accumulator tile
@@ -11,11 +13,12 @@
 //  * BiasActEpi — a7, the expert FFN E(x) = W2 relu(W1 x + b1) + b2 as two grouped GEMMs
 //    over the received centroid rows, segmented per local expert by a device-side tile table.
 //
-// Roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer, warps 2-5 =
-// epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).
+// Roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (leader CTA),
+// warps 2-5 = epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "../abi/lshmoe_internal.h"
@@ -27,44 +30,68 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BM = 128;
+constexpr int BM = 128;                     // rows per CTA
 constexpr int BK = 64;                      // 64 bf16 = 128 B = one SWIZZLE_128B row
-constexpr int kThreads = 192;
-constexpr int kEpiWarp0 = 2;
+constexpr int kEpiWarps = 8;                // two warps per TMEM lane quadrant, each takes half the columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kEpiScratch = 1024;           // per epilogue warp (bias slice)
 
-template <int BN>
+template <int BN, int kCta>
 struct Cfg {
+  static constexpr int kBRows = BN / kCta;  // B rows staged by each CTA
   static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (196 * 1024) / kStageBytes > 8 ? 8 : (196 * 1024) / kStageBytes;
+  static constexpr int kTxBytes = kCta * kStageBytes;   // bytes the leader's full barrier waits for
+  static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + kEpiWarps * kEpiScratch;
 };
 
 struct WorkItem {
-  int a_row;       // first A row (token / centroid row) of the 128-row tile
-  int b_row0;      // first B row (rotation / weight row) of chunk 0
-  int nchunks;     // accumulator chunks of BN columns (hash: d / BN; FFN: 1)
-  int valid_rows;  // rows of the tile that are real outputs
-  int tag0, tag1;  // epilogue-specific (hash: m tile, j; FFN: expert, n0)
+  int a_row;       // first A row of this CTA's 128-row slice
+  int b_row0;      // first B row of chunk 0 (cluster tile; a CTA adds rank * BN / kCta)
+  int nchunks;     // accumulator chunks of BN columns in this unit
+  int valid_rows;  // rows of this CTA's slice that are real outputs (may be <= 0)
+  int tag0, tag1;  // epilogue-specific (hash: (m tile, j) id, j; FFN: expert, n0)
+  int part, nparts;  // hash: which BN-column slice of the d coordinates this unit covers
 };
 
-// ---- schedulers --------------------------------------------------------------------------------
+// ---- schedulers (units are per cluster; bm = 128 * kCta rows per unit) ----------------------
+// Hash units are (token tile, hash j, BN-column slice): d / BN times more units than (tile, j),
+// so the persistent grid's last wave is nearly full (C2: 2304 units over 148 SMs instead of 768).
+// The slices of one (tile, j) are merged by the last one to finish (ArgmaxEpi::finish).
 struct HashSched {
-  int n, q, d, bn;
+  int n, q, d, bn, bm;
   int m_tiles;
   __device__ void init(void*) {}
-  __device__ int units() const { return m_tiles * q; }
-  __device__ WorkItem get(int u) const {
+  int split;   // 1: one unit per BN slice; 0: one unit covers all d / BN slices (no merge)
+  __device__ int units() const { return m_tiles * q * (split ? d / bn : 1); }
+  __device__ WorkItem get(int u, int rank) const {
     WorkItem w;
-    const int mt = u / q, j = u - mt * q;      // j fastest: the q units of one token tile run together
-    w.a_row = mt * BM;
-    w.b_row0 = j * d;
-    w.nchunks = d / bn;
-    w.valid_rows = min(BM, n - mt * BM);
-    w.tag0 = mt;
+    if (!split) {
+      const int mt = u / q, j = u - mt * q;
+      w.a_row = mt * bm + rank * BM;
+      w.b_row0 = j * d;
+      w.nchunks = d / bn;
+      w.valid_rows = min(BM, n - w.a_row);
+      w.tag0 = (mt * (bm / BM) + rank) * q + j;
+      w.tag1 = j;
+      w.part = 0;
+      w.nparts = 1;
+      return w;
+    }
+    const int np = d / bn;
+    const int c = u % np, rest = u / np;       // slice fastest, then j: one token tile at a time
+    const int j = rest % q, mt = rest / q;
+    w.a_row = mt * bm + rank * BM;
+    w.b_row0 = j * d + c * bn;
+    w.nchunks = 1;
+    w.valid_rows = min(BM, n - w.a_row);
+    w.tag0 = (mt * (bm / BM) + rank) * q + j;   // this CTA's 128-token slice x hash j
     w.tag1 = j;
+    w.part = c;
+    w.nparts = np;
     return w;
   }
 };
@@ -73,10 +100,9 @@ constexpr int kMaxLocalExperts = 256;
 
 struct FfnSched {
   const int32_t* recv_rows;  // [E_local, world]
-  int E_local, world, N, bn;
-  // smem tables, filled by init()
-  int* seg_start;   // [E_local + 1]
-  int* tiles_pre;   // [E_local + 1]
+  int E_local, world, N, bn, bm;
+  int* seg_start;   // smem [E_local + 1]
+  int* tiles_pre;   // smem [E_local + 1]
   __device__ void init(void* smem) {
     seg_start = reinterpret_cast<int*>(smem);
     tiles_pre = seg_start + (kMaxLocalExperts + 1);
@@ -89,7 +115,7 @@ struct FfnSched {
         int r = 0;
         for (int s = 0; s < world; ++s) r += recv_rows[e * world + s];
         rows += r;
-        tiles += ((r + BM - 1) / BM) * ntn;
+        tiles += ((r + bm - 1) / bm) * ntn;
       }
       seg_start[E_local] = rows;
       tiles_pre[E_local] = tiles;
@@ -97,72 +123,159 @@ struct FfnSched {
     __syncthreads();
   }
   __device__ int units() const { return tiles_pre[E_local]; }
-  __device__ WorkItem get(int u) const {
+  __device__ WorkItem get(int u, int rank) const {
     int e = 0;
     while (tiles_pre[e + 1] <= u) ++e;
     const int ntn = N / bn;
     const int local = u - tiles_pre[e];
     const int mt = local / ntn, nt = local - mt * ntn;
     WorkItem w;
-    w.a_row = seg_start[e] + mt * BM;
+    w.a_row = seg_start[e] + mt * bm + rank * BM;
     w.b_row0 = e * N + nt * bn;
     w.nchunks = 1;
     w.valid_rows = min(BM, seg_start[e + 1] - w.a_row);
     w.tag0 = e;
     w.tag1 = nt * bn;
+    w.part = 0;
+    w.nparts = 1;
     return w;
   }
 };
 
-// ---- epilogues ---------------------------------------------------------------------------------
+// ---- epilogues -------------------------------------------------------------------------------
 struct ArgmaxEpi {
   int16_t* codes;
   int q;
+  uint2* partial;     // [nparts][rows_pad][q] (|y| bits, index | sign << 31) of each slice
+  int* counter;       // [slices][q] arrival counters, zero at rest (reset by the last arrival)
+  int rows_pad;
+  // four independent running winners (column i goes to chain i % 4) keep the dependent
+  // compare/select chain short; merged by (larger |y|, then smaller index) at the end, which is
+  // exactly the first maximum of one ascending scan.
+  float cb[4];
+  int ci[4];
   float best;
   int bidx;
   bool bneg;
-  __device__ void begin(const WorkItem&) {
-    best = -1.0f;
-    bidx = 0;
-    bneg = false;
+  __device__ void begin(const WorkItem&, uint8_t*) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      cb[k] = -1.0f;
+      ci[k] = 0;
+    }
   }
-  __device__ void chunk_begin(const WorkItem&, int) {}
-  __device__ void consume(const WorkItem&, int /*row*/, const uint32_t (&r)[32], int col0) {
+  __device__ void merge_chains() {
+    best = cb[0];
+    bidx = ci[0];
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+      const int ik = ci[k] & 0x7FFFFFFF, ib = bidx & 0x7FFFFFFF;
+      if (cb[k] > best || (cb[k] == best && ik < ib)) {
+        best = cb[k];
+        bidx = ci[k];
+      }
+    }
+    bneg = (bidx & 0x80000000) != 0;
+    bidx &= 0x7FFFFFFF;
+  }
+  // Slice merge: every slice stores its per-row winner; the last slice of (tile, j) to arrive
+  // merges the nparts winners in slice order (strict '>': an earlier slice keeps ties, so the
+  // result equals one ascending scan over all d coordinates) and writes the code.
+  __device__ void finish_split(const WorkItem& w, int row, uint8_t* shared_flag, int half, int nthr) {
+    const int t = w.a_row + row;
+    if (half == 0 && t >= 0 && t < rows_pad)
+      partial[(static_cast<int64_t>(w.part) * rows_pad + t) * q + w.tag1] =
+          make_uint2(__float_as_uint(best), static_cast<uint32_t>(bidx) | (bneg ? 0x80000000u : 0u));
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");   // all epilogue warps
+    int* flag = reinterpret_cast<int*>(shared_flag);
+    if (threadIdx.x == 64) {                                // first epilogue thread
+      // acq_rel: releases this CTA's winners (ordered before by bar.sync), acquires the others'
+      int old;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(counter + w.tag0) : "memory");
+      const int last = old == w.nparts - 1;
+      if (last) counter[w.tag0] = 0;                        // leave the workspace zeroed
+      *flag = last;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    const int last = *reinterpret_cast<volatile int*>(flag);
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");   // flag consumed before it is reused
+    if (!last || half != 0 || row >= w.valid_rows) return;
+    float b = -1.0f;
+    uint32_t bi = 0;
+    for (int p = 0; p < w.nparts; ++p) {
+      const uint2 v = __ldcg(partial + (static_cast<int64_t>(p) * rows_pad + t) * q + w.tag1);
+      const float a = __uint_as_float(v.x);
+      if (a > b) {
+        b = a;
+        bi = v.y;
+      }
+    }
+    const int idx = static_cast<int>(bi & 0x7FFFFFFFu);
+    codes[static_cast<int64_t>(t) * q + w.tag1] = static_cast<int16_t>((bi >> 31) ? -(idx + 1) : (idx + 1));
+  }
+  __device__ void consume(const WorkItem&, int /*row*/, const uint32_t (&r)[32], int col0, const uint8_t*) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const float v = __uint_as_float(r[i]);
       const float a = fabsf(v);
-      if (a > best) {           // strict: equal magnitudes keep the smaller (earlier) index
-        best = a;
-        bidx = col0 + i;
-        bneg = v < 0.0f;        // -0.0f is not < 0: a zero winner is '+'
+      const int k = i & 3;
+      if (a > cb[k]) {          // strict: equal magnitudes keep the smaller (earlier) index
+        cb[k] = a;
+        // index | sign bit; -0.0f is not < 0, so a zero winner is '+'
+        ci[k] = (col0 + i) | (v < 0.0f ? static_cast<int>(0x80000000u) : 0);
       }
     }
   }
-  __device__ void finish(const WorkItem& w, int row) {
-    if (row < w.valid_rows) {
+  // half: which half of the unit's columns this thread scanned (8 epilogue warps) or 0.
+  __device__ void finish(const WorkItem& w, int row, uint8_t* scratch, int half, int nthr) {
+    merge_chains();
+    if (nthr > 128) {   // combine the two column halves of each row; the lower half wins ties
+      uint2* mb = reinterpret_cast<uint2*>(scratch + 64);
+      if (half == 1) mb[row] = make_uint2(__float_as_uint(best), static_cast<uint32_t>(bidx) | (bneg ? 0x80000000u : 0u));
+      asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+      if (half == 0) {
+        const uint2 o = mb[row];
+        if (__uint_as_float(o.x) > best) {
+          best = __uint_as_float(o.x);
+          bidx = static_cast<int>(o.y & 0x7FFFFFFFu);
+          bneg = (o.y >> 31) != 0;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    }
+    if (w.nparts > 1) {
+      finish_split(w, row, scratch, half, nthr);
+      return;
+    }
+    if (half == 0 && row < w.valid_rows) {
       const int t = w.a_row + row;
       codes[static_cast<int64_t>(t) * q + w.tag1] = static_cast<int16_t>(bneg ? -(bidx + 1) : (bidx + 1));
     }
   }
 };
 
+template <int BN>
 struct BiasActEpi {
   const __nv_bfloat16* bias;  // [E_local, N]
   __nv_bfloat16* out;         // [rows, N]
   int N;
   bool relu;
-  __device__ void begin(const WorkItem&) {}
-  __device__ void chunk_begin(const WorkItem&, int) {}
-  __device__ void consume(const WorkItem& w, int row, const uint32_t (&r)[32], int col0) {
+  // the unit's BN bias values are staged once per warp in shared memory (broadcast reads)
+  __device__ void begin(const WorkItem& w, uint8_t* scratch) {
+    const int lane = threadIdx.x % 32;
+    const uint4* src = reinterpret_cast<const uint4*>(bias + static_cast<int64_t>(w.tag0) * N + w.tag1);
+    for (int i = lane; i < BN / 8; i += 32) reinterpret_cast<uint4*>(scratch)[i] = src[i];
+    __syncwarp();
+  }
+  __device__ void consume(const WorkItem& w, int row, const uint32_t (&r)[32], int col0, const uint8_t* scratch) {
     if (row >= w.valid_rows) return;
-    const int n0 = w.tag1 + col0;
-    const __nv_bfloat16* b = bias + static_cast<int64_t>(w.tag0) * N + n0;
+    const uint32_t* bw = reinterpret_cast<const uint32_t*>(scratch) + col0 / 2;
     uint32_t packed[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      float v0 = __uint_as_float(r[2 * i]) + __bfloat162float(b[2 * i]);
-      float v1 = __uint_as_float(r[2 * i + 1]) + __bfloat162float(b[2 * i + 1]);
+      const uint32_t b2 = bw[i];
+      float v0 = __uint_as_float(r[2 * i]) + __uint_as_float(b2 << 16);
+      float v1 = __uint_as_float(r[2 * i + 1]) + __uint_as_float(b2 & 0xFFFF0000u);
       if (relu) {
         v0 = fmaxf(v0, 0.0f);
         v1 = fmaxf(v1, 0.0f);
@@ -170,19 +283,19 @@ struct BiasActEpi {
       __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
       packed[i] = *reinterpret_cast<uint32_t*>(&h);
     }
-    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<int64_t>(w.a_row + row) * N + n0);
+    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<int64_t>(w.a_row + row) * N + w.tag1 + col0);
 #pragma unroll
     for (int i = 0; i < 4; ++i) dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
   }
-  __device__ void finish(const WorkItem&, int) {}
+  __device__ void finish(const WorkItem&, int, uint8_t*, int, int) {}
 };
 
-// ---- the kernel --------------------------------------------------------------------------------
-template <int BN, class Sched, class Epi>
+// ---- the kernel ----------------------------------------------------------------------------------
+template <int BN, int kCta, class Sched, class Epi>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                    Sched sched, Epi epi) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, kCta>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -192,11 +305,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* epi_scratch = smem + C::kStages * C::kStageBytes + 256;
   __shared__ int sched_tables[2 * (kMaxLocalExperts + 1)];
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int kblocks = K / BK;
+  const int rank = kCta == 2 ? static_cast<int>(cluster_ctarank()) : 0;
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x / kCta;
+  const int nclusters = gridDim.x / kCta;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -205,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], kEpiWarps * kCta);
     }
     fence_mbarrier_init();
   }
@@ -213,27 +331,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if (kCta == 2) tmem_alloc_2cta<C::kTmemCols>(tmem_slot);
+    else tmem_alloc<C::kTmemCols>(tmem_slot);
+  }
   sched.init(sched_tables);   // contains __syncthreads
   tc_fence_before();
-  __syncthreads();
+  if (kCta == 2) cluster_sync();   // peer barriers initialised before any remote arrive / TMA
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int units = sched.units();
 
   if (warp == 0) {
-    // ===== TMA producer =====
+    // ===== TMA producer (every CTA loads its A slice and its half of B) =====
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const WorkItem w = sched.get(u);
+      for (int u = cluster; u < units; u += nclusters) {
+        const WorkItem w = sched.get(u, rank);
         for (int c = 0; c < w.nchunks; ++c) {
+          const int brow = w.b_row0 + c * BN + rank * C::kBRows;
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-            tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, w.a_row);
-            tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, w.b_row0 + c * BN);
+            if (kCta == 2) {
+              if (leader) mbar_arrive_expect_tx(&full[stage], C::kTxBytes);
+              tma_load_2d_2sm(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, w.a_row);
+              tma_load_2d_2sm(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, brow);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], C::kTxBytes);
+              tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, w.a_row);
+              tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, brow);
+            }
             if (++stage == C::kStages) {
               stage = 0;
               phase ^= 1;
@@ -244,15 +373,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ===== MMA issuer (one thread) =====
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+    // ===== MMA issuer (one thread of the leader CTA) =====
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM * kCta, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const WorkItem w = sched.get(u);
+      for (int u = cluster; u < units; u += nclusters) {
+        const WorkItem w = sched.get(u, rank);
         for (int c = 0; c < w.nchunks; ++c) {
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
@@ -264,16 +393,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t b0 = smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
-              mma_bf16_ss(d_tmem, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), idesc,
-                          (kb | kk) != 0);
+              if (kCta == 2)
+                mma_bf16_ss_2cta(d_tmem, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), idesc,
+                                 (kb | kk) != 0);
+              else
+                mma_bf16_ss(d_tmem, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), idesc,
+                            (kb | kk) != 0);
             }
-            mma_commit(&empty[stage]);          // frees the smem slot when these MMAs finish
+            if (kCta == 2) mma_commit_2cta_mc(&empty[stage], 0x3);   // frees the slot in both CTAs
+            else mma_commit(&empty[stage]);
             if (++stage == C::kStages) {
               stage = 0;
               phase ^= 1;
             }
           }
-          mma_commit(&tfull[acc]);              // accumulator ready for the epilogue
+          if (kCta == 2) mma_commit_2cta_mc(&tfull[acc], 0x3);      // both epilogues may read
+          else mma_commit(&tfull[acc]);
           acc ^= 1;
           if (acc == 0) acc_phase ^= 1;
         }
@@ -282,39 +417,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ===== epilogue warps =====
-    const int quad = warp % 4;
+    const int quad = warp % 4;                      // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) / 4;                // which half of the BN columns it drains
+    constexpr int kBlkPer = (BN / 32) * 4 / kEpiWarps;
     const int row = quad * 32 + lane;
+    uint8_t* scratch = epi_scratch + (warp - 2) * kEpiScratch;
+    const uint32_t tempty_leader0 = kCta == 2 ? mapa_shared(&tempty[0], 0) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const WorkItem w = sched.get(u);
-      epi.begin(w);
+    for (int u = cluster; u < units; u += nclusters) {
+      const WorkItem w = sched.get(u, rank);
+      epi.begin(w, scratch);
       for (int c = 0; c < w.nchunks; ++c) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        epi.chunk_begin(w, c);
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN;
 #pragma unroll 1
-        for (int cb = 0; cb < BN / 32; ++cb) {
+        for (int cb = half * kBlkPer; cb < (half + 1) * kBlkPer; ++cb) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + cb * 32, r);
           tmem_ld_wait();
-          epi.consume(w, row, r, c * BN + cb * 32);
+          epi.consume(w, row, r, (w.part + c) * BN + cb * 32, scratch);   // column within the unit's N range
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if (kCta == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+          else mbar_arrive(&tempty[acc]);
+        }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
-      epi.finish(w, row);
+      epi.finish(w, row, epi_scratch, half, 32 * kEpiWarps);
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (kCta == 2) cluster_sync();   // the pair's MMAs / remote arrivals are done before TMEM is freed
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tmem_base);
+    if (kCta == 2) tmem_dealloc_2cta<C::kTmemCols>(tmem_base);
+    else tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 
@@ -350,37 +493,69 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int b
   return r == CUDA_SUCCESS ? 0 : cudaErrorInvalidValue;
 }
 
-template <int BN, class Sched, class Epi>
+template <int BN, int kCta, class Sched, class Epi>
 int launch_tc(const CUtensorMap& a, const CUtensorMap& b, int K, const Sched& s, const Epi& e, int grid,
               cudaStream_t st) {
-  auto kern = tc_gemm_kernel<BN, Sched, Epi>;
+  auto kern = tc_gemm_kernel<BN, kCta, Sched, Epi>;
   static bool configured = false;     // one attribute call per instantiation
   if (!configured) {
-    int err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmem);
+    int err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, kCta>::kSmem);
     if (err) return err;
     configured = true;
   }
-  kern<<<grid, kThreads, Cfg<BN>::kSmem, st>>>(a, b, K, s, e);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg<BN, kCta>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int err = cudaLaunchKernelEx(&cfg, kern, a, b, K, s, e);
   count_launches(1);
-  return cudaGetLastError();
+  return err ? err : cudaGetLastError();
 }
 
 int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64); }
 
+// kCta = 2 needs BN / 2 rows per CTA to stay a multiple of 8 (SW128 atoms) and N >= 16 per CTA.
 template <class Sched, class Epi>
-int launch_bn(int bn, const void* A, int64_t a_rows, const void* B, int64_t b_rows, int K, Sched s, Epi e, int grid,
-              cudaStream_t st) {
+int launch_bn(int bn, int cta, const void* A, int64_t a_rows, const void* B, int64_t b_rows, int K, Sched s, Epi e,
+              int units_hint, cudaStream_t st) {
   CUtensorMap ma, mb;
   int err = make_map(&ma, A, a_rows, K, BM);
   if (err) return err;
-  err = make_map(&mb, B, b_rows, K, bn);
+  err = make_map(&mb, B, b_rows, K, bn / cta);
   if (err) return err;
   s.bn = bn;
-  switch (bn) {
-    case 256: return launch_tc<256>(ma, mb, K, s, e, grid, st);
-    case 128: return launch_tc<128>(ma, mb, K, s, e, grid, st);
-    default: return launch_tc<64>(ma, mb, K, s, e, grid, st);
+  s.bm = BM * cta;
+  const int sms = device_sm_count();
+  int clusters = sms / cta;
+  if (units_hint > 0 && units_hint < clusters) clusters = units_hint;
+  const int grid = clusters * cta;
+  if (cta == 2) {
+    switch (bn) {
+      case 256: return launch_tc<256, 2>(ma, mb, K, s, e, grid, st);
+      case 128: return launch_tc<128, 2>(ma, mb, K, s, e, grid, st);
+      default: return launch_tc<64, 2>(ma, mb, K, s, e, grid, st);
+    }
   }
+  switch (bn) {
+    case 256: return launch_tc<256, 1>(ma, mb, K, s, e, grid, st);
+    case 128: return launch_tc<128, 1>(ma, mb, K, s, e, grid, st);
+    default: return launch_tc<64, 1>(ma, mb, K, s, e, grid, st);
+  }
+}
+
+// MMA width per GEMM: 1 = one CTA (M = 128), 2 = CTA pair (M = 256); overridable for experiments.
+int cta_mode(const char* env_name, int dflt) {
+  const char* env = getenv(env_name);
+  if (env && (env[0] == '1' || env[0] == '2')) return env[0] - '0';
+  return dflt;
 }
 
 }  // namespace
@@ -396,18 +571,38 @@ int device_sm_count() {
   return sms;
 }
 
-int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int16_t* codes, void* stream) {
-  HashSched s;
+// Hash workspace: arrival counters [ceil(n/256)*2][q] int32 (zero at rest) + slice winners
+// [d/BN][rows_pad][q] uint2.  Only needed when d > BN (more than one slice per (tile, j)).
+size_t hash_workspace_bytes(int64_t n, int d, int q) {
+  const int bn = pick_bn(d);
+  if (d <= bn) return 0;
+  const int64_t rows_pad = ((n + 255) / 256) * 256;
+  const size_t counters = ((sizeof(int) * (rows_pad / BM) * q) + 255) & ~size_t(255);
+  return counters + sizeof(uint2) * static_cast<size_t>(d / bn) * rows_pad * q;
+}
+
+int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int16_t* codes, void* ws, void* stream) {
+  const int cta = cta_mode("LSHMOE_HASH_CTA", 1);
+  HashSched s{};
   s.n = static_cast<int>(n);
   s.q = q;
   s.d = d;
-  s.m_tiles = static_cast<int>((n + BM - 1) / BM);
-  ArgmaxEpi e;
+  s.m_tiles = static_cast<int>((n + BM * cta - 1) / (BM * cta));
+  const int bn = pick_bn(d);
+  ArgmaxEpi e{};
   e.codes = codes;
   e.q = q;
-  const int units = s.m_tiles * q;
-  const int grid = units < device_sm_count() ? units : device_sm_count();
-  return launch_bn(pick_bn(d), x, n, R, static_cast<int64_t>(q) * d, d, s, e, grid, static_cast<cudaStream_t>(stream));
+  e.rows_pad = static_cast<int>(((n + 255) / 256) * 256);
+  // Slice split (LSHMOE_HASH_SPLIT=1) evens out the last wave but measured slower on B200 (C2: 94 vs
+  // 88 us, scripts/ab_bench.py): off by default.
+  s.split = (d > bn) && ws && cta_mode("LSHMOE_HASH_SPLIT", 2) == 1 ? 1 : 0;
+  if (s.split) {
+    const size_t counters = ((sizeof(int) * (e.rows_pad / BM) * q) + 255) & ~size_t(255);
+    e.counter = static_cast<int*>(ws);
+    e.partial = reinterpret_cast<uint2*>(static_cast<uint8_t*>(ws) + counters);
+  }
+  return launch_bn(bn, cta, x, n, R, static_cast<int64_t>(q) * d, d, s, e, s.m_tiles * q * (s.split ? d / bn : 1),
+                   static_cast<cudaStream_t>(stream));
 }
 
 int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, int E_local, int world,
@@ -415,14 +610,32 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
                     void* out, void* stream) {
   if (E_local > kMaxLocalExperts) return cudaErrorInvalidValue;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int grid = device_sm_count();
-  FfnSched s1{recv_rows, E_local, world, d_ffn, 0, nullptr, nullptr};
-  BiasActEpi e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true};
-  int err = launch_bn(pick_bn(d_ffn), in, capacity, W1, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, grid, st);
+  const int cta = cta_mode("LSHMOE_FFN_CTA", 2);
+  FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, nullptr, nullptr};
+  const int bn1 = pick_bn(d_ffn);
+  int err;
+  if (bn1 == 256) {
+    BiasActEpi<256> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true};
+    err = launch_bn(bn1, cta, in, capacity, W1, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
+  } else if (bn1 == 128) {
+    BiasActEpi<128> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true};
+    err = launch_bn(bn1, cta, in, capacity, W1, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
+  } else {
+    BiasActEpi<64> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true};
+    err = launch_bn(bn1, cta, in, capacity, W1, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
+  }
   if (err) return err;
-  FfnSched s2{recv_rows, E_local, world, d, 0, nullptr, nullptr};
-  BiasActEpi e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false};
-  return launch_bn(pick_bn(d), hidden, capacity, W2, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, grid, st);
+  FfnSched s2{recv_rows, E_local, world, d, 0, 0, nullptr, nullptr};
+  const int bn2 = pick_bn(d);
+  if (bn2 == 256) {
+    BiasActEpi<256> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false};
+    return launch_bn(bn2, cta, hidden, capacity, W2, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, 0, st);
+  } else if (bn2 == 128) {
+    BiasActEpi<128> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false};
+    return launch_bn(bn2, cta, hidden, capacity, W2, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, 0, st);
+  }
+  BiasActEpi<64> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false};
+  return launch_bn(bn2, cta, hidden, capacity, W2, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, 0, st);
 }
 
 }  // namespace lshmoe

@@ -137,6 +137,7 @@ int launch_unpermute(const void* ret, lshmoe_dtype dtype, int64_t n, int d, cons
 int launch_local_exchange(const void* src, void* dst, int64_t capacity_rows, int row_bytes, const int32_t* counts,
                           int E, int32_t* counts_out, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!dst && !counts_out) return 0;                  // aliased exchange at world 1: nothing to move
   const int grid = dst ? 8 * device_sm_count() : 1;
   local_exchange_kernel<<<grid, 256, 0, st>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), capacity_rows,
                                               row_bytes, counts, E, counts_out);

@@ -1,0 +1,89 @@
+"""A/B timing of kernel variants (env-selected) on the C2 workload, one process, CUDA events,
+L2 flushed before every timed launch.  Usage: python scripts/ab_bench.py [hash|ffn|all]"""
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2411_08446_b200 as L  # noqa: E402
+from lshmoe_inputs import CONFIGS, make_experts, make_rank_inputs, rotation_seed  # noqa: E402
+
+
+def timeit(fn, iters=30, flush=None):
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(iters):
+        if flush is not None:
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3)
+    return statistics.median(ts), min(ts)
+
+
+def main():
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    cfgname = sys.argv[2] if len(sys.argv) > 2 else "C2"
+    cfg = CONFIGS[cfgname]
+    X, zeta, _ = make_rank_inputs(cfg, 0, 0)
+    X, zeta = X.cuda(), zeta.cuda()
+    R = L.rotation(cfg.d, cfg.q, rotation_seed(0), X.dtype).cuda()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
+    codes = torch.empty((cfg.n, cfg.q), dtype=torch.int16, device="cuda")
+    flops = 2.0 * cfg.n * cfg.q * cfg.d * cfg.d
+    if what in ("hash", "all"):
+        for split in ("1", "2"):
+            for cta in ("1", "2"):
+                os.environ["LSHMOE_HASH_SPLIT"] = split
+                os.environ["LSHMOE_HASH_CTA"] = cta
+                med, mn = timeit(lambda: L.hash(X, R, codes), flush=flush)
+                print(f"hash split={split == '1'} cta={cta}: median {med:.1f} us  min {mn:.1f} us  "
+                      f"{flops / med / 1e6:.0f} TFLOP/s", flush=True)
+        os.environ.pop("LSHMOE_HASH_SPLIT")
+        os.environ.pop("LSHMOE_HASH_CTA")
+        # library reference for the same contraction (Y = X R^T, Y materialised, no argmax)
+        Rt = R.reshape(cfg.q * cfg.d, cfg.d)
+        med, mn = timeit(lambda: torch.matmul(X, Rt.t()), flush=flush)
+        print(f"cuBLAS X @ R^T [{cfg.n}x{cfg.d}]x[{cfg.d}x{cfg.q * cfg.d}]: median {med:.1f} us  "
+              f"{flops / med / 1e6:.0f} TFLOP/s", flush=True)
+        A = torch.randn(8192, 8192, device="cuda").to(torch.bfloat16)
+        med, mn = timeit(lambda: torch.matmul(A, A), flush=flush)
+        print(f"cuBLAS 8192^3: median {med:.1f} us  {2 * 8192 ** 3 / med / 1e6:.0f} TFLOP/s", flush=True)
+    if what in ("ffn", "all"):
+        comp = L.compress(X, L.hash(X, R, codes), zeta, cfg.E)
+        ex = make_experts(cfg, 0)
+        W = [torch.stack([ex[e][i] for e in range(cfg.E)]).cuda() for i in range(4)]
+        rr = comp.expert_rows.view(cfg.E, 1)
+        out = torch.empty_like(comp.centroids)
+        hid = torch.empty((comp.centroids.shape[0], cfg.d_ffn), dtype=X.dtype, device="cuda")
+        m = int(comp.num_rows.item())
+        fl = 4.0 * m * cfg.d * cfg.d_ffn
+        for cta in ("1", "2"):
+            os.environ["LSHMOE_FFN_CTA"] = cta
+            med, mn = timeit(lambda: L.expert_ffn(comp.centroids, rr, *W, out=out, hidden=hid), flush=flush)
+            print(f"ffn cta={cta}: median {med:.1f} us  min {mn:.1f} us  {fl / med / 1e6:.0f} TFLOP/s  (m={m})",
+                  flush=True)
+        os.environ.pop("LSHMOE_FFN_CTA")
+        er = comp.expert_rows.cpu().tolist()
+        offs = [0]
+        for r in er:
+            offs.append(offs[-1] + r)
+
+        def torch_ffn():
+            for e in range(cfg.E):
+                a = comp.centroids[offs[e]:offs[e + 1]]
+                h = torch.relu(torch.addmm(W[1][e], a, W[0][e].t()))
+                torch.addmm(W[3][e], h, W[2][e].t(), out=out[offs[e]:offs[e + 1]])
+        med, mn = timeit(torch_ffn, flush=flush)
+        print(f"cuBLAS per-expert FFN (torch.addmm x{2 * cfg.E}): median {med:.1f} us  {fl / med / 1e6:.0f} TFLOP/s",
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()

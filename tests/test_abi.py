@@ -77,12 +77,16 @@ def test_validation_errors(L):
     v = ctypes.c_void_p(16)  # never dereferenced: validation fails first
     assert lib.lshmoe_rotation(0, 1, 1, 0, v) == L.EINVAL
     assert lib.lshmoe_rotation(4, 0, 1, 0, v) == L.EINVAL
-    assert lib.lshmoe_hash(v, 1, 10, 96, v, 2, v, None) == L.EUNSUPPORTED       # bf16, d % 64
-    assert lib.lshmoe_hash(v, 0, 10, 6, v, 2, v, None) == L.EUNSUPPORTED        # f32, d % 4
-    assert lib.lshmoe_hash(v, 1, -1, 64, v, 2, v, None) == L.EINVAL
-    assert lib.lshmoe_hash(v, 1, 10, 64, v, 17, v, None) == L.EUNSUPPORTED      # q > LSHMOE_MAX_Q
+    assert lib.lshmoe_hash(v, 1, 10, 96, v, 2, v, None, 0, None) == L.EUNSUPPORTED       # bf16, d % 64
+    assert lib.lshmoe_hash(v, 0, 10, 6, v, 2, v, None, 0, None) == L.EUNSUPPORTED        # f32, d % 4
+    assert lib.lshmoe_hash(v, 1, -1, 64, v, 2, v, None, 0, None) == L.EINVAL
+    assert lib.lshmoe_hash(v, 1, 10, 64, v, 17, v, None, 0, None) == L.EUNSUPPORTED      # q > LSHMOE_MAX_Q
     assert b"q > LSHMOE_MAX_Q" in lib.lshmoe_last_error()
-    assert lib.lshmoe_hash(v, 1, 0, 64, v, 2, v, None) == L.OK                  # n == 0: no-op
+    ws = ctypes.c_size_t(0)
+    assert lib.lshmoe_hash_workspace(16384, 768, 6, 1, ctypes.byref(ws)) == L.OK and ws.value > 0
+    assert lib.lshmoe_hash(v, 1, 16384, 768, v, 6, v, None, 0, None) == L.EINVAL         # workspace missing
+    assert lib.lshmoe_hash_workspace(100, 256, 6, 1, ctypes.byref(ws)) == L.OK and ws.value == 0
+    assert lib.lshmoe_hash(v, 1, 0, 64, v, 2, v, None, 0, None) == L.OK                  # n == 0: no-op
     ws = ctypes.c_size_t(0)
     assert lib.lshmoe_compress_workspace(100, 2, 4, 6, 64, 1, ctypes.byref(ws)) == L.OK and ws.value > 0
     # k > E

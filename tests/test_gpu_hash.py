@@ -94,6 +94,22 @@ def test_hash_identity_rotation_examples(L, golden):
     assert list(codes) == [c["code"] for c in golden["cp_hash_identity_rotation"]["cases"]]
 
 
+def test_hash_workspace_counters_reset_and_repeatable(L):
+    """The split-slice merge leaves its arrival counters at zero, so repeated calls (and CUDA-graph
+    replays) reuse the workspace; results are bit-identical run to run."""
+    cfg = small_cfg(n=1000, d=768, q=3)
+    case = make_case(L, cfg, seed=5, sanitize=False)
+    X, R = case.X.cuda(), case.R_lib.cuda()
+    ws = torch.zeros(L.hash_workspace_bytes(1000, 768, 3, torch.bfloat16), dtype=torch.uint8, device="cuda")
+    a = L.hash(X, R, workspace=ws).clone()
+    b = L.hash(X, R, workspace=ws)
+    torch.cuda.synchronize()
+    n_counters = ((1000 + 255) // 256) * 2 * 3
+    assert int(ws[:4 * n_counters].count_nonzero()) == 0
+    assert torch.equal(a, b)
+    assert np.array_equal(a.cpu().numpy()[case.margins >= NEAR_TIE], case.codes[case.margins >= NEAR_TIE])
+
+
 def test_hash_scale_invariance(L):
     cfg = small_cfg(n=512, d=128, q=2, dtype="f32")
     case = make_case(L, cfg, seed=4, sanitize=True)
