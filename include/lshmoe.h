@@ -136,6 +136,13 @@ lshmoe_status lshmoe_get_unique_id(uint8_t* id /* [host] LSHMOE_UNIQUE_ID_BYTES 
 lshmoe_status lshmoe_comm_init(const uint8_t* id /* [host] */, int world, int rank,
                                lshmoe_comm** out /* [host] */);
 lshmoe_status lshmoe_comm_destroy(lshmoe_comm* comm);
+/* Host-side plan of the exchange (pure host, no CUDA; used by dispatch/combine, exported so the
+   w-rank layout logic can be tested without GPUs).  counts [host] int32 [world, E]: expert_rows of
+   every rank.  Outputs [host]: send_off int64 [E+1] = row offset of expert e in this rank's centroid
+   layout; recv_off int64 [E/w*w + 1] = row offset of segment (local expert el, source src) at
+   index el*w + src in the receive layout; recv_rows int32 [E/w*w] = its row count. */
+lshmoe_status lshmoe_exchange_plan(int world, int rank, int num_experts, const int32_t* counts,
+                                   int64_t* send_off, int64_t* recv_off, int32_t* recv_rows);
 /* The counts of the last dispatch on this comm: counts [host] int32 [world, E], entry (p, e) =
    expert_rows[e] of rank p.  Only valid at world > 1 after lshmoe_dispatch. */
 lshmoe_status lshmoe_comm_last_counts(const lshmoe_comm* comm, int32_t* counts, int num_experts);

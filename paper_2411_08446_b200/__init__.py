@@ -47,6 +47,7 @@ _SIGS = {
     "lshmoe_comm_init": ([_vp, _i32, _i32, ctypes.POINTER(_vp)], _i32),
     "lshmoe_comm_destroy": ([_vp], _i32),
     "lshmoe_comm_last_counts": ([_vp, _vp, _i32], _i32),
+    "lshmoe_exchange_plan": ([_i32, _i32, _i32, _vp, _vp, _vp, _vp], _i32),
     "lshmoe_dispatch": ([_vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp, ctypes.POINTER(_i64), _vp], _i32),
     "lshmoe_expert_ffn": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp], _i32),
     "lshmoe_combine": ([_vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp], _i32),
@@ -285,6 +286,20 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+def exchange_plan(world: int, rank: int, counts: torch.Tensor):
+    """Host plan of dispatch/combine from every rank's expert_rows (counts int32 [world, E]):
+    (send_off [E+1], recv_off [E/w*w+1], recv_rows [E/w, w]) as CPU tensors."""
+    counts = counts.to(torch.int32).contiguous()
+    E = counts.shape[1]
+    epr = E // world
+    send_off = torch.empty(E + 1, dtype=torch.int64)
+    recv_off = torch.empty(epr * world + 1, dtype=torch.int64)
+    recv_rows = torch.empty((epr, world), dtype=torch.int32)
+    _check(_lib.lshmoe_exchange_plan(world, rank, E, _ptr(counts), _ptr(send_off), _ptr(recv_off), _ptr(recv_rows)),
+           "lshmoe_exchange_plan")
+    return send_off, recv_off, recv_rows
 
 
 def dispatch(comm: Optional[Comm], centroids: torch.Tensor, expert_rows: torch.Tensor, num_experts: int,

@@ -52,6 +52,28 @@ static lshmoe_status ensure_capacity(lshmoe_comm* c, int E) {
 
 extern "C" {
 
+lshmoe_status lshmoe_exchange_plan(int world, int rank, int E, const int32_t* counts, int64_t* send_off,
+                                   int64_t* recv_off, int32_t* recv_rows) {
+  if (world < 1 || rank < 0 || rank >= world || E < 1 || E % world != 0)
+    return set_error(LSHMOE_EINVAL, "lshmoe_exchange_plan: bad world / rank / E (E % world != 0, S:L285)");
+  if (!counts || !send_off || !recv_off || !recv_rows) return set_error(LSHMOE_EINVAL, "lshmoe_exchange_plan: NULL");
+  const int epr = E / world;
+  // send: this rank's centroids, expert-major (rows of expert e at send_off[e])
+  send_off[0] = 0;
+  for (int e = 0; e < E; ++e) send_off[e + 1] = send_off[e] + counts[rank * E + e];
+  // receive: segments ordered (local expert el, source src); S:L311 keeps each (src, dst) order
+  recv_off[0] = 0;
+  for (int el = 0; el < epr; ++el)
+    for (int src = 0; src < world; ++src) {
+      const size_t i = static_cast<size_t>(el) * world + src;
+      const int32_t rows = counts[src * E + rank * epr + el];
+      if (rows < 0) return set_error(LSHMOE_EINVAL, "lshmoe_exchange_plan: negative count");
+      recv_rows[i] = rows;
+      recv_off[i + 1] = recv_off[i] + rows;
+    }
+  return LSHMOE_OK;
+}
+
 lshmoe_status lshmoe_get_unique_id(uint8_t* id) {
   if (!id) return set_error(LSHMOE_EINVAL, "lshmoe_get_unique_id: id is NULL");
   static_assert(sizeof(ncclUniqueId) == LSHMOE_UNIQUE_ID_BYTES, "ncclUniqueId size");
@@ -128,17 +150,9 @@ lshmoe_status lshmoe_dispatch(lshmoe_comm* c, const void* centroids, lshmoe_dtyp
   c->last_E = E;
   const int32_t* cnt = c->counts.data();
   const int me = c->rank;
-  // my send offsets (expert-major centroid layout)
-  std::vector<int64_t> off(E + 1, 0);
-  for (int e = 0; e < E; ++e) off[e + 1] = off[e] + cnt[me * E + e];
-  // receive positions: (local expert, src)
-  std::vector<int64_t> rpos(static_cast<size_t>(epr) * world + 1, 0);
-  for (int el = 0; el < epr; ++el)
-    for (int src = 0; src < world; ++src) {
-      const size_t i = static_cast<size_t>(el) * world + src;
-      rpos[i + 1] = rpos[i] + cnt[src * E + me * epr + el];
-      c->rr_host[i] = cnt[src * E + me * epr + el];
-    }
+  std::vector<int64_t> off(E + 1, 0), rpos(static_cast<size_t>(epr) * world + 1, 0);
+  st = lshmoe_exchange_plan(world, me, E, cnt, off.data(), rpos.data(), c->rr_host);
+  if (st) return st;
   const int64_t total = rpos[static_cast<size_t>(epr) * world];
   if (total > recv_capacity) return set_error(LSHMOE_EINVAL, "lshmoe_dispatch: recv_capacity too small");
   if (recv_total) *recv_total = total;
@@ -198,15 +212,11 @@ lshmoe_status lshmoe_combine(lshmoe_comm* c, const void* expert_out, lshmoe_dtyp
   const int epr = E / world;
   const int me = c->rank;
   const int32_t* cnt = c->counts.data();
-  std::vector<int64_t> off(E + 1, 0);
-  for (int e = 0; e < E; ++e) off[e + 1] = off[e] + cnt[me * E + e];
+  std::vector<int64_t> off(E + 1, 0), rpos(static_cast<size_t>(epr) * world + 1, 0);
+  std::vector<int32_t> rr(static_cast<size_t>(epr) * world);
+  lshmoe_status pst = lshmoe_exchange_plan(world, me, E, cnt, off.data(), rpos.data(), rr.data());
+  if (pst) return pst;
   if (off[E] > returned_capacity) return set_error(LSHMOE_EINVAL, "lshmoe_combine: returned_capacity too small");
-  std::vector<int64_t> rpos(static_cast<size_t>(epr) * world + 1, 0);
-  for (int el = 0; el < epr; ++el)
-    for (int src = 0; src < world; ++src) {
-      const size_t i = static_cast<size_t>(el) * world + src;
-      rpos[i + 1] = rpos[i] + cnt[src * E + me * epr + el];
-    }
   const char* obase = static_cast<const char*>(expert_out);
   char* tbase = static_cast<char*>(returned);
   int err;

@@ -522,6 +522,13 @@ int launch_tc(const CUtensorMap& a, const CUtensorMap& b, int K, const Sched& s,
 
 int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64); }
 
+int env_bn(const char* name, int N, int dflt) {   // experiment override: 64 / 128 / 256 dividing N
+  const char* env = getenv(name);
+  if (!env) return dflt;
+  const int v = atoi(env);
+  return (v == 64 || v == 128 || v == 256) && N % v == 0 ? v : dflt;
+}
+
 // kCta = 2 needs BN / 2 rows per CTA to stay a multiple of 8 (SW128 atoms) and N >= 16 per CTA.
 template <class Sched, class Epi>
 int launch_bn(int bn, int cta, const void* A, int64_t a_rows, const void* B, int64_t b_rows, int K, Sched s, Epi e,
@@ -612,7 +619,7 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int cta = cta_mode("LSHMOE_FFN_CTA", 2);
   FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, nullptr, nullptr};
-  const int bn1 = pick_bn(d_ffn);
+  const int bn1 = env_bn("LSHMOE_FFN_BN1", d_ffn, pick_bn(d_ffn));
   int err;
   if (bn1 == 256) {
     BiasActEpi<256> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true};
@@ -626,7 +633,7 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
   }
   if (err) return err;
   FfnSched s2{recv_rows, E_local, world, d, 0, 0, nullptr, nullptr};
-  const int bn2 = pick_bn(d);
+  const int bn2 = env_bn("LSHMOE_FFN_BN2", d, pick_bn(d));
   if (bn2 == 256) {
     BiasActEpi<256> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false};
     return launch_bn(bn2, cta, hidden, capacity, W2, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, 0, st);

@@ -65,11 +65,17 @@ def main():
         m = int(comp.num_rows.item())
         fl = 4.0 * m * cfg.d * cfg.d_ffn
         for cta in ("1", "2"):
-            os.environ["LSHMOE_FFN_CTA"] = cta
-            med, mn = timeit(lambda: L.expert_ffn(comp.centroids, rr, *W, out=out, hidden=hid), flush=flush)
-            print(f"ffn cta={cta}: median {med:.1f} us  min {mn:.1f} us  {fl / med / 1e6:.0f} TFLOP/s  (m={m})",
-                  flush=True)
-        os.environ.pop("LSHMOE_FFN_CTA")
+            for bn1 in ("256", "128"):
+                for bn2 in ("256", "128", "64"):
+                    os.environ.update(LSHMOE_FFN_CTA=cta, LSHMOE_FFN_BN1=bn1, LSHMOE_FFN_BN2=bn2)
+                    med, mn = timeit(lambda: L.expert_ffn(comp.centroids, rr, *W, out=out, hidden=hid), flush=flush)
+                    print(f"ffn cta={cta} bn1={bn1} bn2={bn2}: median {med:.1f} us  min {mn:.1f} us  "
+                          f"{fl / med / 1e6:.0f} TFLOP/s  (m={m})", flush=True)
+        for k in ("LSHMOE_FFN_CTA", "LSHMOE_FFN_BN1", "LSHMOE_FFN_BN2"):
+            os.environ.pop(k)
+        med, mn = timeit(lambda: L.expert_ffn(comp.centroids, rr, *W, out=out, hidden=hid), flush=None)
+        print(f"ffn default, NO L2 flush (weights L2-resident): median {med:.1f} us  {fl / med / 1e6:.0f} TFLOP/s",
+              flush=True)
         er = comp.expert_rows.cpu().tolist()
         offs = [0]
         for r in er:
