@@ -120,7 +120,9 @@ lshmoe_status lshmoe_compress_workspace(int64_t n, int k, int num_experts, int q
      centroids_f32 float [n*k, d] nullable: the fp32 means before rounding (parity tier 2)
    Bucket key = the q-tuple of codes (AND-composite, reading R4); clustering is per
    (rank, expert) group (Alg. 1 L4-L6, reading R5).  Centroid = fp32 sum in a fixed order
-   divided once by the count (reading R10).  Stream-ordered; no host synchronisation. */
+   scaled once by the correctly rounded reciprocal of the count (reading R10).  Stream-ordered; no
+   host synchronisation.  n*k is bounded by the per-SM shared-memory staging of one perm range
+   (about 2700 * SM count copies, ~400K on B200); larger calls fail with an error. */
 lshmoe_status lshmoe_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d,
                               const int16_t* codes, int q,
                               const int32_t* experts, int k, int num_experts,

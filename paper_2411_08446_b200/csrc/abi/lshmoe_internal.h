@@ -29,8 +29,7 @@ struct CompressWs {            // carved from the caller's workspace by compress
   int32_t* vals[2];            // [nk] radix values (ping-pong)
   int32_t* rowid;              // [nk] centroid row of each first copy
   int32_t* hist;               // [256 * nblocks_max]
-  float* partial;              // [2 * n_items * d] centroid partial sums of rows spanning items
-  int64_t n_items;
+  float* partial;              // [kMaxGrid][2][d] centroid partial sums of rows cut by CTA ranges
   size_t bytes;
 };
 size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, CompressWs* ws);

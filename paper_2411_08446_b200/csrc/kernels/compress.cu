@@ -13,11 +13,11 @@
 //                give m_e and m.
 //   P2 radix   : stable LSD sort (8-bit digits, 2 passes for n*k <= 65536) of all copies by
 //                row = rowid[rep[c]] -> perm (ascending copy id within a row, reading R8), bucket.
-//   P3 centroid: perm split in 16-entry items; one thread per (item, 16-byte column chunk) issues
-//                all 16 member loads at once (128-bit), sums in perm order in fp32, divides once
-//                by the count (IEEE, reading R10) and rounds (RNE) into the send buffer.  Rows
-//                crossing items leave fp32 partials;
-//   P4 fix-up  : the item where such a row starts adds the partials in item order (deterministic).
+//   P3 centroid: perm split in one contiguous range per CTA; member rows are staged in shared
+//                memory by cp.async, summed in perm order in fp32, scaled once by RN(1/count)
+//                (reading R10) and rounded (RNE) into the send buffer.  Rows crossing ranges
+//                leave fp32 partials;
+//   P4 fix-up  : the CTA where such a row starts adds the partials in CTA order (deterministic).
 // Stable ranking inside a 1024-element radix tile: per-warp __match_any_sync + per-warp digit
 // counters in shared memory (a warp's rounds run in order), warp prefixes combined per digit;
 // tiles' histograms are published to global memory and every CTA derives its tiles' offsets.
@@ -34,10 +34,12 @@ namespace {
 
 constexpr int kThreads = 256;            // == kRadix: one thread per digit in the offset step
 constexpr int kRadix = 256;
-constexpr int kIPT = 1;                  // radix items per thread per tile (small tiles: more CTAs busy)
-constexpr int kTile = kThreads * kIPT;   // 1024 elements per radix tile
+constexpr int kIPT = 4;                  // max radix items per thread per tile (runtime P.ipt <= kIPT)
+constexpr int kMinTile = kThreads;       // smallest tile (ipt = 1): sizes the histogram workspace
+constexpr int kHistTiles = 64;           // tile histograms staged in shared memory up to this many
+constexpr int kHistPitch = kHistTiles + 1;
+constexpr int kHistSmem = kRadix * kHistPitch * 4;
 constexpr int kWarps = kThreads / 32;
-constexpr int kCH = 16;                  // perm entries per centroid item
 constexpr int kMaxE = 255;               // expert digit + sentinel fit one 8-bit pass
 constexpr int kHdr = 64 + 2048;          // workspace header ints: barrier counter, phase + per-CTA stamps
 
@@ -104,8 +106,10 @@ struct Params {
   uint32_t* keys[2];
   int32_t* vals[2];
   int32_t* hist;                   // [ntiles][256]
-  float* partial;                  // [n_items][2][d]
-  int ntiles, row_passes, n_items;
+  float* partial;                  // [G][2][d] partial sums of rows cut by CTA ranges
+  int ntiles, row_passes;
+  int max_range;                   // centroid: max perm entries per CTA range
+  int ipt;                         // radix elements per thread per tile (1, 2 or 4)
   int permute;                     // 1: uncompressed baseline (group by expert only)
 };
 
@@ -127,11 +131,16 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& phase) {
   ++phase;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
+    // release this CTA's writes (ordered before by bar.sync), then acquire everyone else's
+    asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     const unsigned target = phase * gridDim.x - 1u;
-    while (static_cast<int>(*reinterpret_cast<volatile unsigned*>(bar) - target) < 0) __nanosleep(32);
-    __threadfence();
+    unsigned v;
+    while (true) {
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (static_cast<int>(v - target) >= 0) break;
+      __nanosleep(20);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     stamp(bar, phase);
   }
   __syncthreads();
@@ -171,16 +180,16 @@ __device__ __forceinline__ void rank_tile(const Params& P, int kind, int pass, i
   for (int i = threadIdx.x; i < kWarps * kRadix; i += kThreads) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
-  const int base = tile * kTile + warp * (kIPT * 32);
+  const int base = tile * (kThreads * P.ipt) + warp * (P.ipt * 32);
 #pragma unroll
   for (int r = 0; r < kIPT; ++r) {   // all key loads in flight before the ordered ranking rounds
     const int i = base + r * 32 + lane;
-    if (i < n) pass_key(P, kind, pass, i, tr.key[r], tr.val[r]);
+    if (r < P.ipt && i < n) pass_key(P, kind, pass, i, tr.key[r], tr.val[r]);
   }
 #pragma unroll
   for (int r = 0; r < kIPT; ++r) {
     const int i = base + r * 32 + lane;
-    const bool ok = i < n;
+    const bool ok = r < P.ipt && i < n;
     tr.dg[r] = ok ? static_cast<int>((tr.key[r] >> shift) & (kRadix - 1)) : kRadix;
     const unsigned peers = __match_any_sync(0xFFFFFFFFu, tr.dg[r]);
     const int leader = __ffs(peers) - 1;
@@ -197,9 +206,10 @@ __device__ __forceinline__ void rank_tile(const Params& P, int kind, int pass, i
 // One stable counting-sort pass over n elements (key digit at `shift`), all CTAs cooperating.
 __device__ void radix_pass(const Params& P, int kind, int pass, int n, int shift, unsigned& phase,
                            int (*wcnt)[kRadix], int* s_off, int* s_tot) {
-  const int ntiles = (n + kTile - 1) / kTile;
+  const int ntiles = (n + kThreads * P.ipt - 1) / (kThreads * P.ipt);
   const int tpad = (ntiles + 3) & ~3;          // hist is digit-major [256][tpad]: 128-bit row loads
   const bool one_tile = ntiles <= static_cast<int>(gridDim.x);   // keep ranks in registers
+  extern __shared__ int s_hist[];              // [256][kHistPitch] when tpad <= kHistTiles
   TileRank tr;
   // (a) tile histograms
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -214,7 +224,30 @@ __device__ void radix_pass(const Params& P, int kind, int pass, int n, int shift
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int dgt = threadIdx.x;
     int tot = 0, pre = 0;
-    {
+    if (tpad <= kHistTiles) {   // whole table -> shared memory with coalesced 128-bit loads
+      const int n4 = kRadix * tpad / 4;          // <= 16 * kThreads
+      int4 v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {             // all loads first: one round trip
+        const int j = threadIdx.x + i * kThreads;
+        v[i] = j < n4 ? __ldcg(reinterpret_cast<const int4*>(P.hist) + j) : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int j = threadIdx.x + i * kThreads;
+        if (j < n4) {
+          const int e = 4 * j, dd = e / tpad, col = e - dd * tpad;
+          int* dst = s_hist + dd * kHistPitch + col;
+          dst[0] = v[i].x; dst[1] = v[i].y; dst[2] = v[i].z; dst[3] = v[i].w;
+        }
+      }
+      __syncthreads();
+      const int* row = s_hist + dgt * kHistPitch;   // pitch 65: conflict-free column walk
+      for (int u = 0; u < ntiles; ++u) {
+        if (u == t) pre = tot;
+        tot += row[u];
+      }
+    } else {
       const int4* hrow = reinterpret_cast<const int4*>(P.hist + dgt * tpad);
       for (int u0 = 0; u0 < tpad; u0 += 32) {   // up to 8 x 128-bit loads in flight
         int4 v[8];
@@ -249,6 +282,7 @@ __device__ void radix_pass(const Params& P, int kind, int pass, int n, int shift
     }
     const int excl = s_tot[32 + dgt] - tot;
     s_off[dgt] = excl + pre;
+    if (kind == PASS_ROW0 && t == 0 && threadIdx.x == 0) P.bar[20] = globaltimer_lo();   // diagnostics
     if (t == 0 && (kind == PASS_FIRSTS || kind == PASS_PERMUTE)) {
       if (dgt < P.E) P.expert_rows[dgt] = tot;
       if (kind == PASS_FIRSTS && dgt == P.E) *P.num_rows = excl;   // firsts precede the sentinel digit
@@ -289,18 +323,47 @@ __device__ void radix_pass(const Params& P, int kind, int pass, int n, int shift
       }
     }
     __syncthreads();
+    if (kind == PASS_ROW0 && t == 0 && threadIdx.x == 0) P.bar[21] = globaltimer_lo();   // diagnostics
   }
   grid_barrier(P.bar, phase);
 }
 
+// ---- centroid phase ------------------------------------------------------------------------
+// CTA b owns the perm range [b*nk/G, (b+1)*nk/G), split again into one contiguous sub-range per
+// warp, so eight segments (centroid rows) are reduced at once and the per-row boundary logic is
+// warp-uniform.  Each lane prefetches its own 16-byte column chunks of the warp's next rows into
+// a per-warp shared-memory ring with cp.async, kB rows per commit group and kNB groups in flight
+// (a lane only ever reads what it copied, so no barrier is needed); a batch's chunks are loaded
+// into registers at once and summed in perm order in fp32.  Rows cut by warp boundaries are
+// combined by the first warp holding them (warp order); rows cut by the CTA range leave fp32
+// partials (slot 0 = the range's first segment, slot 1 = its last) that fixup_phase adds in CTA
+// order.  Columns are processed in blocks of 128 chunks (2 KB of a row) to bound registers.
+constexpr int kBlkChunks = 128;          // 16-byte chunks per column block
+constexpr int kCPL = kBlkChunks / 32;    // chunks per lane per block
+constexpr int kRingSlot = 16 * kBlkChunks;
+constexpr int kWpartFloats = kBlkChunks * 8;   // one warp partial slot (fp32, up to 8 per chunk)
+constexpr int kQ = 10;                   // ring rows per warp (kQ - 1 in flight)
+static_assert(kWpartFloats * 4 <= kQ * kRingSlot, "a warp's slot-1 partial reuses its ring");
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {   // at most N of this thread's groups pending
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <typename T>
-__device__ __forceinline__ void acc_chunk(float* acc, const uint4& raw) {
+__device__ __forceinline__ void add_chunk16(float* acc, uint4 raw) {
   if (sizeof(T) == 2) {
-    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+    const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      acc[2 * i] += __uint_as_float(w[i] << 16);
-      acc[2 * i + 1] += __uint_as_float(w[i] & 0xFFFF0000u);
+      acc[2 * i] += __uint_as_float(u[i] << 16);
+      acc[2 * i + 1] += __uint_as_float(u[i] & 0xFFFF0000u);
     }
   } else {
     acc[0] += __uint_as_float(raw.x);
@@ -310,142 +373,292 @@ __device__ __forceinline__ void acc_chunk(float* acc, const uint4& raw) {
   }
 }
 
+template <int VC>
+__device__ __noinline__ void store_f32_copy(float* dst, const float* v) {   // tier-2 parity output only
+#pragma unroll
+  for (int e = 0; e < VC; ++e) dst[e] = v[e];
+}
+
+// centroid = acc * rc, rc = RN(1/count) (reading R10), RNE to the wire dtype; fp32 copy if requested.
 template <typename T>
-__device__ __forceinline__ void store_centroid(const Params& P, int row, int ch, const float* acc, float cnt) {
-  constexpr int VN = Vec<T>::N;
-  float v[VN];
+__device__ __forceinline__ void store_chunk16(const Params& P, int row, int c16, const float* acc, float rc) {
+  constexpr int VC = 16 / sizeof(T);
+  float v[VC];
 #pragma unroll
-  for (int e = 0; e < VN; ++e) v[e] = __fdiv_rn(acc[e], cnt);
-  Vec<T>::store(P.cent + static_cast<int64_t>(row) * P.row_bytes + 16 * ch, v);
-  if (P.cent32) {
-    float* dst = P.cent32 + static_cast<int64_t>(row) * P.d + ch * VN;
+  for (int e = 0; e < VC; ++e) v[e] = acc[e] * rc;
+  uint4 out;
+  if (sizeof(T) == 2) {
+    uint32_t u[4];
 #pragma unroll
-    for (int e = 0; e < VN; e += 4) *reinterpret_cast<float4*>(dst + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      u[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    out = make_uint4(u[0], u[1], u[2], u[3]);
+  } else {
+    out = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
   }
+  *reinterpret_cast<uint4*>(P.cent + static_cast<int64_t>(row) * P.row_bytes + 16 * c16) = out;
+  if (P.cent32) store_f32_copy<VC>(P.cent32 + static_cast<int64_t>(row) * P.d + c16 * VC, v);
+}
+
+template <typename T>
+__device__ __forceinline__ void add_chunk8(float* acc, uint2 raw) {
+  if (sizeof(T) == 2) {
+    acc[0] += __uint_as_float(raw.x << 16);
+    acc[1] += __uint_as_float(raw.x & 0xFFFF0000u);
+    acc[2] += __uint_as_float(raw.y << 16);
+    acc[3] += __uint_as_float(raw.y & 0xFFFF0000u);
+  } else {
+    acc[0] += __uint_as_float(raw.x);
+    acc[1] += __uint_as_float(raw.y);
+  }
+}
+
+// centroid = acc * RN(1/count) (reading R10), RNE to the wire dtype; fp32 copy if requested.
+template <typename T>
+__device__ __forceinline__ void store_chunk8(const Params& P, int row, int ch, const float* acc, float cnt) {
+  constexpr int VC = sizeof(T) == 2 ? 4 : 2;
+  const float rc = __frcp_rn(cnt);
+  float v[VC];
+#pragma unroll
+  for (int e = 0; e < VC; ++e) v[e] = acc[e] * rc;
+  uint2 out;
+  if (sizeof(T) == 2) {
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]);
+    __nv_bfloat162 h1 = __floats2bfloat162_rn(v[2], v[3]);
+    out = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+  } else {
+    out = make_uint2(__float_as_uint(v[0]), __float_as_uint(v[1]));
+  }
+  *reinterpret_cast<uint2*>(P.cent + static_cast<int64_t>(row) * P.row_bytes + 8 * ch) = out;
+  if (P.cent32) {
+    float* dst = P.cent32 + static_cast<int64_t>(row) * P.d + ch * VC;
+#pragma unroll
+    for (int e = 0; e < VC; ++e) dst[e] = v[e];
+  }
+}
+
+__device__ __forceinline__ int range_begin(int b, int nk, int G) { return static_cast<int>(static_cast<int64_t>(b) * nk / G); }
+__device__ __forceinline__ int range_cta(int p, int nk, int G) {   // CTA whose range holds p
+  return static_cast<int>((static_cast<int64_t>(p + 1) * G - 1) / nk);
+}
+
+// Dynamic shared memory of compress_kernel, named at file scope so that the centroid phase's
+// addresses stay in the shared window (no generic-to-shared conversion per access).
+extern __shared__ __align__(1024) uint8_t g_dsmem[];
+
+// Centroid-phase shared memory: [warp][kQ][kRingSlot] rings | [warp][kWpartFloats] slot-0
+// partials | rows[p_begin-1 .. p_end] | tok[p_begin .. p_end).
+struct CentroidCtx {                     // one CTA's view of its perm range (centroid phase)
+  int p_begin, p_end, range, w, lane, w_begin, w_end, tok_off;
+  uint32_t prev_row;                     // row of entry w_begin - 1
+  __device__ uint8_t* ring() const { return g_dsmem + w * kQ * kRingSlot; }
+  __device__ float* slot0() const { return reinterpret_cast<float*>(g_dsmem + kWarps * kQ * kRingSlot); }
+  __device__ uint32_t* s_row() const { return reinterpret_cast<uint32_t*>(slot0() + kWarps * kWpartFloats); }
+  __device__ int32_t* s_tok() const { return reinterpret_cast<int32_t*>(s_row()) + tok_off; }
+  __device__ uint32_t row_at(int p) const { return s_row()[p - p_begin + 1]; }
+  __device__ int wbeg(int ww) const { return p_begin + range_begin(ww, range, kWarps); }
+  __device__ float* wpart(int ww, int slot) const {   // slot 0: own region; slot 1: the warp's ring
+    return slot == 0 ? slot0() + ww * kWpartFloats : reinterpret_cast<float*>(g_dsmem + ww * kQ * kRingSlot);
+  }
+};
+
+// One column block (chunks [c0, c0 + ncb), CPL = ceil(ncb / 32) chunks per lane) of the centroid
+// phase: stream the warp's rows through its ring, reduce segments, then combine cut rows.
+template <typename T, int CPL>
+__device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, int c0, int ncb) {
+  constexpr int VC = 16 / sizeof(T);
+  const int lane = X.lane, w = X.w, w_begin = X.w_begin, w_end = X.w_end;
+  const bool full = ncb == CPL * 32;
+  auto issue = [&](int p, int slot) {
+    if (p < w_end) {
+      const uint8_t* src = P.x + static_cast<int64_t>(X.s_tok()[p - X.p_begin]) * P.row_bytes + 16 * c0;
+      uint8_t* dst = X.ring() + slot * kRingSlot;
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) {
+        const int c = lane + 32 * t;
+        if (full || c < ncb) cp_async16(dst + 16 * c, src + 16 * c);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll 1
+  for (int i = 0; i < kQ - 1; ++i) issue(w_begin + i, i);
+  float acc[CPL][VC];
+#pragma unroll
+  for (int t = 0; t < CPL; ++t)
+#pragma unroll
+    for (int e = 0; e < VC; ++e) acc[t][e] = 0.0f;
+  int seg_start = w_begin, rd = 0, wr = kQ - 1;   // ring slots: next to read, next to fill
+  uint32_t row = w_end > w_begin ? X.row_at(w_begin) : 0u;
+#pragma unroll 1
+  for (int p = w_begin; p < w_end; ++p) {
+    issue(p + kQ - 1, wr);
+    wr = wr + 1 == kQ ? 0 : wr + 1;
+    cp_async_wait<kQ - 1>();                  // entry p (this lane's chunks) has landed
+    const uint8_t* st = X.ring() + rd * kRingSlot;
+    rd = rd + 1 == kQ ? 0 : rd + 1;
+#pragma unroll
+    for (int t = 0; t < CPL; ++t) {
+      const int c = lane + 32 * t;
+      if (full || c < ncb) add_chunk16<T>(acc[t], *reinterpret_cast<const uint4*>(st + 16 * c));
+    }
+    const uint32_t next = X.row_at(p + 1);
+    if (next == row && p + 1 < w_end) continue;         // the segment goes on
+    const bool head = seg_start > w_begin || X.prev_row != row;   // the row starts in this warp
+    if (cb == 0 && lane == 0) {
+      if (head) P.row_start[row] = seg_start;
+      if (p + 1 == P.nk) P.row_start[row + 1] = P.nk;   // row_start[m] = n*k
+    }
+    if (head && next != row) {                // the whole row lies in this warp's sub-range
+      const float rc = __frcp_rn(static_cast<float>(p + 1 - seg_start));
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) {
+        const int c = lane + 32 * t;
+        if (full || c < ncb) store_chunk16<T>(P, static_cast<int>(row), c0 + c, acc[t], rc);
+      }
+    } else if (p + 1 == w_end) {
+      break;                                  // the last segment stays in acc (partial, see below)
+    } else {                                  // the first segment, begun in an earlier warp
+      float* d0 = X.wpart(w, 0);
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) {
+        const int c = lane + 32 * t;
+        if (full || c < ncb)
+#pragma unroll
+          for (int e = 0; e < VC; ++e) d0[c * VC + e] = acc[t][e];
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < CPL; ++t)
+#pragma unroll
+      for (int e = 0; e < VC; ++e) acc[t][e] = 0.0f;
+    seg_start = p + 1;
+    row = next;
+  }
+  cp_async_wait<0>();                         // the ring is free: it may hold the slot-1 partial
+  const int nrows = w_end - w_begin;
+  const uint32_t r_last = X.row_at(w_end - 1);
+  const bool cut_end = nrows > 0 && X.row_at(w_end) == r_last;
+  const bool from_before = nrows > 0 && seg_start == w_begin && X.prev_row == r_last;   // began in an earlier warp
+  if (cut_end || from_before) {
+    float* d1 = X.wpart(w, seg_start == w_begin ? 0 : 1);
+#pragma unroll
+    for (int t = 0; t < CPL; ++t) {
+      const int c = lane + 32 * t;
+      if (full || c < ncb)
+#pragma unroll
+        for (int e = 0; e < VC; ++e) d1[c * VC + e] = acc[t][e];
+    }
+  }
+  __syncthreads();                            // every warp's pieces are in wpart
+  // Combine the rows cut by warp boundaries; warp w owns a cut row whose first entry in this
+  // CTA lies in its sub-range.  lo = that entry; hi = one past the row's last entry in the CTA.
+  auto own = [&](uint32_t r, int lo) {
+    int a = lo + 1, z = X.p_end;              // rows are sorted: first entry in (lo, p_end] != r
+    while (a < z) {
+      const int mid = (a + z) / 2;
+      if (X.row_at(mid) == r) a = mid + 1; else z = mid;
+    }
+    const int hi = a;
+    const int wl = range_cta(hi - 1 - X.p_begin, X.range, kWarps);
+    const bool before = lo == X.p_begin && X.row_at(X.p_begin - 1) == r;
+    const bool after = hi == X.p_end && X.row_at(X.p_end) == r;
+    const float rc = __frcp_rn(static_cast<float>(hi - lo));
+#pragma unroll
+    for (int t = 0; t < CPL; ++t) {
+      const int c = lane + 32 * t;
+      if (!full && c >= ncb) continue;
+      float v[VC];
+      const float* s0 = X.wpart(w, lo == w_begin ? 0 : 1) + c * VC;
+#pragma unroll
+      for (int e = 0; e < VC; ++e) v[e] = s0[e];
+      for (int ww = w + 1; ww <= wl; ++ww) {
+        if (X.wbeg(ww + 1) == X.wbeg(ww)) continue;          // empty sub-range
+        const float* s1 = X.wpart(ww, 0) + c * VC;
+#pragma unroll
+        for (int e = 0; e < VC; ++e) v[e] += s1[e];
+      }
+      if (before || after) {
+        float* dst = P.partial + (static_cast<int64_t>(blockIdx.x) * 2 + (lo == X.p_begin ? 0 : 1)) * P.d + (c0 + c) * VC;
+#pragma unroll
+        for (int e = 0; e < VC; ++e) dst[e] = v[e];
+      } else {
+        store_chunk16<T>(P, static_cast<int>(r), c0 + c, v, rc);
+      }
+    }
+  };
+  if (nrows > 0) {
+    const bool first_w = w == range_cta(0, X.range, kWarps);   // first non-empty sub-range of the CTA
+    if (cut_end && (first_w || !from_before)) own(r_last, seg_start);
+    if (first_w) {                            // the CTA's first row, begun in an earlier CTA
+      const uint32_t r0 = X.row_at(X.p_begin);
+      if (X.prev_row == r0 && !(r0 == r_last && cut_end)) own(r0, X.p_begin);
+    }
+  }
+  __syncthreads();                            // the ring is reused by the next column block
 }
 
 template <typename T>
 __device__ void centroid_phase(const Params& P, const uint32_t* rows, const int32_t* tok) {
-  constexpr int VN = Vec<T>::N;
-  const int64_t work = static_cast<int64_t>(P.n_items) * P.nch;
-  for (int64_t w = blockIdx.x * int64_t(kThreads) + threadIdx.x; w < work; w += int64_t(gridDim.x) * kThreads) {
-    const int item = static_cast<int>(w / P.nch);
-    const int ch = static_cast<int>(w - int64_t(item) * P.nch);
-    const int p0 = item * kCH;
-    const int cnt = min(kCH, P.nk - p0);
-    uint32_t rw[kCH];
-    int tk[kCH];
-    // 1) the item's 16 row ids + token ids (128-bit loads), 2) the 16 member chunks: each batch
-    // is issued back to back, nothing inside a batch waits on another load
-    if (cnt == kCH) {
-#pragma unroll
-      for (int j = 0; j < kCH; j += 4) {
-        const uint4 r4 = __ldcg(reinterpret_cast<const uint4*>(rows + p0 + j));
-        const int4 t4 = __ldcg(reinterpret_cast<const int4*>(tok + p0 + j));
-        rw[j] = r4.x; rw[j + 1] = r4.y; rw[j + 2] = r4.z; rw[j + 3] = r4.w;
-        tk[j] = t4.x; tk[j + 1] = t4.y; tk[j + 2] = t4.z; tk[j + 3] = t4.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < kCH; ++j) {
-        rw[j] = j < cnt ? ldcg(rows + p0 + j) : 0xFFFFFFFFu;
-        tk[j] = j < cnt ? ldcg(tok + p0 + j) : 0;
-      }
-    }
-    const uint32_t prev = p0 > 0 ? ldcg(rows + p0 - 1) : 0xFFFFFFFFu;
-    const uint32_t next = p0 + cnt < P.nk ? ldcg(rows + p0 + cnt) : 0xFFFFFFFFu;
-    uint4 v[kCH];
-#pragma unroll
-    for (int j = 0; j < kCH; ++j)
-      v[j] = j < cnt ? __ldg(reinterpret_cast<const uint4*>(P.x + static_cast<int64_t>(tk[j]) * P.row_bytes) + ch)
-                     : make_uint4(0, 0, 0, 0);
-    // segment ends (bit j: member j closes its row inside this item) and row heads
-    unsigned ends = 0, heads = 0;
-#pragma unroll
-    for (int j = 0; j < kCH; ++j) {
-      if (j < cnt) {
-        ends |= static_cast<unsigned>(j == cnt - 1 || rw[j + 1 < kCH ? j + 1 : j] != rw[j]) << j;
-        heads |= static_cast<unsigned>(rw[j] != (j == 0 ? prev : rw[j > 0 ? j - 1 : 0])) << j;
-      }
-    }
-    if (ch == 0) {   // row boundaries (perm offsets)
-      for (unsigned h = heads; h; h &= h - 1) {
-        const int j = __ffs(h) - 1;
-        P.row_start[rw[j]] = p0 + j;
-      }
-      if (p0 + cnt == P.nk) P.row_start[rw[cnt - 1] + 1] = P.nk;
-    }
-    float acc[VN];
-#pragma unroll
-    for (int e = 0; e < VN; ++e) acc[e] = 0.0f;
-    int s = 0;
-#pragma unroll
-    for (int j = 0; j < kCH; ++j) {
-      acc_chunk<T>(acc, v[j]);          // members past cnt are zeros after the last flush
-      if ((ends >> j) & 1u) {
-        const bool complete = (s > 0 || prev != rw[j]) && (j < cnt - 1 || next != rw[j]);
-        if (complete) {
-          store_centroid<T>(P, static_cast<int>(rw[j]), ch, acc, static_cast<float>(j + 1 - s));
-        } else {
-          float* dst = P.partial + (static_cast<int64_t>(item) * 2 + (s == 0 ? 0 : 1)) * P.d + ch * VN;
-#pragma unroll
-          for (int e = 0; e < VN; e += 4) *reinterpret_cast<float4*>(dst + e) = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
-        }
-#pragma unroll
-        for (int e = 0; e < VN; ++e) acc[e] = 0.0f;
-        s = j + 1;
-      }
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  CentroidCtx X;
+  X.p_begin = range_begin(b, P.nk, G);
+  X.p_end = range_begin(b + 1, P.nk, G);
+  X.range = X.p_end - X.p_begin;
+  if (X.range == 0) return;                   // CTA-uniform
+  X.lane = tid % 32;
+  X.w = tid / 32;
+  X.tok_off = P.max_range + 2;
+  uint32_t* s_row = X.s_row();
+  int32_t* s_tok = X.s_tok();
+  for (int i = tid; i < X.range + 2; i += kThreads) {
+    const int p = X.p_begin - 1 + i;
+    s_row[i] = (p >= 0 && p < P.nk) ? ldcg(rows + p) : 0xFFFFFFFFu;
+  }
+  for (int i = tid; i < X.range; i += kThreads) s_tok[i] = ldcg(tok + X.p_begin + i);
+  __syncthreads();
+  X.w_begin = X.wbeg(X.w);
+  X.w_end = X.wbeg(X.w + 1);
+  X.prev_row = X.row_at(X.w_begin - 1);
+  for (int c0 = 0, cb = 0; c0 < P.nch; c0 += kBlkChunks, ++cb) {
+    const int ncb = min(kBlkChunks, P.nch - c0);
+    switch ((ncb + 31) / 32) {
+      case 1: centroid_block<T, 1>(P, X, cb, c0, ncb); break;
+      case 2: centroid_block<T, 2>(P, X, cb, c0, ncb); break;
+      case 3: centroid_block<T, 3>(P, X, cb, c0, ncb); break;
+      default: centroid_block<T, 4>(P, X, cb, c0, ncb); break;
     }
   }
 }
 
+// Rows cut by CTA ranges: the CTA in which such a row starts adds the partials in CTA order.
 template <typename T>
 __device__ void fixup_phase(const Params& P, const uint32_t* rows) {
-  constexpr int VN = Vec<T>::N;
-  const int64_t work = static_cast<int64_t>(P.n_items) * P.nch;
-  for (int64_t w = blockIdx.x * int64_t(kThreads) + threadIdx.x; w < work; w += int64_t(gridDim.x) * kThreads) {
-    const int item = static_cast<int>(w / P.nch);
-    const int ch = static_cast<int>(w - int64_t(item) * P.nch);
-    const int p0 = item * kCH;
-    const int p1 = min(p0 + kCH, P.nk);
-    if (p1 >= P.nk) continue;
-    const uint32_t row = ldcg(rows + p1 - 1);
-    if (ldcg(rows + p1) != row) continue;             // the item's last row ends inside it
-    const int rs = ldcg(P.row_start + row);
-    if (rs < p0) continue;                            // started earlier: not the owner
-    const int re = ldcg(P.row_start + row + 1);
-    const int i1 = (re - 1) / kCH;
-    float acc[VN];
-    {
-      const float* src = P.partial + (static_cast<int64_t>(item) * 2 + (rs == p0 ? 0 : 1)) * P.d + ch * VN;
+  constexpr int VC = sizeof(T) == 2 ? 4 : 2;
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const int p_begin = range_begin(b, P.nk, G), p_end = range_begin(b + 1, P.nk, G);
+  if (p_end >= P.nk || p_end <= p_begin) return;
+  const uint32_t row = ldcg(rows + p_end - 1);
+  if (ldcg(rows + p_end) != row) return;               // the range's last row ends inside it
+  const int rs = ldcg(P.row_start + row);
+  if (rs < p_begin) return;                            // started in an earlier range: not the owner
+  const int re = ldcg(P.row_start + row + 1);
+  const int b1 = range_cta(re - 1, P.nk, G);
+  const int nc8 = P.row_bytes / 8;
+  for (int ch = tid; ch < nc8; ch += kThreads) {
+    float acc[VC];
+    const float* src = P.partial + (static_cast<int64_t>(b) * 2 + (rs == p_begin ? 0 : 1)) * P.d + ch * VC;
 #pragma unroll
-      for (int e = 0; e < VN; e += 4) {
-        const float4 f = __ldcg(reinterpret_cast<const float4*>(src + e));
-        acc[e] = f.x; acc[e + 1] = f.y; acc[e + 2] = f.z; acc[e + 3] = f.w;
-      }
+    for (int e = 0; e < VC; ++e) acc[e] = __ldcg(src + e);
+    for (int bb = b + 1; bb <= b1; ++bb) {
+      if (range_begin(bb + 1, P.nk, G) == range_begin(bb, P.nk, G)) continue;   // empty range (nk < G)
+      const float* s2 = P.partial + (static_cast<int64_t>(bb) * 2) * P.d + ch * VC;
+#pragma unroll
+      for (int e = 0; e < VC; ++e) acc[e] += __ldcg(s2 + e);
     }
-    for (int it0 = item + 1; it0 <= i1; it0 += 8) {   // 8 partials in flight, summed in item order
-      float4 f[8][VN / 4];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (it0 + u <= i1) {
-          const float* src = P.partial + (static_cast<int64_t>(it0 + u) * 2) * P.d + ch * VN;
-#pragma unroll
-          for (int e = 0; e < VN / 4; ++e) f[u][e] = __ldcg(reinterpret_cast<const float4*>(src) + e);
-        }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (it0 + u <= i1) {
-#pragma unroll
-          for (int e = 0; e < VN / 4; ++e) {
-            acc[4 * e] += f[u][e].x;
-            acc[4 * e + 1] += f[u][e].y;
-            acc[4 * e + 2] += f[u][e].z;
-            acc[4 * e + 3] += f[u][e].w;
-          }
-        }
-    }
-    store_centroid<T>(P, static_cast<int>(row), ch, acc, static_cast<float>(re - rs));
+    store_chunk8<T>(P, static_cast<int>(row), ch, acc, static_cast<float>(re - rs));
   }
 }
 
@@ -484,7 +697,7 @@ __device__ void gather_phase(const Params& P) {   // baseline: send[p] = x[token
   }
 }
 
-__global__ void __launch_bounds__(kThreads) compress_kernel(Params P) {
+__global__ void __launch_bounds__(kThreads, 1) compress_kernel(Params P) {
   __shared__ int wcnt[kWarps][kRadix];
   __shared__ int s_off[kRadix];
   __shared__ int s_tot[kRadix + 32];
@@ -504,17 +717,13 @@ __global__ void __launch_bounds__(kThreads) compress_kernel(Params P) {
   const int32_t* tok = P.vals[P.row_passes & 1];    // token id of each perm entry
   // per-CTA centroid-phase start / end stamps (diagnostics, bar[64 + 2 * cta])
   if (threadIdx.x == 0 && blockIdx.x < 1024) P.bar[64 + 2 * blockIdx.x] = globaltimer_lo();
-  if (P.is_bf16) {
-    centroid_phase<__nv_bfloat16>(P, rows, tok);
-    __syncthreads();
-    if (threadIdx.x == 0 && blockIdx.x < 1024) P.bar[65 + 2 * blockIdx.x] = globaltimer_lo();
-    grid_barrier(P.bar, phase);
-    fixup_phase<__nv_bfloat16>(P, rows);
-  } else {
-    centroid_phase<float>(P, rows, tok);
-    grid_barrier(P.bar, phase);
-    fixup_phase<float>(P, rows);
-  }
+  if (P.is_bf16) centroid_phase<__nv_bfloat16>(P, rows, tok);
+  else centroid_phase<float>(P, rows, tok);
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x < 1024) P.bar[65 + 2 * blockIdx.x] = globaltimer_lo();
+  grid_barrier(P.bar, phase);
+  if (P.is_bf16) fixup_phase<__nv_bfloat16>(P, rows);
+  else fixup_phase<float>(P, rows);
   __syncthreads();
   stamp(P.bar, phase + 1);   // CTA 0's end (other CTAs may still be finishing the fix-up)
 }
@@ -525,21 +734,35 @@ int bits_for(int64_t maxval) {   // bits needed to represent values in [0, maxva
   return b;
 }
 
-int coop_grid() {
-  static int grid = 0;
-  if (!grid) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress_kernel, kThreads, 0);
-    grid = std::max(1, std::min(per_sm, 4)) * device_sm_count();
-  }
-  return grid;
+constexpr int kMaxGrid = 512;            // CTAs of the cooperative kernel (one per SM) <= this
+
+// Dynamic shared memory: the radix offset step's tile histograms or the centroid ring, whichever
+// is larger (the phases run one after the other).
+constexpr int kMaxDynSmem = 214 * 1024;   // + the kernel's static shared memory <= 227 KB
+int coop_max_range(int nk) {
+  const int G = std::min(device_sm_count(), kMaxGrid);
+  return (nk + G - 1) / G + 1;
 }
+// Centroid-phase shared memory: per-warp rings, warp partials, the range's index arrays.
+int centroid_smem(int max_range) {
+  return kWarps * kQ * kRingSlot + kWarps * kWpartFloats * 4 + 4 * (2 * max_range + 2);
+}
+int coop_smem(int max_range) { return std::max(centroid_smem(max_range), kHistSmem); }
 
 int launch_coop(const Params& P, cudaStream_t st) {
+  static int configured = 0;                 // largest dynamic smem size set so far
+  const int max_range = coop_max_range(P.nk);
+  const int smem = coop_smem(max_range);
+  if (!P.permute && centroid_smem(max_range) > kMaxDynSmem) return cudaErrorInvalidValue;   // range too long
+  if (smem > configured) {
+    int err = cudaFuncSetAttribute(compress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err) return err;
+    configured = smem;
+  }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(coop_grid());
+  cfg.gridDim = dim3(std::min(device_sm_count(), kMaxGrid));   // one CTA per SM, all co-resident
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -547,6 +770,7 @@ int launch_coop(const Params& P, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   Params p = P;
+  p.max_range = max_range;
   int err = cudaLaunchKernelEx(&cfg, compress_kernel, p);
   count_launches(1);
   return err;
@@ -569,8 +793,7 @@ size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, Com
   const int64_t nk = n * k;
   int64_t tsize = 1024;
   while (tsize < 2 * nk) tsize <<= 1;
-  const int64_t ntiles = (nk + kTile - 1) / kTile;
-  const int64_t n_items = (nk + kCH - 1) / kCH;
+  const int64_t ntiles = (nk + kMinTile - 1) / kMinTile;   // upper bound over every ipt
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -585,7 +808,7 @@ size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, Com
   const size_t o_v1 = take(sizeof(int32_t) * nk);
   const size_t o_rowid = take(sizeof(int32_t) * nk);
   const size_t o_hist = take(sizeof(int32_t) * kRadix * ((ntiles + 3) & ~int64_t(3)) + 64);
-  const size_t o_part = take(sizeof(float) * 2 * n_items * d);
+  const size_t o_part = take(sizeof(float) * 2 * kMaxGrid * d);
   if (ws) {
     uint8_t* b = static_cast<uint8_t*>(base);
     ws->table = reinterpret_cast<int32_t*>(b + o_table);
@@ -598,7 +821,6 @@ size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, Com
     ws->rowid = reinterpret_cast<int32_t*>(b + o_rowid);
     ws->hist = reinterpret_cast<int32_t*>(b + o_hist);
     ws->partial = reinterpret_cast<float*>(b + o_part);
-    ws->n_items = n_items;
     ws->bytes = off;
   }
   return off;
@@ -627,8 +849,10 @@ static Params base_params(const void* x, lshmoe_dtype dtype, int64_t n, int d, c
   P.vals[1] = ws.vals[1];
   P.hist = ws.hist;
   P.partial = ws.partial;
-  P.ntiles = (P.nk + kTile - 1) / kTile;
-  P.n_items = static_cast<int>(ws.n_items);
+  // elements per thread per radix tile: as few as possible while keeping <= 64 tiles (the tile
+  // histograms then fit in shared memory for the offset step)
+  P.ipt = P.nk <= kHistTiles * kThreads ? 1 : (P.nk <= 2 * kHistTiles * kThreads ? 2 : 4);
+  P.ntiles = (P.nk + kThreads * P.ipt - 1) / (kThreads * P.ipt);
   return P;
 }
 

@@ -55,6 +55,27 @@ def main():
         A = torch.randn(8192, 8192, device="cuda").to(torch.bfloat16)
         med, mn = timeit(lambda: torch.matmul(A, A), flush=flush)
         print(f"cuBLAS 8192^3: median {med:.1f} us  {2 * 8192 ** 3 / med / 1e6:.0f} TFLOP/s", flush=True)
+    if what in ("compress", "all"):
+        ws = torch.empty(L.compress_workspace_bytes(cfg.n, cfg.k, cfg.E, cfg.q, cfg.d, X.dtype), dtype=torch.uint8,
+                         device="cuda")
+        L.hash(X, R, codes)
+        comp = L.alloc_compressed(cfg.n, cfg.k, cfg.E, cfg.d, X.dtype, "cuda")
+        med, mn = timeit(lambda: L.compress(X, codes, zeta, cfg.E, out=comp, workspace=ws), flush=flush)
+        print(f"compress: median {med:.1f} us  min {mn:.1f}", flush=True)
+        print("  phases", L.compress_phase_times(ws))
+        print("  centroid CTAs", L.compress_cta_times(ws))
+        raw = ws[:128].cpu().view(torch.int32).numpy().astype("int64") & 0xFFFFFFFF
+        if int(os.environ.get("LSHMOE_CDBG", "0")) & 8:
+            import numpy as np
+            hdr = ws[:4 * 1000].cpu().view(torch.int32).numpy().astype("int64") & 0xFFFFFFFF
+            st = hdr[64:64 + 2 * 148:2]; en = hdr[65:65 + 2 * 148:2]
+            q = hdr[400:400 + 4 * 148].reshape(148, 4)
+            idx = (q[:, 0] - st) / 1e3; loop = q[:, 1] / 1e3; sync = (q[:, 2] - q[:, 0]) / 1e3 - loop
+            comb = (q[:, 3] - q[:, 2]) / 1e3; tail = (en - q[:, 3]) / 1e3
+            for nm, v in (("idx", idx), ("loop", loop), ("sync", sync), ("combine", comb), ("tail", tail)):
+                print(f"  {nm}: min {v.min():.2f} med {np.median(v):.2f} max {v.max():.2f}")
+        print(f"  row_lo scatter sub-steps: offsets {(raw[20] - raw[6]) / 1e3:.2f} us, scatter "
+              f"{(raw[21] - raw[20]) / 1e3:.2f} us, barrier {(raw[7] - raw[21]) / 1e3:.2f} us", flush=True)
     if what in ("ffn", "all"):
         comp = L.compress(X, L.hash(X, R, codes), zeta, cfg.E)
         ex = make_experts(cfg, 0)
