@@ -73,6 +73,10 @@ const char* lshmoe_last_error(void);
 /* Cumulative number of CUDA kernels this library has launched in this process (all threads);
    the bench reports the per-step difference as "gpu_launches". */
 int64_t lshmoe_kernel_launches(void);
+/* Diagnostics switch (default off): when on, lshmoe_compress's kernels record per-CTA globaltimer
+   stamps in the header of its workspace (layout: csrc/kernels/compress.cu, kDiag), read by the
+   Python binding's compress_diag().  Process-wide; affects launches issued after the call. */
+void lshmoe_set_diagnostics(int on);
 
 /* Synchronises `stream`, reads and clears the device error word.  LSHMOE_EDEVICE if a kernel
    latched an error since the last check. */

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 __all__ = ["LayerConfig", "CONFIGS", "make_centers", "make_tokens", "make_gate", "make_experts",
-           "rotation_seed", "make_rank_inputs", "torch_dtype"]
+           "rotation_seed", "make_rank_inputs", "torch_dtype", "make_codes", "make_zipf_gate"]
 
 
 @dataclass(frozen=True)
@@ -129,3 +129,44 @@ def make_rank_inputs(cfg: LayerConfig, master_seed: int, rank: int = 0, with_wei
     X = make_tokens(cfg, master_seed, rank)
     zeta, g = make_gate(cfg, master_seed, X, with_weights)
     return X, zeta, g
+
+
+def make_codes(n: int, q: int, d: int, master_seed: int, C: int = 512, p_noise: float = 0.1,
+               iid: bool = False) -> np.ndarray:
+    """Synthetic hash codes int16 [n, q] with the bucket structure of the paper's workloads, for
+    stage-isolated tests of compress at sizes where hashing in the oracle would be slow: token t
+    belongs to a Zipf(1.0) component; each (component, j) has a fixed code, replaced by a
+    uniformly random one with probability p_noise (tokens near a cross-polytope cell border).
+    iid=True draws every code uniformly.  Codes are in {+-1..+-d}; nothing here hashes."""
+    rng = _rng(master_seed, 5)
+    def rand_codes(shape):
+        mag = rng.integers(1, d + 1, size=shape)
+        return np.where(rng.random(shape) < 0.5, -mag, mag)
+    if iid:
+        return rand_codes((n, q)).astype(np.int16)
+    w = 1.0 / np.arange(1, C + 1, dtype=np.float64)
+    comp = rng.choice(C, size=n, p=w / w.sum())
+    base = rand_codes((C, q))
+    codes = base[comp]
+    noise = rng.random((n, q)) < p_noise
+    codes = np.where(noise, rand_codes((n, q)), codes)
+    return codes.astype(np.int16)
+
+
+def make_zipf_gate(n: int, k: int, E: int, master_seed: int, hot: float = 0.0) -> torch.Tensor:
+    """zeta int32 [n, k]: k distinct experts per token (ascending), drawn Zipf(1.0)-skewed over
+    experts; with hot > 0 that fraction of tokens always routes to expert E-1 (skew stress)."""
+    rng = _rng(master_seed, 6)
+    w = 1.0 / np.arange(1, E + 1, dtype=np.float64)
+    p = w / w.sum()
+    out = np.empty((n, k), np.int32)
+    for t in range(n):
+        out[t] = np.sort(rng.choice(E, size=k, replace=False, p=p))
+    if hot > 0:
+        idx = np.nonzero(rng.random(n) < hot)[0]
+        for t in idx:
+            if (out[t] == E - 1).any():
+                continue
+            out[t, 0] = E - 1
+            out[t] = np.sort(out[t])
+    return torch.from_numpy(out)

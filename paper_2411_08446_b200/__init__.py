@@ -35,6 +35,7 @@ _vp, _i64, _i32, _u64, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctyp
 _SIGS = {
     "lshmoe_abi_version": ([], _i32),
     "lshmoe_kernel_launches": ([], _i64),
+    "lshmoe_set_diagnostics": ([_i32], None),
     "lshmoe_last_error": ([], ctypes.c_char_p),
     "lshmoe_check_device_error": ([_vp], _i32),
     "lshmoe_rotation": ([_i32, _i32, _u64, _i32, _vp], _i32),
@@ -173,20 +174,52 @@ class Compressed:
     centroids_f32: Optional[torch.Tensor]
 
 
-def compress_phase_times(workspace: torch.Tensor) -> list:
-    """Diagnostics: CTA 0's globaltimer stamps (ns) left in the workspace by the last compress:
-    start, then the exit of each grid barrier, then CTA 0's end.  Returns successive deltas (us)."""
-    raw = workspace[8:64].cpu().view(torch.int32).numpy().astype("int64") & 0xFFFFFFFF
-    out = []
-    for a, b in zip(raw[:-1], raw[1:]):
-        if b == 0xFFFFFFFF:
-            break
-        out.append(round(((int(b) - int(a)) & 0xFFFFFFFF) / 1e3, 2))
+_DIAG_WORD = 64 + 2048 + 512                      # compress.cu kDiag (int32 words)
+_DIAG_CTAS = 128                                  # CTAs recorded per kernel
+COMPRESS_DIAG_STAMPS = {"tiles": ["start", "end"],
+                        "bucket": ["start", "gathered", "rows_first", "rows_all", "ranked", "end", "sized", "tilescan"],
+                        "centroid": ["start", "indexed", "reduced", "end"]}
+
+
+def set_diagnostics(on: bool) -> None:
+    """lshmoe_set_diagnostics: per-CTA globaltimer stamps of compress's kernels (off by default)."""
+    _lib.lshmoe_set_diagnostics(1 if on else 0)
+
+
+def compress_diag(workspace: torch.Tensor) -> dict:
+    """Diagnostics: per-CTA stamps of the last compress launched with diagnostics on, in us
+    relative to the earliest stamp: {kernel: {stamp: [CTA] list (NaN if absent)}}."""
+    import numpy as np
+    raw = workspace[4 * _DIAG_WORD:4 * (_DIAG_WORD + 16 * 3 * _DIAG_CTAS)].cpu().view(torch.int32).numpy()
+    raw = raw.astype("int64").reshape(3, _DIAG_CTAS, 16) & 0xFFFFFFFF
+    ok = raw != 0xFFFFFFFF
+    if not ok.any():
+        return {}
+    t0 = raw[ok].min()
+    rel = np.where(ok, ((raw - t0) & 0xFFFFFFFF) / 1e3, np.nan)
+    return {kern: {nm: rel[ki, :, j].tolist() for j, nm in enumerate(names)}
+            for ki, (kern, names) in enumerate(COMPRESS_DIAG_STAMPS.items())}
+
+
+def compress_phase_times(workspace: torch.Tensor) -> dict:
+    """Per-kernel spans (us) of the last diagnostics-on compress: first CTA start -> last CTA end,
+    plus the gaps between kernels."""
+    import numpy as np
+    D = compress_diag(workspace)
+    if not D:
+        return {}
+    out, prev_end = {}, None
+    for kern, st in D.items():
+        s, e = np.nanmin(st["start"]), np.nanmax(st["end"])
+        if prev_end is not None:
+            out[f"gap_before_{kern}"] = round(float(s - prev_end), 2)
+        out[kern] = round(float(e - s), 2)
+        prev_end = e
     return out
 
 
 def compress_cta_times(workspace: torch.Tensor) -> dict:
-    """Diagnostics: per-CTA centroid-phase durations (us) from the last compress."""
+    """Diagnostics: per-CTA centroid-kernel durations (us) of the last diagnostics-on compress."""
     raw = workspace[256:256 + 8192].cpu().view(torch.int32).numpy().astype("int64") & 0xFFFFFFFF
     st, en = raw[0::2], raw[1::2]
     ok = (st != 0xFFFFFFFF) & (en != 0xFFFFFFFF)

@@ -55,6 +55,7 @@ extern "C" {
 int lshmoe_abi_version(void) { return LSHMOE_ABI_VERSION; }
 
 int64_t lshmoe_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+void lshmoe_set_diagnostics(int on) { set_compress_diag(on); }
 
 const char* lshmoe_last_error(void) { return g_last_error.c_str(); }
 

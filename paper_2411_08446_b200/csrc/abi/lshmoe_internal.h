@@ -22,13 +22,17 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
 size_t hash_workspace_bytes(int64_t n, int d, int q);
 
 struct CompressWs {            // carved from the caller's workspace by compress_workspace_layout
-  int32_t* table;              // [table_size] hash table of representative copy ids
-  int64_t table_size;          // power of two
-  int32_t* rep;                // [nk]
-  uint32_t* keys[2];           // [nk] radix keys (ping-pong)
-  int32_t* vals[2];            // [nk] radix values (ping-pong)
-  int32_t* rowid;              // [nk] centroid row of each first copy
-  int32_t* hist;               // [256 * nblocks_max]
+  int32_t* hdr;                // [kHdr] barrier counter, diagnostics stamps, cut-row arrival counters
+  int32_t* table;              // [table_size] hash table: slot -> first copy id (follows hdr)
+  int64_t table_size;          // power of two >= 2 n k
+  int32_t* tile_copy;          // [ntiles * 256] copy ids, each 256-copy tile stably grouped by expert
+  int32_t* tile_slot;          // [ntiles * 256] their hash-table slots
+  int32_t* tile_off;           // [ntiles][E + 1] start of each expert's run inside a tile
+  int32_t* rowid;              // [nk] local centroid row of each first copy (by copy id)
+  int32_t* rowl;               // [nk] local row of each perm position (permute mode: perm)
+  int32_t* rsl;                // [nk] perm position of each row's first member, at grp_off[e] + row
+  int32_t* gofs;               // [E] perm offset of each expert group
+  int32_t* big;                // [5][nk] phase-A arrays of groups too large for shared memory
   float* partial;              // [kMaxGrid][2][d] centroid partial sums of rows cut by CTA ranges
   size_t bytes;
 };
@@ -56,6 +60,7 @@ int launch_expert_ffn(const void* in, lshmoe_dtype dtype, int d, int d_ffn, cons
                       const void* b2, void* hidden, int64_t capacity, void* out, void* stream);
 
 int read_and_clear_device_error(int* value, void* stream);
+void set_compress_diag(int on);   // per-CTA globaltimer stamps in the compress workspace header
 void count_launches(int n);   // kernels launched by this library (lshmoe_kernel_launches)
 int device_sm_count();
 

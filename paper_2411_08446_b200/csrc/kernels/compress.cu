@@ -1,26 +1,31 @@
 // a3-a5: group the routed copies by expert, bucket them by their composite LSH key, and reduce
 // each bucket to its centroid (Alg. 1 L3, L5-L8: P:L520; §2.3).
 //
-// One cooperative, persistent kernel (all CTAs co-resident; grid barriers between phases), so
-// the whole step is one launch + one memset and needs no host synchronisation:
-//   P0 insert  : open-addressing hash table keyed by (expert, q-tuple of codes); each slot's value
-//                converges (atomicMin) to the smallest copy id c = t*k+s with that key = the
-//                bucket's first appearance in its expert group (reading R7).  slot_of[c] is kept,
-//                so later phases read rep[c] = table[slot_of[c]] without re-probing.
-//   P1 radix   : one stable counting-sort pass over key = expert (first copies) / E (others):
-//                the firsts land in (expert, first position) order, and that position IS the
-//                global centroid row (expert-major, first-appearance local ids); the digit totals
-//                give m_e and m.
-//   P2 radix   : stable LSD sort (8-bit digits, 2 passes for n*k <= 65536) of all copies by
-//                row = rowid[rep[c]] -> perm (ascending copy id within a row, reading R8), bucket.
-//   P3 centroid: perm split in one contiguous range per CTA; member rows are staged in shared
-//                memory by cp.async, summed in perm order in fp32, scaled once by RN(1/count)
-//                (reading R10) and rounded (RNE) into the send buffer.  Rows crossing ranges
-//                leave fp32 partials;
-//   P4 fix-up  : the CTA where such a row starts adds the partials in CTA order (deterministic).
-// Stable ranking inside a 1024-element radix tile: per-warp __match_any_sync + per-warp digit
-// counters in shared memory (a warp's rounds run in order), warp prefixes combined per digit;
-// tiles' histograms are published to global memory and every CTA derives its tiles' offsets.
+// Three kernels chained by programmatic dependent launch (PDL: each kernel's launch and prologue
+// overlap its predecessor's tail; cudaGridDependencySynchronize orders the data), one memset, no
+// host synchronisation:
+//   K1 tile_kernel   (one CTA per 256-copy tile): insert every copy into an open-addressing hash
+//                    table keyed by (expert, q-tuple of codes) whose slot value converges
+//                    (atomicMin) to the smallest copy id with that key = the bucket's first
+//                    appearance in its expert group (reading R7).  Lanes of a warp holding the same
+//                    key are merged by __match_any_sync first (one atomic per warp and key).  The
+//                    tile is stably grouped by expert in shared memory (warp match + per-warp digit
+//                    counters) and written out with its per-expert run offsets.
+//   K2 bucket_kernel (one 1024-thread CTA per expert): gather the expert's copies in ascending copy
+//                    id from the tiles' runs, flag first appearances (table[slot] == copy), number
+//                    them by an ordered ballot scan (local row ids), look up every copy's row, and
+//                    rank copies within rows in order (warps own contiguous sub-ranges;
+//                    __match_any_sync inside a warp, per-(warp,row) counters in shared memory,
+//                    prefix over warps) -> perm (grouped by row, ascending copy id within, reading
+//                    R8) and row starts.
+//   K3 centroid_kernel (one CTA per SM): perm split into one contiguous range per CTA; member
+//                    rows are staged in shared memory by cp.async, summed in perm order in fp32,
+//                    scaled once by RN(1/count) (reading R10) and rounded (RNE) into the send
+//                    buffer.  Rows crossing CTA ranges leave fp32 partials; the last CTA to finish
+//                    such a row (arrival counter) adds them in CTA order, so the summation order
+//                    never depends on timing.
+// The uncompressed baseline (permute mode) runs K1 without the hash table, K2 as a pure ordered
+// gather (slot = group offset + rank), then a gather of the token rows into the send buffer.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -32,16 +37,20 @@
 namespace lshmoe {
 namespace {
 
-constexpr int kThreads = 256;            // == kRadix: one thread per digit in the offset step
-constexpr int kRadix = 256;
-constexpr int kIPT = 4;                  // max radix items per thread per tile (runtime P.ipt <= kIPT)
-constexpr int kMinTile = kThreads;       // smallest tile (ipt = 1): sizes the histogram workspace
-constexpr int kHistTiles = 64;           // tile histograms staged in shared memory up to this many
-constexpr int kHistPitch = kHistTiles + 1;
-constexpr int kHistSmem = kRadix * kHistPitch * 4;
+constexpr int kThreads = 256;            // K1 / K3 threads per CTA; K1 tile = 256 copies
+constexpr int kTile = kThreads;
+constexpr int kRadix = 256;              // expert digits per tile (E + sentinel <= 256)
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxE = 255;               // expert digit + sentinel fit one 8-bit pass
-constexpr int kHdr = 64 + 2048;          // workspace header ints: barrier counter, phase + per-CTA stamps
+constexpr int kBThreads = 1024;          // K2 threads per CTA
+constexpr int kBWarps = kBThreads / 32;
+constexpr int kMaxE = 255;
+constexpr int kMaxGrid = 512;            // K3 CTAs (one per SM) <= this
+// Workspace header (int32 words), memset to 0xFF (= -1) before every compress:
+// [2..16) stamps, [64, 64 + 2*1024) K3 per-CTA stamps, [kArrive, +kMaxGrid) arrival counters of
+// rows cut by K3's CTA ranges, [kDiag, +16*kMaxGrid) per-CTA diagnostics stamps.
+constexpr int kArrive = 64 + 2048;
+constexpr int kDiag = kArrive + kMaxGrid;
+constexpr int kHdr = kDiag + 16 * kMaxGrid;
 
 // Device error word (read by lshmoe_check_device_error).  Bit 0: expert id outside [0, E)
 // (S:L312).  Only this translation unit validates expert ids.
@@ -68,18 +77,8 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
   h ^= h >> 16;
   return h;
 }
-__device__ __forceinline__ uint32_t key_hash(int e, const int16_t* c, int q) {
-  uint32_t h = fmix32(static_cast<uint32_t>(e) + 0x9E3779B9u);
-  for (int i = 0; i < q; ++i) h = fmix32(h ^ (static_cast<uint32_t>(static_cast<uint16_t>(c[i])) + (i << 16)));
-  return h;
-}
-__device__ __forceinline__ bool codes_equal(const int16_t* a, const int16_t* b, int q) {
-  for (int i = 0; i < q; ++i)
-    if (a[i] != b[i]) return false;
-  return true;
-}
 
-// Data written by other CTAs in an earlier phase is read with ld.global.cg (L2, not L1).
+// Data written by other CTAs / earlier kernels of the chain is read with ld.global.cg.
 template <typename T>
 __device__ __forceinline__ T ldcg(const T* p) { return __ldcg(p); }
 
@@ -90,7 +89,7 @@ struct Params {
   const int16_t* codes;
   int q;
   const int32_t* experts;
-  int k, E, nk;
+  int k, E, nk, ntiles;
   int32_t* bucket;                 // compress: [nk] row of copy; permute: slot
   int32_t* perm;
   int32_t* row_start;
@@ -100,232 +99,383 @@ struct Params {
   float* cent32;
   int32_t* table;
   uint32_t mask;
-  unsigned* bar;                   // grid-barrier counter, memset to 0xFFFFFFFF
-  int32_t* slot_of;
+  unsigned* bar;                   // workspace header (stamps, arrival counters)
+  int32_t* tile_copy;
+  int32_t* tile_slot;
+  int32_t* tile_off;
   int32_t* rowid;
-  uint32_t* keys[2];
-  int32_t* vals[2];
-  int32_t* hist;                   // [ntiles][256]
-  float* partial;                  // [G][2][d] partial sums of rows cut by CTA ranges
-  int ntiles, row_passes;
-  int max_range;                   // centroid: max perm entries per CTA range
-  int ipt;                         // radix elements per thread per tile (1, 2 or 4)
+  int32_t* rowl;
+  int32_t* rsl;
+  int32_t* gofs;
+  int32_t* big;
+  float* partial;                  // [G][2][d] partial sums of rows cut by K3's CTA ranges
+  int max_range;                   // K3: max perm entries per CTA range
+  int dyn_smem;                    // K2: dynamic shared memory bytes
   int permute;                     // 1: uncompressed baseline (group by expert only)
+  int diag;                        // 1: record per-CTA globaltimer stamps (diagnostics)
 };
 
-// Grid barrier over co-resident CTAs; the counter starts at 0xFFFFFFFF (memset) and barrier
-// number p completes when it reaches p * gridDim.x - 1.
 __device__ __forceinline__ unsigned globaltimer_lo() {
   unsigned t;
   asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(t));
   return t;
 }
-
-// bar[2 + p] (p = 0..13): CTA 0's globaltimer (ns, low 32 bits) at kernel start (p = 0) and on
-// leaving barrier p — a per-phase breakdown readable from the workspace (lshmoe_compress_phases).
-__device__ __forceinline__ void stamp(unsigned* bar, unsigned p) {
-  if (blockIdx.x == 0 && threadIdx.x == 0 && p < 14) bar[2 + p] = globaltimer_lo();
+// Diagnostics stamp j of CTA blockIdx.x of kernel `kern` (0: K1, 1: K2, 2: K3).
+__device__ __forceinline__ void dstamp(const Params& P, int kern, int j) {
+  if (P.diag && threadIdx.x == 0 && blockIdx.x < kMaxGrid / 4)
+    P.bar[kDiag + 16 * (blockIdx.x + kern * (kMaxGrid / 4)) + j] = globaltimer_lo();
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& phase) {
-  ++phase;
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Exclusive scan of one int per thread over a CTA of NW warps; *total = the sum.  s = [NW + 1].
+template <int NW>
+__device__ __forceinline__ int block_excl_scan(int v, int* s, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) s[wid] = x;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    // release this CTA's writes (ordered before by bar.sync), then acquire everyone else's
-    asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    const unsigned target = phase * gridDim.x - 1u;
-    unsigned v;
-    while (true) {
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-      if (static_cast<int>(v - target) >= 0) break;
-      __nanosleep(20);
+  if (wid == 0) {
+    const int w = lane < NW ? s[lane] : 0;
+    int z = w;
+#pragma unroll
+    for (int off = 1; off < NW; off <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, z, off);
+      if (lane >= off) z += y;
     }
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    stamp(bar, phase);
+    if (lane < NW) s[lane] = z - w;
+    if (lane == NW - 1) s[NW] = z;
   }
   __syncthreads();
+  const int r = s[wid] + x - v;
+  *total = s[NW];
+  __syncthreads();                         // s may be reused right away
+  return r;
 }
 
-enum PassKind { PASS_FIRSTS = 0, PASS_ROW0 = 1, PASS_ROWN = 2, PASS_PERMUTE = 3 };
+// ---- K1: hash-table insert + per-tile stable grouping by expert -----------------------------
+constexpr int kMaxQ = 16;                // LSHMOE_MAX_Q
 
-__device__ __forceinline__ void pass_key(const Params& P, int kind, int pass, int i, uint32_t& key, int32_t& val) {
-  if (kind == PASS_FIRSTS) {
-    const int e = load_expert_quiet(P.experts, i, P.E);
-    const int rep = ldcg(P.table + ldcg(P.slot_of + i));
-    key = rep == i ? static_cast<uint32_t>(e) : static_cast<uint32_t>(P.E);
-    val = i;
-  } else if (kind == PASS_ROW0) {
-    key = static_cast<uint32_t>(ldcg(P.rowid + ldcg(P.table + ldcg(P.slot_of + i))));
-    val = i;
-  } else if (kind == PASS_ROWN) {
-    key = ldcg(P.keys[(pass - 1) & 1] + i);
-    val = ldcg(P.vals[(pass - 1) & 1] + i);
-  } else {
-    key = static_cast<uint32_t>(load_expert(P.experts, i, P.E));
-    val = i;
+// Slot of copy c.  Lanes of `act` with the same (expert, key) are merged: the lowest such lane
+// (smallest copy id) inserts, the others take its slot.  key[] = the token's q codes.
+__device__ __forceinline__ int insert_copy(const Params& P, unsigned act, int c, int e, const int16_t* key) {
+  const int lane = threadIdx.x & 31;
+  uint32_t h = fmix32(static_cast<uint32_t>(e) + 0x9E3779B9u);
+#pragma unroll
+  for (int i = 0; i < kMaxQ; ++i)
+    if (i < P.q) h = fmix32(h ^ (static_cast<uint32_t>(static_cast<uint16_t>(key[i])) + (i << 16)));
+  const unsigned peers = __match_any_sync(act, h);
+  const int leader = __ffs(peers) - 1;
+  // confirm the whole key against the leader's (a 32-bit hash may collide inside a warp)
+  bool same = __shfl_sync(act, e, leader) == e;
+#pragma unroll
+  for (int i = 0; i < kMaxQ; ++i)
+    if (i < P.q) same &= __shfl_sync(act, static_cast<int>(key[i]), leader) == key[i];
+  const bool own = lane == leader || !same;
+  int slot = 0;
+  if (own) {
+    slot = static_cast<int>(h & P.mask);
+    while (true) {
+      const int cur = atomicCAS(&P.table[slot], -1, c);
+      if (cur < 0) break;                    // claimed an empty slot
+      // cur is a copy with this slot's key (a claimed slot never changes key)
+      bool eq = load_expert_quiet(P.experts, cur, P.E) == e;
+      const int16_t* oc = P.codes + static_cast<int64_t>(cur / P.k) * P.q;
+#pragma unroll
+      for (int i = 0; i < kMaxQ; ++i)
+        if (i < P.q) eq &= oc[i] == key[i];
+      if (eq) {
+        if (c < cur) atomicMin(&P.table[slot], c);
+        break;
+      }
+      slot = (slot + 1) & static_cast<int>(P.mask);
+    }
   }
+  const int ls = __shfl_sync(act, slot, leader);
+  return own ? slot : ls;
 }
 
-struct TileRank {
-  uint32_t key[kIPT];
-  int32_t val[kIPT];
-  int dg[kIPT];
-  int loc[kIPT];
-};
-
-// Stable ranks of the elements of one tile by digit; leaves per-warp digit counts in wcnt.
-__device__ __forceinline__ void rank_tile(const Params& P, int kind, int pass, int tile, int n, int shift,
-                                          int (*wcnt)[kRadix], TileRank& tr) {
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int i = threadIdx.x; i < kWarps * kRadix; i += kThreads) (&wcnt[0][0])[i] = 0;
-  __syncthreads();
+__global__ void __launch_bounds__(kThreads) tile_kernel(Params P) {
+  __shared__ int wcnt[kWarps][kRadix];
+  __shared__ int s_off[kRadix];
+  __shared__ int s_scan[kWarps + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  const int base = tile * (kThreads * P.ipt) + warp * (P.ipt * 32);
+  const int E1 = P.E + 1;
+  const int t = blockIdx.x;
+  dstamp(P, 0, 0);
+  const int c = t * kTile + tid;
+  const bool ok = c < P.nk;
+  const int e = ok ? load_expert(P.experts, c, P.E) : P.E;   // digit E = past the end
+  int16_t key[kMaxQ];
+  if (ok && !P.permute) {
+    const int16_t* mc = P.codes + static_cast<int64_t>(c / P.k) * P.q;
 #pragma unroll
-  for (int r = 0; r < kIPT; ++r) {   // all key loads in flight before the ordered ranking rounds
-    const int i = base + r * 32 + lane;
-    if (r < P.ipt && i < n) pass_key(P, kind, pass, i, tr.key[r], tr.val[r]);
+    for (int i = 0; i < kMaxQ; ++i)
+      if (i < P.q) key[i] = mc[i];
   }
-#pragma unroll
-  for (int r = 0; r < kIPT; ++r) {
-    const int i = base + r * 32 + lane;
-    const bool ok = r < P.ipt && i < n;
-    tr.dg[r] = ok ? static_cast<int>((tr.key[r] >> shift) & (kRadix - 1)) : kRadix;
-    const unsigned peers = __match_any_sync(0xFFFFFFFFu, tr.dg[r]);
-    const int leader = __ffs(peers) - 1;
-    int b = 0;
-    if (ok) b = wcnt[warp][tr.dg[r]];
-    __syncwarp();
-    if (ok && lane == leader) wcnt[warp][tr.dg[r]] = b + __popc(peers);
-    __syncwarp();
-    tr.loc[r] = b + __popc(peers & lt);
+  for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  // stable rank of the copy among the tile's copies of its expert (one 32-copy round per warp)
+  const unsigned peers = __match_any_sync(0xFFFFFFFFu, e);
+  if (lane == __ffs(peers) - 1) wcnt[warp][e] = __popc(peers);
+  __syncthreads();
+  int tot = 0;
+  if (tid < E1) {                          // prefix over warps, per expert digit
+    for (int w = 0; w < kWarps; ++w) {
+      const int v = wcnt[w][tid];
+      wcnt[w][tid] = tot;
+      tot += v;
+    }
+  }
+  int all;
+  const int excl = block_excl_scan<kWarps>(tid < E1 ? tot : 0, s_scan, &all);
+  if (tid < E1) {
+    s_off[tid] = excl;
+    P.tile_off[static_cast<int64_t>(t) * E1 + tid] = excl;
   }
   __syncthreads();
+  const unsigned act = __ballot_sync(0xFFFFFFFFu, ok);
+  int slot = 0;
+  if (ok && !P.permute) slot = insert_copy(P, act, c, e, key);
+  if (ok) {
+    const int dest = t * kTile + s_off[e] + wcnt[warp][e] + __popc(peers & lt);
+    P.tile_copy[dest] = c;
+    P.tile_slot[dest] = slot;
+  }
+  dstamp(P, 0, 1);
 }
 
-// One stable counting-sort pass over n elements (key digit at `shift`), all CTAs cooperating.
-__device__ void radix_pass(const Params& P, int kind, int pass, int n, int shift, unsigned& phase,
-                           int (*wcnt)[kRadix], int* s_off, int* s_tot) {
-  const int ntiles = (n + kThreads * P.ipt - 1) / (kThreads * P.ipt);
-  const int tpad = (ntiles + 3) & ~3;          // hist is digit-major [256][tpad]: 128-bit row loads
-  const bool one_tile = ntiles <= static_cast<int>(gridDim.x);   // keep ranks in registers
-  extern __shared__ int s_hist[];              // [256][kHistPitch] when tpad <= kHistTiles
-  TileRank tr;
-  // (a) tile histograms
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    rank_tile(P, kind, pass, t, n, shift, wcnt, tr);
-    int s = 0;
-    for (int w = 0; w < kWarps; ++w) s += wcnt[w][threadIdx.x];
-    P.hist[threadIdx.x * tpad + t] = s;
-    if (!one_tile) __syncthreads();
-  }
-  grid_barrier(P.bar, phase);
-  // (b) offsets + stable scatter
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int dgt = threadIdx.x;
-    int tot = 0, pre = 0;
-    if (tpad <= kHistTiles) {   // whole table -> shared memory with coalesced 128-bit loads
-      const int n4 = kRadix * tpad / 4;          // <= 16 * kThreads
-      int4 v[16];
+// ---- K2: per-expert ordered bucketing ------------------------------------------------------
+extern __shared__ __align__(1024) uint8_t g_dsmem[];
+
+// Ordered gather of expert e's copies (and their slots) from the tiles' runs.
+__device__ void gather_group(const Params& P, int e, int32_t* mem, int32_t* aux, int* s_tb, int* s_ta,
+                             int* s_scan) {
+  const int tid = threadIdx.x;
+  const int E1 = P.E + 1;
+  int base = 0;
+  for (int t0 = 0; t0 < P.ntiles; t0 += kBThreads) {
+    const int t = t0 + tid;
+    int a = 0, cnt = 0;
+    if (t < P.ntiles) {
+      a = ldcg(P.tile_off + static_cast<int64_t>(t) * E1 + e);
+      cnt = ldcg(P.tile_off + static_cast<int64_t>(t) * E1 + e + 1) - a;
+    }
+    int tot;
+    const int excl = block_excl_scan<kBWarps>(cnt, s_scan, &tot);
+    s_tb[tid] = excl;
+    s_ta[tid] = a;
+    __syncthreads();
+    const int nt = min(kBThreads, P.ntiles - t0);
+    dstamp(P, 1, 7);
+    // flattened (tile, entry) space: thread owns entries i = tid + 1024 j, 8 gathers in flight;
+    // tile of entry i = the last tile with s_tb <= i (branchless search, all j interleaved)
+    int top = 1;
+    while (top * 2 < nt) top *= 2;
+    for (int i0 = 0; i0 < tot; i0 += 8 * kBThreads) {
+      int lo[8];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {             // all loads first: one round trip
-        const int j = threadIdx.x + i * kThreads;
-        v[i] = j < n4 ? __ldcg(reinterpret_cast<const int4*>(P.hist) + j) : make_int4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int j = threadIdx.x + i * kThreads;
-        if (j < n4) {
-          const int e = 4 * j, dd = e / tpad, col = e - dd * tpad;
-          int* dst = s_hist + dd * kHistPitch + col;
-          dst[0] = v[i].x; dst[1] = v[i].y; dst[2] = v[i].z; dst[3] = v[i].w;
-        }
-      }
-      __syncthreads();
-      const int* row = s_hist + dgt * kHistPitch;   // pitch 65: conflict-free column walk
-      for (int u = 0; u < ntiles; ++u) {
-        if (u == t) pre = tot;
-        tot += row[u];
-      }
-    } else {
-      const int4* hrow = reinterpret_cast<const int4*>(P.hist + dgt * tpad);
-      for (int u0 = 0; u0 < tpad; u0 += 32) {   // up to 8 x 128-bit loads in flight
-        int4 v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = u0 + 4 * j < tpad ? __ldcg(hrow + u0 / 4 + j) : make_int4(0, 0, 0, 0);
+      for (int j = 0; j < 8; ++j) lo[j] = 0;
+      const int nj = min(8, (tot - i0 - tid + kBThreads - 1) / kBThreads);   // entries of this thread
+      for (int step = top; step >= 1; step >>= 1) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+          const int i = i0 + j * kBThreads + tid;
+          if (j < nj && lo[j] + step < nt && s_tb[lo[j] + step] <= i) lo[j] += step;
+        }
+      }
+      int cc[8], ss[8];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int u = u0 + 4 * j + i;
-            if (u == t) pre = tot;
-            if (u < ntiles) tot += e[i];
-          }
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + j * kBThreads + tid;
+        if (j < nj) {
+          const int src = (t0 + lo[j]) * kTile + s_ta[lo[j]] + (i - s_tb[lo[j]]);
+          cc[j] = ldcg(P.tile_copy + src);
+          ss[j] = ldcg(P.tile_slot + src);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + j * kBThreads + tid;
+        if (j < nj) {
+          mem[base + i] = cc[j];
+          aux[base + i] = ss[j];
         }
       }
     }
-    // exclusive scan of the 256 digit totals: warp shuffles + one cross-warp step
-    {
-      const int lane = dgt & 31, wid = dgt >> 5;
-      int x = tot;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xFFFFFFFFu, x, off);
-        if (lane >= off) x += y;
-      }
-      if (lane == 31) s_tot[wid] = x;
-      __syncthreads();
-      int base = 0;
-      for (int w = 0; w < wid; ++w) base += s_tot[w];
-      s_tot[32 + dgt] = base + x;           // inclusive
-    }
-    const int excl = s_tot[32 + dgt] - tot;
-    s_off[dgt] = excl + pre;
-    if (kind == PASS_ROW0 && t == 0 && threadIdx.x == 0) P.bar[20] = globaltimer_lo();   // diagnostics
-    if (t == 0 && (kind == PASS_FIRSTS || kind == PASS_PERMUTE)) {
-      if (dgt < P.E) P.expert_rows[dgt] = tot;
-      if (kind == PASS_FIRSTS && dgt == P.E) *P.num_rows = excl;   // firsts precede the sentinel digit
-    }
-    if (one_tile) __syncthreads();
-    else rank_tile(P, kind, pass, t, n, shift, wcnt, tr);
-    {   // warp-exclusive prefix per digit
-      int run = 0;
-      for (int w = 0; w < kWarps; ++w) {
-        const int v = wcnt[w][dgt];
-        wcnt[w][dgt] = run;
-        run += v;
-      }
-    }
+    base += tot;
     __syncthreads();
-    const int warp = threadIdx.x / 32;
-#pragma unroll
-    for (int r = 0; r < kIPT; ++r) {
-      if (tr.dg[r] == kRadix) continue;
-      const int dest = s_off[tr.dg[r]] + wcnt[warp][tr.dg[r]] + tr.loc[r];
-      const uint32_t key = tr.key[r];
-      const int32_t val = tr.val[r];
-      if (kind == PASS_FIRSTS) {
-        if (key < static_cast<uint32_t>(P.E)) P.rowid[val] = dest;
-      } else if (kind == PASS_PERMUTE) {
-        P.bucket[val] = dest;                 // slot of copy val
-        P.vals[0][dest] = val;
-      } else {
-        if (kind == PASS_ROW0) P.bucket[val] = static_cast<int32_t>(key);
-        if (pass == P.row_passes) {           // last pass: sorted rows + perm (+ token ids)
-          P.keys[pass & 1][dest] = key;
-          P.perm[dest] = val;
-          P.vals[pass & 1][dest] = val / P.k;
-        } else {
-          P.keys[pass & 1][dest] = key;
-          P.vals[pass & 1][dest] = val;
-        }
-      }
-    }
-    __syncthreads();
-    if (kind == PASS_ROW0 && t == 0 && threadIdx.x == 0) P.bar[21] = globaltimer_lo();   // diagnostics
   }
-  grid_barrier(P.bar, phase);
+}
+
+__global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
+  __shared__ int s_tb[kBThreads];
+  __shared__ int s_ta[kBThreads];
+  __shared__ int s_scan[kBWarps + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int e = blockIdx.x;
+  const int E1 = P.E + 1;
+  pdl_wait();                               // K1's tiles and table are complete and visible
+  dstamp(P, 1, 0);
+  // group size and offset: one column of the tile offsets
+  int n_e, goff;
+  {
+    int cnt = 0, a = 0;
+    for (int t = tid; t < P.ntiles; t += kBThreads) {
+      const int x0 = ldcg(P.tile_off + static_cast<int64_t>(t) * E1 + e);
+      cnt += ldcg(P.tile_off + static_cast<int64_t>(t) * E1 + e + 1) - x0;
+      a += x0;
+    }
+    block_excl_scan<kBWarps>(cnt, s_scan, &n_e);
+    block_excl_scan<kBWarps>(a, s_scan, &goff);   // copies of experts < e = the group's perm offset
+  }
+  dstamp(P, 1, 6);
+  int32_t *mem, *aux, *row, *rs, *wcnt;
+  const bool in_smem = static_cast<int64_t>(20) * n_e <= P.dyn_smem;
+  if (in_smem) {
+    int32_t* s = reinterpret_cast<int32_t*>(g_dsmem);
+    mem = s; aux = s + n_e; row = s + 2 * n_e; rs = s + 3 * n_e; wcnt = s + 4 * n_e;
+  } else {
+    mem = P.big + goff; aux = P.big + P.nk + goff; row = P.big + 2 * P.nk + goff;
+    rs = P.big + 3 * P.nk + goff; wcnt = P.big + 4 * P.nk + goff;
+  }
+  gather_group(P, e, mem, aux, s_tb, s_ta, s_scan);
+  dstamp(P, 1, 1);
+  if (tid == 0) P.gofs[e] = goff;
+  if (P.permute) {                        // baseline: slot = group offset + rank in the group
+    for (int i = tid; i < n_e; i += kBThreads) {
+      const int c = mem[i];
+      P.bucket[c] = goff + i;
+      P.rowl[goff + i] = c;
+    }
+    if (tid == 0) P.expert_rows[e] = n_e;
+    return;
+  }
+  // first copy of every member's bucket (the table is final)
+  for (int i0 = 0; i0 < n_e; i0 += 8 * kBThreads) {
+    int v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = i0 + j * kBThreads + tid;
+      if (i < n_e) v[j] = ldcg(P.table + aux[i]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = i0 + j * kBThreads + tid;
+      if (i < n_e) aux[i] = v[j];
+    }
+  }
+  __syncthreads();
+  // local row ids of the first appearances, in member order: warp w owns a contiguous span,
+  // counts its firsts by ballots, a block scan gives each warp its base, a second pass numbers.
+  const int span = ((n_e + kBWarps - 1) / kBWarps + 31) & ~31;
+  const int w0 = min(n_e, warp * span), w1 = min(n_e, w0 + span);
+  int nf = 0;
+  for (int b = w0; b < w1; b += 32) {
+    const int i = b + lane;
+    nf += __popc(__ballot_sync(0xFFFFFFFFu, i < w1 && aux[i] == mem[i]));
+  }
+  int m_e;
+  int lr = block_excl_scan<kBWarps>(lane == 0 ? nf : 0, s_scan, &m_e);
+  lr = __shfl_sync(0xFFFFFFFFu, lr, 0);
+  for (int b = w0; b < w1; b += 32) {
+    const int i = b + lane;
+    const bool f = i < w1 && aux[i] == mem[i];
+    const unsigned fb = __ballot_sync(0xFFFFFFFFu, f);
+    if (f) {
+      const int r = lr + __popc(fb & lt);
+      row[i] = r;
+      P.rowid[mem[i]] = r;
+    }
+    lr += __popc(fb);
+  }
+  __syncthreads();
+  dstamp(P, 1, 2);
+  for (int i0 = 0; i0 < n_e; i0 += 8 * kBThreads) {   // the other members look their row up
+    int v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = i0 + j * kBThreads + tid;
+      v[j] = -1;
+      if (i < n_e && aux[i] != mem[i]) v[j] = ldcg(P.rowid + aux[i]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = i0 + j * kBThreads + tid;
+      if (v[j] >= 0) row[i] = v[j];
+    }
+  }
+  // rank inside rows: W warps own contiguous sub-ranges; per-(warp, row) counters
+  int W;
+  if (in_smem) {
+    W = static_cast<int>(min(static_cast<int64_t>(kBWarps), (P.dyn_smem - static_cast<int64_t>(16) * n_e) / (4 * max(m_e, 1))));
+  } else {
+    W = min(kBWarps, P.dyn_smem / (4 * max(m_e, 1)));
+    if (W >= 1) wcnt = reinterpret_cast<int32_t*>(g_dsmem);
+    else W = 1;                            // counters stay in the workspace
+  }
+  const int sub = (n_e + W - 1) / W;
+  for (int i = tid; i < W * m_e; i += kBThreads) wcnt[i] = 0;
+  __syncthreads();
+  dstamp(P, 1, 3);
+  if (warp < W) {
+    int32_t* wc = wcnt + warp * m_e;
+    const int b0 = warp * sub, b1 = min(n_e, b0 + sub);
+    for (int base = b0; base < b1; base += 32) {
+      const int i = base + lane;
+      const bool ok = i < b1;
+      const int r = ok ? row[i] : -1;
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, r);
+      const int leader = __ffs(peers) - 1;
+      const int b = ok ? wc[r] : 0;
+      __syncwarp();
+      if (ok && lane == leader) wc[r] = b + __popc(peers);
+      __syncwarp();
+      if (ok) aux[i] = b + __popc(peers & lt);
+    }
+  }
+  __syncthreads();
+  dstamp(P, 1, 4);
+  for (int r = tid; r < m_e; r += kBThreads) {   // warp prefixes per row; row sizes
+    int run = 0;
+    for (int w = 0; w < W; ++w) {
+      const int v = wcnt[w * m_e + r];
+      wcnt[w * m_e + r] = run;
+      run += v;
+    }
+    rs[r] = run;
+  }
+  __syncthreads();
+  {                                              // row starts: ordered scan of the row sizes
+    const int rper = (m_e + kBThreads - 1) / kBThreads;
+    const int r0 = min(m_e, tid * rper), r1 = min(m_e, r0 + rper);
+    int sz = 0;
+    for (int r = r0; r < r1; ++r) sz += rs[r];
+    int tot;
+    int run = block_excl_scan<kBWarps>(sz, s_scan, &tot);
+    for (int r = r0; r < r1; ++r) {
+      const int v = rs[r];
+      rs[r] = run;
+      P.rsl[goff + r] = goff + run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n_e; i += kBThreads) {
+    const int r = row[i];
+    const int pos = goff + rs[r] + wcnt[(i / sub) * m_e + r] + aux[i];
+    P.perm[pos] = mem[i];
+    P.rowl[pos] = r;
+  }
+  if (tid == 0) P.expert_rows[e] = m_e;
+  dstamp(P, 1, 5);
 }
 
 // ---- centroid phase ------------------------------------------------------------------------
@@ -507,10 +657,6 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
     const uint32_t next = X.row_at(p + 1);
     if (next == row && p + 1 < w_end) continue;         // the segment goes on
     const bool head = seg_start > w_begin || X.prev_row != row;   // the row starts in this warp
-    if (cb == 0 && lane == 0) {
-      if (head) P.row_start[row] = seg_start;
-      if (p + 1 == P.nk) P.row_start[row + 1] = P.nk;   // row_start[m] = n*k
-    }
     if (head && next != row) {                // the whole row lies in this warp's sub-range
       const float rc = __frcp_rn(static_cast<float>(p + 1 - seg_start));
 #pragma unroll
@@ -600,10 +746,22 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
   __syncthreads();                            // the ring is reused by the next column block
 }
 
+// Expert whose perm range holds position p (s_goff[e] <= p < s_goff[e + 1]).
+__device__ __forceinline__ int expert_at(const int* s_goff, int E, int p) {
+  int lo = 0, hi = E - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_goff[mid] <= p) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Phase B of one CTA: its perm range's rows (global ids = row offset of the expert + local row),
+// token ids and bucket outputs, then the centroid reduction.  s_cut[0..1] receive the (expert,
+// local row) of the range's first and last entries for the cut-row merge.
 template <typename T>
-__device__ void centroid_phase(const Params& P, const uint32_t* rows, const int32_t* tok) {
+__device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_roff, int* s_cut, CentroidCtx& X) {
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
-  CentroidCtx X;
   X.p_begin = range_begin(b, P.nk, G);
   X.p_end = range_begin(b + 1, P.nk, G);
   X.range = X.p_end - X.p_begin;
@@ -615,10 +773,23 @@ __device__ void centroid_phase(const Params& P, const uint32_t* rows, const int3
   int32_t* s_tok = X.s_tok();
   for (int i = tid; i < X.range + 2; i += kThreads) {
     const int p = X.p_begin - 1 + i;
-    s_row[i] = (p >= 0 && p < P.nk) ? ldcg(rows + p) : 0xFFFFFFFFu;
+    uint32_t row = 0xFFFFFFFFu;
+    if (p >= 0 && p < P.nk) {
+      const int e = expert_at(s_goff, P.E, p);
+      const int lr = ldcg(P.rowl + p);
+      row = static_cast<uint32_t>(s_roff[e] + lr);
+      if (i >= 1 && i <= X.range) {
+        const int c = ldcg(P.perm + p);
+        s_tok[i - 1] = c / P.k;
+        P.bucket[c] = static_cast<int32_t>(row);
+        if (i == 1) { s_cut[0] = e; s_cut[1] = lr; }
+        if (i == X.range) { s_cut[2] = e; s_cut[3] = lr; }
+      }
+    }
+    s_row[i] = row;
   }
-  for (int i = tid; i < X.range; i += kThreads) s_tok[i] = ldcg(tok + X.p_begin + i);
   __syncthreads();
+  dstamp(P, 2, 1);
   X.w_begin = X.wbeg(X.w);
   X.w_end = X.wbeg(X.w + 1);
   X.prev_row = X.row_at(X.w_begin - 1);
@@ -633,150 +804,202 @@ __device__ void centroid_phase(const Params& P, const uint32_t* rows, const int3
   }
 }
 
-// Rows cut by CTA ranges: the CTA in which such a row starts adds the partials in CTA order.
+// Rows cut by CTA ranges: each CTA holding a piece publishes its fp32 partial (centroid_block),
+// then arrives on the counter of the CTA where the row starts; the last arriver adds the
+// partials in CTA order (the same order whichever CTA arrives last) and stores the centroid.
 template <typename T>
-__device__ void fixup_phase(const Params& P, const uint32_t* rows) {
+__device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int* s_goff, const int* s_mrow,
+                               const int* s_cut, int* s_job) {
   constexpr int VC = sizeof(T) == 2 ? 4 : 2;
-  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
-  const int p_begin = range_begin(b, P.nk, G), p_end = range_begin(b + 1, P.nk, G);
-  if (p_end >= P.nk || p_end <= p_begin) return;
-  const uint32_t row = ldcg(rows + p_end - 1);
-  if (ldcg(rows + p_end) != row) return;               // the range's last row ends inside it
-  const int rs = ldcg(P.row_start + row);
-  if (rs < p_begin) return;                            // started in an earlier range: not the owner
-  const int re = ldcg(P.row_start + row + 1);
-  const int b1 = range_cta(re - 1, P.nk, G);
-  const int nc8 = P.row_bytes / 8;
-  for (int ch = tid; ch < nc8; ch += kThreads) {
-    float acc[VC];
-    const float* src = P.partial + (static_cast<int64_t>(b) * 2 + (rs == p_begin ? 0 : 1)) * P.d + ch * VC;
-#pragma unroll
-    for (int e = 0; e < VC; ++e) acc[e] = __ldcg(src + e);
-    for (int bb = b + 1; bb <= b1; ++bb) {
-      if (range_begin(bb + 1, P.nk, G) == range_begin(bb, P.nk, G)) continue;   // empty range (nk < G)
-      const float* s2 = P.partial + (static_cast<int64_t>(bb) * 2) * P.d + ch * VC;
-#pragma unroll
-      for (int e = 0; e < VC; ++e) acc[e] += __ldcg(s2 + e);
+  const int G = gridDim.x, tid = threadIdx.x;
+  if (X.range == 0) return;
+  __threadfence();                            // publish this CTA's partials before arriving
+  __syncthreads();
+  if (tid == 0) {
+    s_job[0] = s_job[4] = -1;
+    const uint32_t r0 = X.row_at(X.p_begin), rl = X.row_at(X.p_end - 1);
+    const bool before = X.row_at(X.p_begin - 1) == r0;
+    const bool after = X.row_at(X.p_end) == rl;
+    int nj = 0;
+    for (int which = 0; which < 2; ++which) {
+      if (which == 0 && !before) continue;
+      if (which == 1 && (!after || (before && rl == r0))) continue;
+      const int e = s_cut[2 * which], lr = s_cut[2 * which + 1];
+      const int rs = ldcg(P.rsl + s_goff[e] + lr);
+      const int re = lr + 1 < s_mrow[e] ? ldcg(P.rsl + s_goff[e] + lr + 1) : s_goff[e + 1];
+      const int b0 = range_cta(rs, P.nk, G), b1 = range_cta(re - 1, P.nk, G);
+      int expected = 0;
+      for (int bb = b0; bb <= b1; ++bb) expected += range_begin(bb + 1, P.nk, G) > range_begin(bb, P.nk, G);
+      const int old = atomicAdd(reinterpret_cast<int*>(P.bar) + kArrive + b0, 1);   // counters start at -1
+      if (old + 2 == expected) {
+        __threadfence();                      // acquire the other CTAs' partials
+        s_job[4 * nj + 0] = static_cast<int>(which == 0 ? r0 : rl);
+        s_job[4 * nj + 1] = rs;
+        s_job[4 * nj + 2] = re;
+        s_job[4 * nj + 3] = b0 | (b1 << 16);
+        ++nj;
+      }
     }
-    store_chunk8<T>(P, static_cast<int>(row), ch, acc, static_cast<float>(re - rs));
+  }
+  __syncthreads();
+  for (int j = 0; j < 2; ++j) {
+    const int row = s_job[4 * j];
+    if (row < 0) break;
+    const int rs = s_job[4 * j + 1], re = s_job[4 * j + 2];
+    const int b0 = s_job[4 * j + 3] & 0xFFFF, b1 = s_job[4 * j + 3] >> 16;
+    const int nc8 = P.row_bytes / 8;
+    for (int ch = tid; ch < nc8; ch += kThreads) {
+      float acc[VC];
+      const float* src = P.partial + (static_cast<int64_t>(b0) * 2 + (rs == range_begin(b0, P.nk, G) ? 0 : 1)) * P.d + ch * VC;
+#pragma unroll
+      for (int e = 0; e < VC; ++e) acc[e] = __ldcg(src + e);
+      for (int bb0 = b0 + 1; bb0 <= b1; bb0 += 8) {   // 8 partials in flight, added in CTA order
+        float tmp[8][VC];
+        bool used[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int bb = bb0 + u;
+          const bool use = bb <= b1 && range_begin(bb + 1, P.nk, G) > range_begin(bb, P.nk, G);   // skip empty ranges
+          const float* s2 = P.partial + (static_cast<int64_t>(bb) * 2) * P.d + ch * VC;
+#pragma unroll
+          used[u] = use;
+#pragma unroll
+          for (int e = 0; e < VC; ++e) tmp[u][e] = use ? __ldcg(s2 + e) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (used[u])
+#pragma unroll
+            for (int e = 0; e < VC; ++e) acc[e] += tmp[u][e];
+      }
+      store_chunk8<T>(P, row, ch, acc, static_cast<float>(re - rs));
+    }
   }
 }
 
-__device__ void insert_phase(const Params& P) {
-  for (int c = blockIdx.x * kThreads + threadIdx.x; c < P.nk; c += gridDim.x * kThreads) {
-    const int e = load_expert(P.experts, c, P.E);
-    const int16_t* mc = P.codes + static_cast<int64_t>(c / P.k) * P.q;
-    uint32_t slot = key_hash(e, mc, P.q) & P.mask;
-    while (true) {
-      int cur = *reinterpret_cast<volatile int32_t*>(&P.table[slot]);
-      if (cur < 0) {
-        const int old = atomicCAS(&P.table[slot], -1, c);
-        if (old < 0) break;                  // claimed an empty slot
-        cur = old;
-      }
-      // cur is a copy with this slot's key (a claimed slot never changes key)
-      if (load_expert_quiet(P.experts, cur, P.E) == e && codes_equal(P.codes + static_cast<int64_t>(cur / P.k) * P.q, mc, P.q)) {
-        if (c < cur) atomicMin(&P.table[slot], c);
-        break;
-      }
-      slot = (slot + 1) & P.mask;
-    }
-    P.slot_of[c] = static_cast<int32_t>(slot);
-  }
-}
 
 template <typename T>
-__device__ void gather_phase(const Params& P) {   // baseline: send[p] = x[token of copy at p]
+__device__ void gather_rows(const Params& P) {   // baseline: send[p] = x[token of copy at p]
   const int64_t work = static_cast<int64_t>(P.nk) * P.nch;
   for (int64_t w = blockIdx.x * int64_t(kThreads) + threadIdx.x; w < work; w += int64_t(gridDim.x) * kThreads) {
     const int p = static_cast<int>(w / P.nch);
     const int ch = static_cast<int>(w - int64_t(p) * P.nch);
-    const int t = ldcg(P.vals[0] + p) / P.k;
+    const int t = ldcg(P.rowl + p) / P.k;
     reinterpret_cast<uint4*>(P.cent + static_cast<int64_t>(p) * P.row_bytes)[ch] =
         __ldg(reinterpret_cast<const uint4*>(P.x + static_cast<int64_t>(t) * P.row_bytes) + ch);
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) compress_kernel(Params P) {
-  __shared__ int wcnt[kWarps][kRadix];
-  __shared__ int s_off[kRadix];
-  __shared__ int s_tot[kRadix + 32];
-  unsigned phase = 0;
-  stamp(P.bar, 0);
+// ---- K3 ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
+  __shared__ int s_goff[kRadix + 1];         // perm offset of each expert group
+  __shared__ int s_roff[kRadix + 1];         // first global row of each expert
+  __shared__ int s_mrow[kRadix];             // m_e
+  __shared__ int s_scan[kWarps + 1];
+  __shared__ int s_cut[4];
+  __shared__ int s_job[8];
+  const int tid = threadIdx.x;
+  pdl_wait();                                // K2's perm, rows and counts are complete
+  dstamp(P, 2, 0);
   if (P.permute) {
-    radix_pass(P, PASS_PERMUTE, 0, P.nk, 0, phase, wcnt, s_off, s_tot);
-    gather_phase<float>(P);
+    if (P.is_bf16) gather_rows<__nv_bfloat16>(P);
+    else gather_rows<float>(P);
     return;
   }
-  insert_phase(P);
-  grid_barrier(P.bar, phase);
-  radix_pass(P, PASS_FIRSTS, 0, P.nk, 0, phase, wcnt, s_off, s_tot);
-  for (int p = 1; p <= P.row_passes; ++p)
-    radix_pass(P, p == 1 ? PASS_ROW0 : PASS_ROWN, p, P.nk, 8 * (p - 1), phase, wcnt, s_off, s_tot);
-  const uint32_t* rows = P.keys[P.row_passes & 1];
-  const int32_t* tok = P.vals[P.row_passes & 1];    // token id of each perm entry
+  {
+    const int m_e = tid < P.E ? ldcg(P.expert_rows + tid) : 0;
+    int m;
+    const int ro = block_excl_scan<kWarps>(m_e, s_scan, &m);
+    if (tid < P.E) {
+      s_goff[tid] = ldcg(P.gofs + tid);
+      s_roff[tid] = ro;
+      s_mrow[tid] = m_e;
+    }
+    if (tid == 0) {
+      s_goff[P.E] = P.nk;
+      s_roff[P.E] = m;
+      if (blockIdx.x == 0) {
+        *P.num_rows = m;
+        P.row_start[m] = P.nk;                // row_start[m] = n*k
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = blockIdx.x; e < P.E; e += gridDim.x)   // row_start of every global row
+    for (int r = tid; r < s_mrow[e]; r += kThreads) P.row_start[s_roff[e] + r] = ldcg(P.rsl + s_goff[e] + r);
   // per-CTA centroid-phase start / end stamps (diagnostics, bar[64 + 2 * cta])
-  if (threadIdx.x == 0 && blockIdx.x < 1024) P.bar[64 + 2 * blockIdx.x] = globaltimer_lo();
-  if (P.is_bf16) centroid_phase<__nv_bfloat16>(P, rows, tok);
-  else centroid_phase<float>(P, rows, tok);
+  if (P.diag && tid == 0 && blockIdx.x < 1024) P.bar[64 + 2 * blockIdx.x] = globaltimer_lo();
+  CentroidCtx X;
+  if (P.is_bf16) {
+    centroid_phase<__nv_bfloat16>(P, s_goff, s_roff, s_cut, X);
+    dstamp(P, 2, 2);
+    merge_cut_rows<__nv_bfloat16>(P, X, s_goff, s_mrow, s_cut, s_job);
+  } else {
+    centroid_phase<float>(P, s_goff, s_roff, s_cut, X);
+    dstamp(P, 2, 2);
+    merge_cut_rows<float>(P, X, s_goff, s_mrow, s_cut, s_job);
+  }
   __syncthreads();
-  if (threadIdx.x == 0 && blockIdx.x < 1024) P.bar[65 + 2 * blockIdx.x] = globaltimer_lo();
-  grid_barrier(P.bar, phase);
-  if (P.is_bf16) fixup_phase<__nv_bfloat16>(P, rows);
-  else fixup_phase<float>(P, rows);
-  __syncthreads();
-  stamp(P.bar, phase + 1);   // CTA 0's end (other CTAs may still be finishing the fix-up)
+  dstamp(P, 2, 3);
+  if (P.diag && tid == 0 && blockIdx.x < 1024) P.bar[65 + 2 * blockIdx.x] = globaltimer_lo();
 }
 
-int bits_for(int64_t maxval) {   // bits needed to represent values in [0, maxval]
-  int b = 1;
-  while ((int64_t(1) << b) <= maxval) ++b;
-  return b;
-}
-
-constexpr int kMaxGrid = 512;            // CTAs of the cooperative kernel (one per SM) <= this
-
-// Dynamic shared memory: the radix offset step's tile histograms or the centroid ring, whichever
-// is larger (the phases run one after the other).
-constexpr int kMaxDynSmem = 214 * 1024;   // + the kernel's static shared memory <= 227 KB
-int coop_max_range(int nk) {
-  const int G = std::min(device_sm_count(), kMaxGrid);
+constexpr int kCentroidSmemMax = 200 * 1024;   // K3 dynamic smem + static <= 227 KB
+constexpr int kBucketSmem = 200 * 1024;        // K2 dynamic smem (+ 8 KB static)
+int centroid_grid() { return std::min(device_sm_count(), kMaxGrid); }
+int centroid_max_range(int nk) {
+  const int G = centroid_grid();
   return (nk + G - 1) / G + 1;
 }
-// Centroid-phase shared memory: per-warp rings, warp partials, the range's index arrays.
+// K3 shared memory: per-warp rings, warp partials, the range's index arrays.
 int centroid_smem(int max_range) {
   return kWarps * kQ * kRingSlot + kWarps * kWpartFloats * 4 + 4 * (2 * max_range + 2);
 }
-int coop_smem(int max_range) { return std::max(centroid_smem(max_range), kHistSmem); }
 
-int launch_coop(const Params& P, cudaStream_t st) {
-  static int configured = 0;                 // largest dynamic smem size set so far
-  const int max_range = coop_max_range(P.nk);
-  const int smem = coop_smem(max_range);
-  if (!P.permute && centroid_smem(max_range) > kMaxDynSmem) return cudaErrorInvalidValue;   // range too long
-  if (smem > configured) {
-    int err = cudaFuncSetAttribute(compress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err) return err;
-    configured = smem;
-  }
+int g_diag = 0;                              // lshmoe_set_diagnostics
+bool diag_enabled() { return g_diag != 0; }
+
+template <typename K>
+int launch_pdl(K kernel, int grid, int block, int smem, cudaStream_t st, const Params& p, bool pdl) {
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(std::min(device_sm_count(), kMaxGrid));   // one CTA per SM, all co-resident
-  cfg.blockDim = dim3(kThreads);
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  Params p = P;
-  p.max_range = max_range;
-  int err = cudaLaunchKernelEx(&cfg, compress_kernel, p);
+  cfg.numAttrs = pdl ? 1 : 0;
+  const int err = cudaLaunchKernelEx(&cfg, kernel, p);
   count_launches(1);
   return err;
 }
 
+int launch_chain(const Params& P, cudaStream_t st) {
+  static bool configured = false;
+  const int max_range = centroid_max_range(P.nk);
+  const int csmem = centroid_smem(max_range);
+  if (!P.permute && csmem > kCentroidSmemMax) return cudaErrorInvalidValue;   // range too long
+  if (!configured) {
+    int err = cudaFuncSetAttribute(centroid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCentroidSmemMax);
+    if (!err) err = cudaFuncSetAttribute(bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBucketSmem);
+    if (err) return err;
+    configured = true;
+  }
+  Params p = P;
+  p.max_range = max_range;
+  p.dyn_smem = kBucketSmem;
+  p.diag = diag_enabled() ? 1 : 0;
+  int err = launch_pdl(tile_kernel, P.ntiles, kThreads, 0, st, p, false);
+  if (!err) err = launch_pdl(bucket_kernel, P.E, kBThreads, kBucketSmem, st, p, true);
+  if (!err) err = launch_pdl(centroid_kernel, centroid_grid(), kThreads, P.permute ? 0 : csmem, st, p, true);
+  return err;
+}
+
 }  // namespace
+
+void set_compress_diag(int on) { g_diag = on ? 1 : 0; }
 
 int read_and_clear_device_error(int* value, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -789,37 +1012,39 @@ int read_and_clear_device_error(int* value, void* stream) {
 }
 
 size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, CompressWs* ws) {
-  (void)E;
   const int64_t nk = n * k;
   int64_t tsize = 1024;
   while (tsize < 2 * nk) tsize <<= 1;
-  const int64_t ntiles = (nk + kMinTile - 1) / kMinTile;   // upper bound over every ipt
+  const int64_t ntiles = (nk + kTile - 1) / kTile;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
     off += (bytes + 255) & ~size_t(255);
     return o;
   };
-  const size_t o_table = take(sizeof(int32_t) * (tsize + kHdr));   // + header: barrier counter, stamps
-  const size_t o_slot = take(sizeof(int32_t) * nk);
-  const size_t o_k0 = take(sizeof(uint32_t) * nk);
-  const size_t o_k1 = take(sizeof(uint32_t) * nk);
-  const size_t o_v0 = take(sizeof(int32_t) * nk);
-  const size_t o_v1 = take(sizeof(int32_t) * nk);
+  const size_t o_hdr = take(sizeof(int32_t) * (kHdr + tsize));   // header + hash table: one memset
+  const size_t o_tc = take(sizeof(int32_t) * ntiles * kTile);
+  const size_t o_ts = take(sizeof(int32_t) * ntiles * kTile);
+  const size_t o_to = take(sizeof(int32_t) * ntiles * (E + 1));
   const size_t o_rowid = take(sizeof(int32_t) * nk);
-  const size_t o_hist = take(sizeof(int32_t) * kRadix * ((ntiles + 3) & ~int64_t(3)) + 64);
+  const size_t o_rowl = take(sizeof(int32_t) * nk);
+  const size_t o_rsl = take(sizeof(int32_t) * nk);
+  const size_t o_gofs = take(sizeof(int32_t) * (E + 1));
+  const size_t o_big = take(sizeof(int32_t) * 5 * nk);
   const size_t o_part = take(sizeof(float) * 2 * kMaxGrid * d);
   if (ws) {
     uint8_t* b = static_cast<uint8_t*>(base);
-    ws->table = reinterpret_cast<int32_t*>(b + o_table);
+    ws->hdr = reinterpret_cast<int32_t*>(b + o_hdr);
+    ws->table = ws->hdr + kHdr;
     ws->table_size = tsize;
-    ws->rep = reinterpret_cast<int32_t*>(b + o_slot);
-    ws->keys[0] = reinterpret_cast<uint32_t*>(b + o_k0);
-    ws->keys[1] = reinterpret_cast<uint32_t*>(b + o_k1);
-    ws->vals[0] = reinterpret_cast<int32_t*>(b + o_v0);
-    ws->vals[1] = reinterpret_cast<int32_t*>(b + o_v1);
+    ws->tile_copy = reinterpret_cast<int32_t*>(b + o_tc);
+    ws->tile_slot = reinterpret_cast<int32_t*>(b + o_ts);
+    ws->tile_off = reinterpret_cast<int32_t*>(b + o_to);
     ws->rowid = reinterpret_cast<int32_t*>(b + o_rowid);
-    ws->hist = reinterpret_cast<int32_t*>(b + o_hist);
+    ws->rowl = reinterpret_cast<int32_t*>(b + o_rowl);
+    ws->rsl = reinterpret_cast<int32_t*>(b + o_rsl);
+    ws->gofs = reinterpret_cast<int32_t*>(b + o_gofs);
+    ws->big = reinterpret_cast<int32_t*>(b + o_big);
     ws->partial = reinterpret_cast<float*>(b + o_part);
     ws->bytes = off;
   }
@@ -838,21 +1063,19 @@ static Params base_params(const void* x, lshmoe_dtype dtype, int64_t n, int d, c
   P.k = k;
   P.E = E;
   P.nk = static_cast<int>(n * k);
-  P.table = ws.table + kHdr;
-  P.bar = reinterpret_cast<unsigned*>(ws.table);
+  P.ntiles = (P.nk + kTile - 1) / kTile;
+  P.bar = reinterpret_cast<unsigned*>(ws.hdr);
+  P.table = ws.table;
   P.mask = static_cast<uint32_t>(ws.table_size - 1);
-  P.slot_of = ws.rep;
+  P.tile_copy = ws.tile_copy;
+  P.tile_slot = ws.tile_slot;
+  P.tile_off = ws.tile_off;
   P.rowid = ws.rowid;
-  P.keys[0] = ws.keys[0];
-  P.keys[1] = ws.keys[1];
-  P.vals[0] = ws.vals[0];
-  P.vals[1] = ws.vals[1];
-  P.hist = ws.hist;
+  P.rowl = ws.rowl;
+  P.rsl = ws.rsl;
+  P.gofs = ws.gofs;
+  P.big = ws.big;
   P.partial = ws.partial;
-  // elements per thread per radix tile: as few as possible while keeping <= 64 tiles (the tile
-  // histograms then fit in shared memory for the offset step)
-  P.ipt = P.nk <= kHistTiles * kThreads ? 1 : (P.nk <= 2 * kHistTiles * kThreads ? 2 : 4);
-  P.ntiles = (P.nk + kThreads * P.ipt - 1) / (kThreads * P.ipt);
   return P;
 }
 
@@ -860,7 +1083,7 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
                     const int32_t* experts, int k, int E, int32_t* bucket, int32_t* perm, int32_t* row_start,
                     int32_t* expert_rows, int32_t* num_rows, void* centroids, float* centroids_f32,
                     const CompressWs& ws, void* stream) {
-  if (E > kMaxE) return cudaErrorInvalidValue;
+  if (E > kMaxE || q > kMaxQ) return cudaErrorInvalidValue;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nk = static_cast<int>(n * k);
   int err;
@@ -869,8 +1092,8 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
     if ((err = cudaMemsetAsync(num_rows, 0, sizeof(int32_t), st))) return err;
     return cudaMemsetAsync(row_start, 0, sizeof(int32_t), st);
   }
-  // hash table slots (-1) and the grid-barrier counter (0xFFFFFFFF) in one memset
-  if ((err = cudaMemsetAsync(ws.table, 0xFF, sizeof(int32_t) * (ws.table_size + kHdr), st))) return err;
+  // header (arrival counters, stamps: -1) and hash table slots (-1) in one memset
+  if ((err = cudaMemsetAsync(ws.hdr, 0xFF, sizeof(int32_t) * (kHdr + ws.table_size), st))) return err;
   Params P = base_params(x, dtype, n, d, experts, k, E, ws);
   P.codes = codes;
   P.q = q;
@@ -881,24 +1104,21 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
   P.num_rows = num_rows;
   P.cent = static_cast<uint8_t*>(centroids);
   P.cent32 = centroids_f32;
-  P.row_passes = (bits_for(nk - 1) + 7) / 8;
-  return launch_coop(P, st);
+  return launch_chain(P, st);
 }
 
 int launch_permute(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int32_t* experts, int k, int E,
                    int32_t* slot, int32_t* expert_rows, void* send, const CompressWs& ws, void* stream) {
-  if (E > kMaxE + 1) return cudaErrorInvalidValue;
+  if (E > kMaxE) return cudaErrorInvalidValue;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nk = static_cast<int>(n * k);
   if (nk == 0) return cudaMemsetAsync(expert_rows, 0, sizeof(int32_t) * E, st);
-  int err;
-  if ((err = cudaMemsetAsync(ws.table, 0xFF, sizeof(int32_t) * 64, st))) return err;   // barrier counter
   Params P = base_params(x, dtype, n, d, experts, k, E, ws);
   P.bucket = slot;
   P.expert_rows = expert_rows;
   P.cent = static_cast<uint8_t*>(send);
   P.permute = 1;
-  return launch_coop(P, st);
+  return launch_chain(P, st);
 }
 
 }  // namespace lshmoe

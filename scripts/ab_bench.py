@@ -62,7 +62,7 @@ def main():
         comp = L.alloc_compressed(cfg.n, cfg.k, cfg.E, cfg.d, X.dtype, "cuda")
         med, mn = timeit(lambda: L.compress(X, codes, zeta, cfg.E, out=comp, workspace=ws), flush=flush)
         print(f"compress: median {med:.1f} us  min {mn:.1f}", flush=True)
-        print("  phases", L.compress_phase_times(ws))
+        pass
         print("  centroid CTAs", L.compress_cta_times(ws))
         raw = ws[:128].cpu().view(torch.int32).numpy().astype("int64") & 0xFFFFFFFF
         if int(os.environ.get("LSHMOE_CDBG", "0")) & 8:

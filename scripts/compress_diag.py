@@ -1,0 +1,49 @@
+"""Diagnostics (not a test): per-CTA phase stamps of lshmoe_compress on a config's inputs.
+Prints, per phase boundary, the max over CTAs and the critical CTA's sub-step times (us)."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
+import paper_2411_08446_b200 as L  # noqa: E402
+from lshmoe_inputs import CONFIGS, make_gate, make_tokens, rotation_seed  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C2"
+cfg = CONFIGS[name]
+X = make_tokens(cfg, 0)
+zeta, _ = make_gate(cfg, 0, X)
+Xd, zd = X.cuda(), zeta.cuda()
+R = L.rotation(cfg.d, cfg.q, rotation_seed(0), X.dtype).cuda()
+codes = L.hash(Xd, R)
+nk = cfg.n * cfg.k
+ws = torch.empty(L.compress_workspace_bytes(cfg.n, cfg.k, cfg.E, cfg.q, cfg.d, X.dtype), dtype=torch.uint8, device="cuda")
+out = L.alloc_compressed(cfg.n, cfg.k, cfg.E, cfg.d, X.dtype, "cuda")
+G = torch.cuda.get_device_properties(0).multi_processor_count
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+times = []
+for it in range(20):
+    flush.zero_()
+    ev[0].record()
+    L.compress(Xd, codes, zd, cfg.E, out=out, workspace=ws)
+    ev[1].record()
+    torch.cuda.synchronize()
+    times.append(ev[0].elapsed_time(ev[1]) * 1e3)
+print(f"{name}: compress event time us: median {np.median(times[5:]):.1f} min {min(times[5:]):.1f}")
+L.set_diagnostics(True)
+L.compress(Xd, codes, zd, cfg.E, out=out, workspace=ws)
+torch.cuda.synchronize()
+L.set_diagnostics(False)
+print("kernel spans", L.compress_phase_times(ws))
+m = int(out.num_rows.item())
+print(f"m={m} expert_rows max={int(out.expert_rows.max())}")
+for kern, st in L.compress_diag(ws).items():
+    D = {k: np.array(v) for k, v in st.items()}
+    print(kern)
+    for k, v in D.items():
+        if np.all(np.isnan(v)):
+            continue
+        print(f"  {k:12s} max {np.nanmax(v):7.2f}  med {np.nanmedian(v):7.2f}  min {np.nanmin(v):7.2f}  argmax {int(np.nanargmax(v))}")
+    crit = int(np.nanargmax(D["end"]))
+    print("  critical CTA", crit, {k: round(float(D[k][crit]), 2) for k in D})

@@ -118,3 +118,48 @@ def test_invalid_expert_raises_device_error(L):
         L.check_device_error()
     assert ei.value.status == L.EDEVICE
     L.check_device_error()          # cleared
+
+
+@pytest.mark.parametrize("cfgname", ["C3", "C4", "C5"])
+def test_compress_full_size_synthetic_codes(L, cfgname):
+    """Full C3/C4/C5 shapes (k=2, d=1024, E up to 64; groups up to ~8K copies), stage-isolated on
+    synthetic codes with the workloads' bucket structure (hashing them in the fp64 oracle would
+    take minutes).  Expected values come from the oracle's bucketize/centroids only."""
+    from lshmoe_inputs import make_codes
+    cfg = CONFIGS[cfgname]
+    X = make_tokens(cfg, 0)
+    codes = make_codes(cfg.n, cfg.q, cfg.d, 0, C=cfg.C, p_noise=0.08)
+    from lshmoe_inputs import make_gate
+    zeta, _ = make_gate(cfg, 0, X)
+    _compress_and_check(L, X, codes, zeta, cfg.E, cfg.dtype, cfgname, repeat=False)
+
+
+def test_compress_group_larger_than_shared_memory(L):
+    """Two groups of ~20K copies: phase A keeps its arrays in the workspace, not shared memory."""
+    from lshmoe_inputs import make_codes, make_zipf_gate
+    cfg = small_cfg(n=40000, k=1, E=2, q=3, d=64, dtype="f32")
+    X = make_tokens(cfg, 1)
+    codes = make_codes(cfg.n, cfg.q, cfg.d, 1, C=64, p_noise=0.05)
+    zeta = make_zipf_gate(cfg.n, 1, 2, 1)
+    _compress_and_check(L, X, codes, zeta, 2, "f32", "big-group")
+
+
+def test_compress_iid_group_counters_in_workspace(L):
+    """One group of 60K distinct keys: the per-(warp, row) counters no longer fit shared memory."""
+    from lshmoe_inputs import make_codes
+    cfg = small_cfg(n=60000, k=1, E=1, q=4, d=64, dtype="f32")
+    X = make_tokens(cfg, 2, iid=True)
+    codes = make_codes(cfg.n, cfg.q, cfg.d, 2, iid=True)
+    zeta = torch.zeros((cfg.n, 1), dtype=torch.int32)
+    out, b = _compress_and_check(L, X, codes, zeta, 1, "f32", "iid-60K", repeat=False)
+    assert b.m == len({tuple(r) for r in codes.tolist()})
+
+
+def test_compress_hot_expert_full_c2(L):
+    """C2 with 30% of tokens forced onto one expert (SURVEY §8d.1 stress 3)."""
+    from lshmoe_inputs import make_codes, make_zipf_gate
+    cfg = CONFIGS["C2"]
+    X = make_tokens(cfg, 3)
+    codes = make_codes(cfg.n, cfg.q, cfg.d, 3, C=cfg.C, p_noise=0.08)
+    zeta = make_zipf_gate(cfg.n, 1, cfg.E, 3, hot=0.3)
+    _compress_and_check(L, X, codes, zeta, cfg.E, "bf16", "C2-hot", repeat=False)
