@@ -106,19 +106,50 @@ struct FfnSched {
   __device__ void init(void* smem) {
     seg_start = reinterpret_cast<int*>(smem);
     tiles_pre = seg_start + (kMaxLocalExperts + 1);
-    if (threadIdx.x == 0) {
-      int rows = 0, tiles = 0;
-      const int ntn = N / bn;
-      for (int e = 0; e < E_local; ++e) {
-        seg_start[e] = rows;
-        tiles_pre[e] = tiles;
-        int r = 0;
-        for (int s = 0; s < world; ++s) r += recv_rows[e * world + s];
-        rows += r;
-        tiles += ((r + bm - 1) / bm) * ntn;
+    // thread e loads expert e's row counts (all loads in flight at once), warp 0 scans
+    const int tid = threadIdx.x;
+    if (tid < E_local) {
+      int r = 0;
+      for (int s = 0; s < world; ++s) r += recv_rows[tid * world + s];
+      seg_start[tid] = r;
+      tiles_pre[tid] = ((r + bm - 1) / bm) * (N / bn);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      constexpr int kPer = (kMaxLocalExperts + 31) / 32;   // entries per lane
+      int rs[kPer], ts[kPer], rsum = 0, tsum = 0;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int e = tid * kPer + i;
+        rs[i] = e < E_local ? seg_start[e] : 0;
+        ts[i] = e < E_local ? tiles_pre[e] : 0;
+        rsum += rs[i];
+        tsum += ts[i];
       }
-      seg_start[E_local] = rows;
-      tiles_pre[E_local] = tiles;
+      int rx = rsum, tx = tsum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int ry = __shfl_up_sync(0xFFFFFFFFu, rx, off), ty = __shfl_up_sync(0xFFFFFFFFu, tx, off);
+        if (tid >= off) {
+          rx += ry;
+          tx += ty;
+        }
+      }
+      int rrun = rx - rsum, trun = tx - tsum;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int e = tid * kPer + i;
+        if (e <= E_local) {
+          seg_start[e] = rrun;
+          tiles_pre[e] = trun;
+        }
+        rrun += rs[i];
+        trun += ts[i];
+      }
+      if (tid == 31) {                     // totals (E_local may equal kMaxLocalExperts)
+        seg_start[E_local] = rx;
+        tiles_pre[E_local] = tx;
+      }
     }
     __syncthreads();
   }

@@ -76,6 +76,17 @@ def main():
                 print(f"  {nm}: min {v.min():.2f} med {np.median(v):.2f} max {v.max():.2f}")
         print(f"  row_lo scatter sub-steps: offsets {(raw[20] - raw[6]) / 1e3:.2f} us, scatter "
               f"{(raw[21] - raw[20]) / 1e3:.2f} us, barrier {(raw[7] - raw[21]) / 1e3:.2f} us", flush=True)
+    if what in ("restore", "all"):
+        comp = L.compress(X, L.hash(X, R, codes), zeta, cfg.E)
+        ret = comp.centroids.clone()
+        y = torch.empty_like(X)
+        nb = 2 * X.numel() * X.element_size()
+        for fl in (flush, None):
+            med, mn = timeit(lambda: L.restore(X, comp.centroids, ret, comp.bucket, y=y), flush=fl)
+            print(f"restore V={'v1'} flush={fl is not None}: median {med:.1f} us "
+                  f"min {mn:.1f}  x+y streams {nb / med / 1e3:.0f} GB/s", flush=True)
+        med, mn = timeit(lambda: y.copy_(X), flush=flush)
+        print(f"torch copy x->y (same bytes, no gathers): median {med:.1f} us  {nb / med / 1e3:.0f} GB/s", flush=True)
     if what in ("ffn", "all"):
         comp = L.compress(X, L.hash(X, R, codes), zeta, cfg.E)
         ex = make_experts(cfg, 0)
