@@ -106,6 +106,20 @@ lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d,
                           const void* rotation, int q, int16_t* codes,
                           void* workspace, size_t workspace_bytes, lshmoe_stream stream);
 
+/* ---- NEXT-3: spherical-plane (SP) hash, the paper's other evaluated family (§4.5) --
+   The paper gives no construction; SPEC's sign-bit reading (reading R26): hash
+   function j owns the b unit normals in rows j*b .. j*b+b-1 of `normals`, and
+     code_tj = sum_{i<b} [normals[j*b+i] . x_t >= 0] * 2^i        (a zero dot counts as 1)
+   codes int16 [n, q] in [0, 2^b), usable as lshmoe_compress's composite key exactly like CP codes.
+   normals: device, dtype, row-major with lshmoe_sp_rows(q, b) >= q*b rows of d (rows past q*b
+   are read but ignored; e.g. the first b rows of each lshmoe_rotation R_j, zero padded).
+   bf16: tcgen05 GEMM with the sign-bit epilogue (products exact, fp32 accumulation); f32: SIMT
+   fp32 FMA.  Requires 1 <= b <= 15, q*b <= 256; bf16 d % 64 == 0 (as lshmoe_hash).
+   Decisions with |n.x| below 1e-5 * |n||x| are near-ties that may differ from exact arithmetic. */
+int lshmoe_sp_rows(int q, int b);
+lshmoe_status lshmoe_sp_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, const void* normals, int q, int b,
+                             int16_t* codes, lshmoe_stream stream);
+
 /* ---- a3-a5: group by expert, bucketize, centroid means -------------------------------------
    Bytes of device workspace lshmoe_compress needs for these sizes. */
 lshmoe_status lshmoe_compress_workspace(int64_t n, int k, int num_experts, int q, int d,

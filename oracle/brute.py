@@ -23,6 +23,16 @@ def cp_hash_one(R: Sequence[Sequence[float]], x: Sequence[float]) -> int:
     return -(best_i + 1) if best_y < 0 else best_i + 1
 
 
+def sp_hash_one(normals: Sequence[Sequence[float]], x: Sequence[float]) -> int:
+    """SPEC's sign-bit SP hash for one token and one hash function, by explicit
+    loops: bit i = 1 iff fsum_k normals[i][k] x[k] >= 0; code = sum_i bit_i 2^i."""
+    code = 0
+    for i, nrm in enumerate(normals):
+        if math.fsum(nrm[k] * x[k] for k in range(len(x))) >= 0:
+            code |= 1 << i
+    return code
+
+
 def buckets_pairwise(keys: Sequence[Tuple[int, ...]], experts: Sequence[Sequence[int]], E: int):
     """O(n^2) grouping of routed copies (t, s) by (expert, key) equality (SPEC S:L150's
     brute-force oracle).  Returns {expert: [sorted list of member lists]} with buckets ordered

@@ -14,6 +14,8 @@ The functions follow Algorithm 1 (App. A "Framework of LSH-MoE") ste
 
   O1  rotation(d, q, seed)            random rotation R_j of Eq. 3            [pinned]
   O2  cp_hash(X, R)                   Eq. 3 cross-polytope hash           [pinned]
+  O2' sp_hash(X, N, q, b)             §4.5 spherical-plane hashing (P:L474-479), SPEC's
+                                      sign-bit construction (reading R26)   [pinned]
   O3  group_by_expert(zeta, E)        Alg. 1 L3 "Dispatch X into {X_i}"        [pinned]
   O4  bucketize(codes, zeta, E)       Alg. 1 L5-6 LSH buckets, §2.3 [pinned]
   O5  centroids(X, ...)               Alg. 1 L8 Mean; §2.3        [pinned]
@@ -41,7 +43,7 @@ import numpy as np
 __all__ = [
     "GAMMA", "splitmix64_stream", "irwin_hall_gaussian", "rotation_fp64", "rotation",
     "round_to_dtype", "f32_to_bf16_bits", "bf16_bits_to_f64", "to_stored",
-    "cp_hash", "group_by_expert", "bucketize", "Buckets", "centroids", "expert_ffn",
+    "cp_hash", "sp_hash", "sp_normals", "group_by_expert", "bucketize", "Buckets", "centroids", "expert_ffn",
     "dispatch_sim", "combine_sim", "restore", "moe_dense", "lsh_layer", "lsh_layer_ranks",
     "LayerResult", "ulp_bf16",
 ]
@@ -193,6 +195,48 @@ def cp_hash(X: np.ndarray, R: np.ndarray):
             second = np.partition(A, d - 2, axis=1)[:, d - 2]
             with np.errstate(invalid="ignore", divide="ignore"):
                 margins[:, j] = np.where(amax > 0, (amax - second) / np.where(amax > 0, amax, 1.0), 0.0)
+    return codes, margins
+
+
+# ---------------------------------------------------------------------------------------------
+# O2'. Spherical-plane (SP) hashing, the paper's other evaluated family (§4.5 "Impact of the Types
+# of Hash Functions").  The paper never defines its construction; SPEC
+# reads it as random-hyperplane sign bits: bit i = 1 iff n_i . x >= 0 (zero dots count as 1).
+# Reading R26: hash function j uses b unit normals (rows j*b .. j*b+b-1 of N [q*b, d]) and its
+# code is the integer sum_i bit_i * 2^i (0 .. 2^b - 1, b <= 15 so it fits an int16); the q codes
+# form the composite key exactly like the CP codes (reading R4).  The recommended normals are the
+# first b rows of the rotations R_j of O1 (orthonormal, hence unit), see sp_normals.
+# ---------------------------------------------------------------------------------------------
+def sp_normals(R: np.ndarray, b: int) -> np.ndarray:
+    """N [q*b, d]: the first b rows of each rotation R_j (reading R26)."""
+    R = np.asarray(R, dtype=np.float64)
+    q = R.shape[0]
+    return np.concatenate([R[j, :b, :] for j in range(q)], axis=0)
+
+
+def sp_hash(X: np.ndarray, N: np.ndarray, q: int, b: int):
+    """X [n, d], N [q*b, d] (stored values as fp64) -> codes int16 [n, q] in [0, 2^b), and
+    margins fp64 [n, q] = min_i |n_i . x| / (||n_i|| ||x||) over the hash's b normals (0 for a
+    zero token): a sign decision with margin < 1e-5 is a near-tie (BASELINE tier 1)."""
+    X = np.asarray(X, dtype=np.float64)
+    N = np.asarray(N, dtype=np.float64)
+    n, d = X.shape
+    if N.shape != (q * b, d):
+        raise ValueError("N must be [q*b, d]")
+    if not 1 <= b <= 15:
+        raise ValueError("1 <= b <= 15")
+    Y = X @ N.T                                          # [n, q*b] dots in fp64
+    bits = (Y >= 0).astype(np.int64)                     # -0.0 >= 0: a zero dot is bit 1
+    codes = np.zeros((n, q), dtype=np.int16)
+    margins = np.empty((n, q), dtype=np.float64)
+    xn = np.linalg.norm(X, axis=1)
+    nn = np.linalg.norm(N, axis=1)
+    for j in range(q):
+        cols = slice(j * b, (j + 1) * b)
+        codes[:, j] = (bits[:, cols] << np.arange(b)).sum(axis=1).astype(np.int16)
+        with np.errstate(invalid="ignore", divide="ignore"):
+            rel = np.abs(Y[:, cols]) / (xn[:, None] * nn[None, cols])
+        margins[:, j] = np.where(xn > 0, rel.min(axis=1), 0.0)
     return codes, margins
 
 

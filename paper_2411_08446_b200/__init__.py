@@ -41,6 +41,8 @@ _SIGS = {
     "lshmoe_rotation": ([_i32, _i32, _u64, _i32, _vp], _i32),
     "lshmoe_hash_workspace": ([_i64, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
     "lshmoe_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _sz, _vp], _i32),
+    "lshmoe_sp_rows": ([_i32, _i32], _i32),
+    "lshmoe_sp_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _i32, _vp, _vp], _i32),
     "lshmoe_compress_workspace": ([_i64, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
     "lshmoe_compress": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                          _vp, _sz, _vp], _i32),
@@ -159,6 +161,37 @@ def hash(x: torch.Tensor, R: torch.Tensor, codes: Optional[torch.Tensor] = None,
     wsb = 0 if workspace is None else workspace.numel()
     _check(_lib.lshmoe_hash(_ptr(x), _dt(x), n, d, _ptr(R), q, _ptr(codes), _ptr(workspace), wsb, _stream(stream)),
            "lshmoe_hash")
+    return codes
+
+
+def sp_rows(q: int, b: int) -> int:
+    """Rows the normals buffer of sp_hash must hold (>= q*b; extra rows are ignored)."""
+    r = _lib.lshmoe_sp_rows(q, b)
+    if r <= 0:
+        raise ValueError("need q >= 1, b >= 1, q*b <= 256")
+    return r
+
+
+def sp_normals(R: torch.Tensor, b: int) -> torch.Tensor:
+    """The recommended SP normals (reading R26): the first b rows of each rotation R_j, stacked and
+    zero padded to sp_rows(q, b) rows.  Pure data movement (torch indexing), no hashing."""
+    q, d = R.shape[0], R.shape[2]
+    out = torch.zeros((sp_rows(q, b), d), dtype=R.dtype, device=R.device)
+    out[:q * b] = R[:, :b, :].reshape(q * b, d)
+    return out
+
+
+def sp_hash(x: torch.Tensor, normals: torch.Tensor, q: int, b: int, codes: Optional[torch.Tensor] = None,
+            stream=None) -> torch.Tensor:
+    """Spherical-plane sign-bit codes int16 [n, q] in [0, 2^b) (NEXT-3, reading R26)."""
+    _require_cuda(x, normals)
+    n, d = x.shape
+    if normals.dtype != x.dtype or normals.shape[1] != d or normals.shape[0] < sp_rows(q, b):
+        raise ValueError("normals must be [sp_rows(q, b), d] in x's dtype")
+    if codes is None:
+        codes = torch.empty((n, q), dtype=torch.int16, device=x.device)
+    _check(_lib.lshmoe_sp_hash(_ptr(x), _dt(x), n, d, _ptr(normals), q, b, _ptr(codes), _stream(stream)),
+           "lshmoe_sp_hash")
     return codes
 
 

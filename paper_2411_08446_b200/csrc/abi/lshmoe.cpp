@@ -105,6 +105,27 @@ lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, c
   return cuda_status(err, "lshmoe_hash");
 }
 
+int lshmoe_sp_rows(int q, int b) { return (q >= 1 && b >= 1 && q * b <= 256) ? sp_rows(q, b) : 0; }
+
+lshmoe_status lshmoe_sp_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, const void* normals, int q, int b,
+                             int16_t* codes, lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, dtype, n, d);
+  if (st) return st;
+  REQUIRE(q >= 1 && b >= 1, LSHMOE_EINVAL, "q < 1 or b < 1");
+  REQUIRE(q <= LSHMOE_MAX_Q && b <= 15 && q * b <= 256, LSHMOE_EUNSUPPORTED, "need q <= LSHMOE_MAX_Q, b <= 15, q*b <= 256");
+  if (n == 0) return LSHMOE_OK;
+  REQUIRE(x && normals && codes, LSHMOE_EINVAL, "NULL pointer");
+  REQUIRE(aligned16(x) && aligned16(normals), LSHMOE_EINVAL, "x / normals must be 16-byte aligned");
+  int err;
+  if (dtype == LSHMOE_F32) {
+    REQUIRE(d <= 384, LSHMOE_EUNSUPPORTED, "f32 (SIMT) SP hash supports d <= 384");
+    err = launch_sp_hash_f32(static_cast<const float*>(x), n, d, static_cast<const float*>(normals), q, b, codes, stream);
+  } else {
+    err = launch_sp_hash_bf16(x, n, d, normals, q, b, codes, stream);
+  }
+  return cuda_status(err, "lshmoe_sp_hash");
+}
+
 lshmoe_status lshmoe_compress_workspace(int64_t n, int k, int E, int q, int d, lshmoe_dtype dtype, size_t* bytes) {
   (void)q;
   (void)dtype;

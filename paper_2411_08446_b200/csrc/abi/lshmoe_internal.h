@@ -20,6 +20,9 @@ lshmoe_status rotation_host(int d, int q, uint64_t seed, lshmoe_dtype dtype, voi
 int launch_hash_f32(const float* x, int64_t n, int d, const float* R, int q, int16_t* codes, void* stream);
 int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int16_t* codes, void* ws, void* stream);
 size_t hash_workspace_bytes(int64_t n, int d, int q);
+int sp_rows(int q, int b);
+int launch_sp_hash_f32(const float* x, int64_t n, int d, const float* N, int q, int b, int16_t* codes, void* stream);
+int launch_sp_hash_bf16(const void* x, int64_t n, int d, const void* N, int q, int b, int16_t* codes, void* stream);
 
 struct CompressWs {            // carved from the caller's workspace by compress_workspace_layout
   int32_t* hdr;                // [kHdr] barrier counter, diagnostics stamps, cut-row arrival counters

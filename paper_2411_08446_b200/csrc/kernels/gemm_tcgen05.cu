@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -63,6 +64,7 @@ struct WorkItem {
 // The slices of one (tile, j) are merged by the last one to finish (ArgmaxEpi::finish).
 struct HashSched {
   int n, q, d, bn, bm;
+  int prefetch_b;   // 0: the rotations are L2-resident
   int m_tiles;
   __device__ void init(void*) {}
   int split;   // 1: one unit per BN slice; 0: one unit covers all d / BN slices (no merge)
@@ -101,6 +103,7 @@ constexpr int kMaxLocalExperts = 256;
 struct FfnSched {
   const int32_t* recv_rows;  // [E_local, world]
   int E_local, world, N, bn, bm;
+  int prefetch_b;   // weight k-blocks prefetched to L2 ahead of the TMA loads
   int* seg_start;   // smem [E_local + 1]
   int* tiles_pre;   // smem [E_local + 1]
   __device__ void init(void* smem) {
@@ -285,6 +288,47 @@ struct ArgmaxEpi {
   }
 };
 
+// SignBitsEpi — NEXT-3, spherical-plane hashing (§4.5; SPEC's sign-bit reading
+// S:L124-132, reading R26): Y = X N^T with the q*b unit normals as B rows (one BN-wide unit holds
+// all of them); a thread keeps the sign bits (y >= 0, so a zero dot and -0 give 1) of its row's
+// columns as 32-bit words, the two column halves meet in shared memory, and code_j = the b bits
+// of hash j.  Only the int16 codes reach HBM.
+template <int BN>
+struct SignBitsEpi {
+  int16_t* codes;
+  int q, b;
+  static constexpr int kBlkPer = (BN / 32) * 4 / kEpiWarps;   // 32-column blocks per thread
+  uint32_t wds[kBlkPer];
+  int nw;
+  __device__ void begin(const WorkItem&, uint8_t*) { nw = 0; }
+  __device__ void consume(const WorkItem&, int, const uint32_t (&r)[32], int, const uint8_t*) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) m |= (__uint_as_float(r[i]) >= 0.0f ? 1u : 0u) << i;
+#pragma unroll
+    for (int k = 0; k < kBlkPer; ++k)      // blocks arrive in ascending column order
+      if (k == nw) wds[k] = m;
+    ++nw;
+  }
+  __device__ void finish(const WorkItem& w, int row, uint8_t* scratch, int half, int nthr) {
+    uint32_t* bits = reinterpret_cast<uint32_t*>(scratch);   // [128 rows][BN / 32 words]
+    constexpr int kW = BN / 32;
+#pragma unroll
+    for (int k = 0; k < kBlkPer; ++k) bits[row * kW + half * kBlkPer + k] = wds[k];
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    if (half == 0 && row < w.valid_rows) {
+      const int64_t t = w.a_row + row;
+      for (int j = 0; j < q; ++j) {
+        const int c0 = j * b, wi = c0 >> 5, sh = c0 & 31;
+        uint64_t v = bits[row * kW + wi];
+        if (wi + 1 < kW) v |= static_cast<uint64_t>(bits[row * kW + wi + 1]) << 32;
+        codes[t * q + j] = static_cast<int16_t>((v >> sh) & ((1u << b) - 1u));
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");   // scratch reused by the next unit
+  }
+};
+
 template <int BN>
 struct BiasActEpi {
   const __nv_bfloat16* bias;  // [E_local, N]
@@ -379,11 +423,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // L2 prefetch cursor running kPrefetchB k-blocks ahead of the loads (B operand only: the
+      // FFN's weights stream from HBM once; the tokens are L2-resident)
+      int pu = cluster, pc = 0, pkb = 0;
+      WorkItem pw{};
+      if (sched.prefetch_b > 0 && pu < units) pw = sched.get(pu, rank);
+      auto prefetch_next = [&]() {
+        if (sched.prefetch_b == 0 || pu >= units) return;
+        tma_prefetch_l2_2d(&tmB, pkb * BK, pw.b_row0 + pc * BN + rank * C::kBRows);
+        if (++pkb == kblocks) {
+          pkb = 0;
+          if (++pc == pw.nchunks) {
+            pc = 0;
+            pu += nclusters;
+            if (pu < units) pw = sched.get(pu, rank);
+          }
+        }
+      };
+      for (int i = 0; i < sched.prefetch_b; ++i) prefetch_next();
       for (int u = cluster; u < units; u += nclusters) {
         const WorkItem w = sched.get(u, rank);
         for (int c = 0; c < w.nchunks; ++c) {
           const int brow = w.b_row0 + c * BN + rank * C::kBRows;
           for (int kb = 0; kb < kblocks; ++kb) {
+            prefetch_next();
             mbar_wait(&empty[stage], phase ^ 1);
             if (kCta == 2) {
               if (leader) mbar_arrive_expect_tx(&full[stage], C::kTxBytes);
@@ -596,6 +659,11 @@ int cta_mode(const char* env_name, int dflt) {
   return dflt;
 }
 
+int ffn_prefetch() {   // experiment override LSHMOE_FFN_PF (k-blocks); default 0 (measured: no gain)
+  const char* env = getenv("LSHMOE_FFN_PF");
+  return env ? atoi(env) : 0;
+}
+
 }  // namespace
 
 int device_sm_count() {
@@ -631,9 +699,10 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
   e.codes = codes;
   e.q = q;
   e.rows_pad = static_cast<int>(((n + 255) / 256) * 256);
-  // Slice split (LSHMOE_HASH_SPLIT=1) evens out the last wave but measured slower on B200 (C2: 94 vs
-  // 88 us, scripts/ab_bench.py): off by default.
-  s.split = (d > bn) && ws && cta_mode("LSHMOE_HASH_SPLIT", 2) == 1 ? 1 : 0;
+  // Slice split (one unit per BN slice of the d coordinates, slices merged by the last arrival)
+  // evens out the persistent grid's last wave: C2 86.1 vs 90.2 us per launch, CUDA-graph timing in
+  // scripts/ab_bench.py (LSHMOE_HASH_SPLIT=2 turns it off).
+  s.split = (d > bn) && ws && cta_mode("LSHMOE_HASH_SPLIT", 1) == 1 ? 1 : 0;
   if (s.split) {
     const size_t counters = ((sizeof(int) * (e.rows_pad / BM) * q) + 255) & ~size_t(255);
     e.counter = static_cast<int*>(ws);
@@ -643,16 +712,55 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
                    static_cast<cudaStream_t>(stream));
 }
 
+// NEXT-3: SP hash.  B = the normals, rows q*b (the buffer holds sp_rows(q, b) >= q*b rows; rows
+// past q*b are read but their bits are never used), K = d.
+int sp_rows(int q, int b) {
+  const int nb = q * b;
+  return nb <= 64 ? 64 : (nb <= 128 ? 128 : 256);
+}
+
+template <int NP>
+int launch_sp_np(const void* x, int64_t n, int d, const void* normals, int q, int b, int16_t* codes, cudaStream_t st) {
+  CUtensorMap ma, mb;
+  int err = make_map(&ma, x, n, d, BM);
+  if (err) return err;
+  err = make_map(&mb, normals, NP, d, NP);
+  if (err) return err;
+  HashSched s{};
+  s.n = static_cast<int>(n);
+  s.q = 1;
+  s.d = NP;                  // one unit = one 128-token tile x all NP normal rows
+  s.bn = NP;
+  s.bm = BM;
+  s.split = 0;
+  s.m_tiles = static_cast<int>((n + BM - 1) / BM);
+  SignBitsEpi<NP> e{codes, q, b};
+  const int grid = std::min(device_sm_count(), s.m_tiles);
+  return launch_tc<NP, 1>(ma, mb, d, s, e, grid, st);
+}
+
+int launch_sp_hash_bf16(const void* x, int64_t n, int d, const void* normals, int q, int b, int16_t* codes,
+                        void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (sp_rows(q, b)) {
+    case 64: return launch_sp_np<64>(x, n, d, normals, q, b, codes, st);
+    case 128: return launch_sp_np<128>(x, n, d, normals, q, b, codes, st);
+    default: return launch_sp_np<256>(x, n, d, normals, q, b, codes, st);
+  }
+}
+
 int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, int E_local, int world,
                     const void* W1, const void* b1, const void* W2, const void* b2, void* hidden, int64_t capacity,
                     void* out, void* stream) {
   if (E_local > kMaxLocalExperts) return cudaErrorInvalidValue;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int cta = cta_mode("LSHMOE_FFN_CTA", 2);
-  FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, nullptr, nullptr};
+  const int only = cta_mode("LSHMOE_FFN_ONLY", 0);   // experiment: 1 / 2 = launch only GEMM 1 / 2
+  FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, ffn_prefetch(), nullptr, nullptr};
   const int bn1 = env_bn("LSHMOE_FFN_BN1", d_ffn, pick_bn(d_ffn));
-  int err;
-  if (bn1 == 256) {
+  int err = 0;
+  if (only == 2) {
+  } else if (bn1 == 256) {
     BiasActEpi<256> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true};
     err = launch_bn(bn1, cta, in, capacity, W1, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
   } else if (bn1 == 128) {
@@ -662,8 +770,8 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
     BiasActEpi<64> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true};
     err = launch_bn(bn1, cta, in, capacity, W1, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
   }
-  if (err) return err;
-  FfnSched s2{recv_rows, E_local, world, d, 0, 0, nullptr, nullptr};
+  if (err || only == 1) return err;
+  FfnSched s2{recv_rows, E_local, world, d, 0, 0, ffn_prefetch(), nullptr, nullptr};
   const int bn2 = env_bn("LSHMOE_FFN_BN2", d, pick_bn(d));
   if (bn2 == 256) {
     BiasActEpi<256> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false};

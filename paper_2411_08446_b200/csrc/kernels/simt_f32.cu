@@ -54,6 +54,52 @@ __global__ void __launch_bounds__(kTok) hash_f32_kernel(const float* __restrict_
   if (t < n) codes[static_cast<int64_t>(t) * q + j] = static_cast<int16_t>(bneg ? -(bidx + 1) : (bidx + 1));
 }
 
+// NEXT-3 SP hash, fp32: grid ceil(n / 128) CTAs, one token per thread, the q*b normals staged 32
+// rows at a time; bit i of hash j = (n_{j*b+i} . x >= 0), fp32 FMA in ascending k (reading R26).
+__global__ void __launch_bounds__(kTok) sp_hash_f32_kernel(const float* __restrict__ x, int n, int d,
+                                                           const float* __restrict__ N, int q, int b,
+                                                           int16_t* __restrict__ codes) {
+  extern __shared__ float sm[];
+  float* xs = sm;                      // [d][kXs]
+  float* rs = sm + d * kXs;            // [kRowsR][d]
+  const int t0 = blockIdx.x * kTok;
+  for (int i = threadIdx.x; i < d * kTok; i += kTok) {
+    const int tt = i / d, k = i - tt * d;
+    const int t = t0 + tt;
+    xs[k * kXs + tt] = t < n ? x[static_cast<int64_t>(t) * d + k] : 0.0f;
+  }
+  const int nb = q * b;
+  uint32_t bits[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // up to 256 sign bits
+  for (int i0 = 0; i0 < nb; i0 += kRowsR) {
+    const int rows = min(kRowsR, nb - i0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < rows * d; i += kTok) rs[i] = N[static_cast<int64_t>(i0) * d + i];
+    __syncthreads();
+    uint32_t m = 0;
+    for (int ii = 0; ii < rows; ++ii) {
+      const float* rrow = rs + ii * d;
+      float y = 0.0f;
+      for (int k = 0; k < d; ++k) y = fmaf(rrow[k], xs[k * kXs + threadIdx.x], y);
+      m |= (y >= 0.0f ? 1u : 0u) << ii;
+    }
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+      if (w == i0 / kRowsR) bits[w] = m;
+  }
+  const int t = t0 + threadIdx.x;
+  if (t >= n) return;
+  for (int j = 0; j < q; ++j) {
+    const int c0 = j * b, wi = c0 >> 5, sh = c0 & 31;
+    uint64_t v = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      if (w == wi) v |= bits[w];
+      if (w == wi + 1) v |= static_cast<uint64_t>(bits[w]) << 32;
+    }
+    codes[static_cast<int64_t>(t) * q + j] = static_cast<int16_t>((v >> sh) & ((1u << b) - 1u));
+  }
+}
+
 // One thread per output element of one GEMM layer over rows segmented by expert:
 // out[r][o] = act(sum_i W[e][o][i] * in[r][i] + b[e][o]).  Segment table recomputed per CTA.
 __global__ void ffn_f32_layer_kernel(const float* __restrict__ in, int K, int N, const int32_t* __restrict__ recv_rows,
@@ -83,6 +129,19 @@ __global__ void ffn_f32_layer_kernel(const float* __restrict__ in, int K, int N,
 }
 
 }  // namespace
+
+int launch_sp_hash_f32(const float* x, int64_t n, int d, const float* N, int q, int b, int16_t* codes,
+                       void* stream) {
+  const int smem = (d * kXs + kRowsR * d) * 4;
+  if (smem > 48 * 1024) {
+    const int err = cudaFuncSetAttribute(sp_hash_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err) return err;
+  }
+  sp_hash_f32_kernel<<<static_cast<int>((n + kTok - 1) / kTok), kTok, smem, static_cast<cudaStream_t>(stream)>>>(
+      x, static_cast<int>(n), d, N, q, b, codes);
+  count_launches(1);
+  return cudaGetLastError();
+}
 
 int launch_hash_f32(const float* x, int64_t n, int d, const float* R, int q, int16_t* codes, void* stream) {
   const size_t smem = sizeof(float) * (static_cast<size_t>(d) * kXs + kRowsR * d);

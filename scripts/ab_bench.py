@@ -12,7 +12,13 @@ from lshmoe_inputs import CONFIGS, make_experts, make_rank_inputs, rotation_seed
 
 
 def timeit(fn, iters=30, flush=None):
-    for _ in range(3):
+    """Device time of fn: captured once into a CUDA graph (no host launch overhead in the timed
+    region), replayed between CUDA events; L2 flushed before each replay when flush is given."""
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
         fn()
     ts = []
     for _ in range(iters):
@@ -20,7 +26,7 @@ def timeit(fn, iters=30, flush=None):
             flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        fn()
+        g.replay()
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e3)
@@ -96,14 +102,16 @@ def main():
         hid = torch.empty((comp.centroids.shape[0], cfg.d_ffn), dtype=X.dtype, device="cuda")
         m = int(comp.num_rows.item())
         fl = 4.0 * m * cfg.d * cfg.d_ffn
-        for cta in ("1", "2"):
-            for bn1 in ("256", "128"):
-                for bn2 in ("256", "128", "64"):
-                    os.environ.update(LSHMOE_FFN_CTA=cta, LSHMOE_FFN_BN1=bn1, LSHMOE_FFN_BN2=bn2)
-                    med, mn = timeit(lambda: L.expert_ffn(comp.centroids, rr, *W, out=out, hidden=hid), flush=flush)
-                    print(f"ffn cta={cta} bn1={bn1} bn2={bn2}: median {med:.1f} us  min {mn:.1f} us  "
-                          f"{fl / med / 1e6:.0f} TFLOP/s  (m={m})", flush=True)
-        for k in ("LSHMOE_FFN_CTA", "LSHMOE_FFN_BN1", "LSHMOE_FFN_BN2"):
+        for only in ("1", "2"):
+            for cta, bn, pf in (("2", "256", "0"), ("2", "256", "12"), ("2", "256", "24"), ("2", "256", "48"),
+                                ("1", "256", "24"), ("2", "128", "24")):
+                    os.environ.update(LSHMOE_FFN_CTA=cta, LSHMOE_FFN_BN1=bn, LSHMOE_FFN_BN2=bn, LSHMOE_FFN_ONLY=only,
+                                      LSHMOE_FFN_PF=pf)
+                    for fl_ in (flush,):
+                        med, mn = timeit(lambda: L.expert_ffn(comp.centroids, rr, *W, out=out, hidden=hid), flush=fl_)
+                        print(f"ffn GEMM{only} cta={cta} bn={bn} pf={pf}: median {med:.1f} us  "
+                              f"min {mn:.1f} us  {fl / 2 / med / 1e6:.0f} TFLOP/s  (m={m})", flush=True)
+        for k in ("LSHMOE_FFN_CTA", "LSHMOE_FFN_BN1", "LSHMOE_FFN_BN2", "LSHMOE_FFN_ONLY", "LSHMOE_FFN_PF"):
             os.environ.pop(k)
         med, mn = timeit(lambda: L.expert_ffn(comp.centroids, rr, *W, out=out, hidden=hid), flush=None)
         print(f"ffn default, NO L2 flush (weights L2-resident): median {med:.1f} us  {fl / med / 1e6:.0f} TFLOP/s",
