@@ -38,6 +38,9 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--q", type=int, default=None, help="override the number of hash functions")
     p.add_argument("--impl", default="lsh", choices=["lsh", "reference"])
+    p.add_argument("--hash", default="cp", choices=["cp", "sp"],
+                   help="hash family: cross-polytope (paper default, Eq. 3) or spherical-plane (NEXT-3)")
+    p.add_argument("--sp-bits", type=int, default=12, help="sign bits per SP hash function")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-uncompressed", action="store_true")
     p.add_argument("--no-graph", action="store_true")
@@ -156,8 +159,12 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(cfg, world):
-    return {"workload": f"{cfg.name}: {cfg.note}", "tokens_per_gpu": cfg.n, "d_model": cfg.d, "experts": cfg.E,
+def workload_config(cfg, world, args=None):
+    hashing = "cross-polytope (Eq. 3)"
+    if args is not None and args.hash == "sp":
+        hashing = f"spherical-plane sign bits, {args.sp_bits} per hash (NEXT-3)"
+    return {"workload": f"{cfg.name}: {cfg.note}", "hash": hashing, "tokens_per_gpu": cfg.n, "d_model": cfg.d,
+            "experts": cfg.E,
             "experts_per_gpu": cfg.E // world, "top_k": cfg.k, "hash_functions": cfg.q, "d_ffn": cfg.d_ffn,
             "parallelism": f"ep{world}", "l2": "flushed between timed steps (256 MiB write, outside the events)"}
 
@@ -254,9 +261,15 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     n, k, d = cfg.n, cfg.k, cfg.d
     nk = n * k
 
+    if args.hash == "sp":
+        Nrm = L.sp_normals(R, args.sp_bits)
+        hash_call = lambda: L.sp_hash(X, Nrm, cfg.q, args.sp_bits, codes)   # noqa: E731
+    else:
+        hash_call = lambda: L.hash(X, R, codes)   # noqa: E731
+
     def stage_calls():
         return [
-            lambda: L.hash(X, R, codes),
+            hash_call,
             lambda: L.compress(X, codes, zeta, cfg.E, out=comp, workspace=ws),
             lambda: L.dispatch(comm, comp.centroids, comp.expert_rows, cfg.E, recv, rr),
             lambda: L.expert_ffn(recv, rr, W1, b1, W2, b2, out=eo, hidden=hid),
@@ -423,16 +436,38 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                "speedup_of_lsh": bms / ms}
 
     L.check_device_error()
+    # ---- the dominant kernel alone (the hash launch), CUDA-graph replay on `stream`, L2 flushed
+    # before each replay, CUDA events on `stream` around the replay: its device time per launch ----
+    hg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(hg, stream=stream):
+        hash_call()
+    hev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for s in range(args.steps):
+        flush.zero_()
+        hev[s][0].record(stream)
+        hg.replay()
+        hev[s][1].record(stream)
+    torch.cuda.synchronize()
+    hash_dev_ms = statistics.median(a.elapsed_time(b) for a, b in hev)
     pk = peaks()
-    flops = 2.0 * n * cfg.q * d * d
-    achieved = flops / (hash_ms / 1e3) / 1e12
-    roof = {"bound": "tensor", "kernel": "tc_gemm_kernel<ArgmaxEpi> (lshmoe_hash)", "achieved": achieved,
-            "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops"],
-            "traffic": ncu_traffic(),
-            "per_launch": {"flops": flops, "algorithmic_bytes": n * d * 2 + cfg.q * d * d * 2 + n * cfg.q * 2,
-                           "avg_ms": hash_ms},
-            "peak_source": pk["source"] + " bf16 dense (burst) — cuBLAS bf16 GEMM",
-            "frac_of_sustained": achieved / pk["bf16_tflops_sustained"] if pk.get("bf16_tflops_sustained") else None}
+    if args.hash == "sp":
+        nbytes = n * d * 2 + L.sp_rows(cfg.q, args.sp_bits) * d * 2 + n * cfg.q * 2
+        achieved = nbytes / (hash_dev_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": "tc_gemm_kernel<SignBitsEpi> (lshmoe_sp_hash)", "achieved": achieved,
+                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                "per_launch": {"algorithmic_bytes": nbytes, "avg_ms": hash_dev_ms, "eager_stage_ms": hash_ms},
+                "peak_source": pk["source"] + " HBM copy bandwidth"}
+    else:
+        flops = 2.0 * n * cfg.q * d * d
+        achieved = flops / (hash_dev_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": "tc_gemm_kernel<ArgmaxEpi> (lshmoe_hash)", "achieved": achieved,
+                "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops"],
+                "traffic": ncu_traffic(),
+                "per_launch": {"flops": flops, "algorithmic_bytes": n * d * 2 + cfg.q * d * d * 2 + n * cfg.q * 2,
+                               "avg_ms": hash_dev_ms, "eager_stage_ms": hash_ms,
+                               "timing": "CUDA-graph replay of the launch, L2 flushed before each, events on its stream"},
+                "peak_source": pk["source"] + " bf16 dense (burst) — cuBLAS bf16 GEMM",
+                "frac_of_sustained": achieved / pk["bf16_tflops_sustained"] if pk.get("bf16_tflops_sustained") else None}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -443,7 +478,7 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32",
                 "data": "synthetic (seeded Zipf mixture tokens, linear top-k gate, random experts)",
-                "config": workload_config(cfg, world),
+                "config": workload_config(cfg, world, args),
                 "compression_ratio": ratio, "centroids": m, "routed_copies": nk,
                 "gpu_launches": launches_per_step * args.steps, "gpu_launches_per_step": launches_per_step,
                 "cuda_graph": use_graph,
