@@ -26,6 +26,10 @@ The functions follow Algorithm 1 (App. A "Framework of LSH-MoE") ste
                                       (P:L536-538), composed with Eq. 2's k-sum [pinned]
   O11 stats                           compression rate (Table 3)
   O12 moe_dense                       Eq. 2 uncompressed MoE output          [pinned]
+  B1  grad_compress(dY, b, k, g)      NEXT-1 backward: dL/dE(c~)_b = sum_{(t,s) in b} g dY_t [pinned]
+  B3  expert_ffn_vjp(c, W1.., G)      expert backward J_E(c)^T G (the expert's own rule) [pinned]
+  B5  grad_restore(...)               dL/dx_t and dL/dg_ts of Eq. 4-5 + Eq. 2 with the
+                                      centroid mean, straight-through rounding (R27)    [pinned]
 
 Every function above is pinned by a ``-m "not gpu"`` test in tests/test_oracle_*.py against
 something other than itself (worked examples, closed forms, invariants, brute force, textbook
@@ -45,7 +49,7 @@ __all__ = [
     "round_to_dtype", "f32_to_bf16_bits", "bf16_bits_to_f64", "to_stored",
     "cp_hash", "sp_hash", "sp_normals", "group_by_expert", "bucketize", "Buckets", "centroids", "expert_ffn",
     "dispatch_sim", "combine_sim", "restore", "moe_dense", "lsh_layer", "lsh_layer_ranks",
-    "LayerResult", "ulp_bf16",
+    "LayerResult", "ulp_bf16", "grad_compress", "expert_ffn_vjp", "grad_restore", "lsh_layer_backward",
 ]
 
 # ---------------------------------------------------------------------------------------------
@@ -461,3 +465,73 @@ def lsh_layer_ranks(X_by_rank, zeta_by_rank, R, experts, E: int, dtype: str,
 def lsh_layer(X, zeta, R, experts, E: int, dtype: str, g=None, round_expert_out: bool = True) -> LayerResult:
     """Single-rank (w = 1) Alg. 1."""
     return lsh_layer_ranks([X], [zeta], R, experts, E, dtype, None if g is None else [g], round_expert_out)
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-1. Backward of the compressed layer (the paper trains with LSH-MoE, P:L365-366, App. B
+# P:L577, but never writes the gradient; "residual-based gradient compensation", P:L238, is read
+# as compensating activations -- reading R14).  Reading R27: the codes and buckets are constants
+# (piecewise-constant hash), the rounding c~ = RNE(c) is straight-through, and the forward is
+#   c_b = (1/n_b) sum_{(t,s) in b} x_t        (O5, Alg. 1 L8)
+#   o_b = E_{e(b)}(c~_b)                      (O8, Alg. 1 L15)
+#   y_t = sum_s g_ts (o_{b_ts} + x_t - c~_{b_ts})   (O10, Eq. 4-5 inside Eq. 2)
+# so, for an upstream gradient dY:
+#   B1 G_b   = sum_{(t,s) in b} g_ts dY_t               dL/do_b; the c~ term contributes -G_b
+#   B2/B4    G travels to the expert's rank and back like c~ / o (Alg. 1 L14/L16 in reverse)
+#   B3 H_b   = J_E(c~_b)^T G_b                          the expert's backward
+#   B5 dX_t  = sum_s [ g_ts dY_t + (H_b - G_b) / n_b ]  with b = b_ts (chain rule through c_b)
+#      dg_ts = dY_t . (o_b + x_t - c~_b)
+# ---------------------------------------------------------------------------------------------
+def grad_compress(dY: np.ndarray, b: Buckets, k: int, g: Optional[np.ndarray] = None) -> np.ndarray:
+    """B1: G [m, d] = per-row sums of g_ts dY_t over the row's routed copies (fp64), in the
+    centroid (send) layout."""
+    dY = np.asarray(dY, np.float64)
+    if b.m == 0:
+        return np.zeros((0, dY.shape[1]))
+    w = np.ones(b.perm.shape[0]) if g is None else np.asarray(g, np.float64).reshape(-1)[b.perm]
+    rows = dY[b.perm // k] * w[:, None]
+    return np.add.reduceat(rows, b.row_start[:-1], axis=0)
+
+
+def expert_ffn_vjp(Cin: np.ndarray, W1: np.ndarray, b1: np.ndarray, W2: np.ndarray, G: np.ndarray) -> np.ndarray:
+    """B3: J_E(c)^T G for E(c) = W2 relu(W1 c + b1) + b2, row by row: W1^T (relu'(W1 c + b1) * (W2^T G)),
+    relu'(0) = 0.  fp64."""
+    pre = np.asarray(Cin, np.float64) @ np.asarray(W1, np.float64).T + np.asarray(b1, np.float64)
+    dh = (np.asarray(G, np.float64) @ np.asarray(W2, np.float64)) * (pre > 0)
+    return dh @ np.asarray(W1, np.float64)
+
+
+def grad_restore(dY: np.ndarray, X: np.ndarray, Ct: np.ndarray, ret: np.ndarray, G: np.ndarray, H: np.ndarray,
+                 b: Buckets, g: Optional[np.ndarray] = None):
+    """B5: (dX [n, d], dg [n, k]) of y_t = sum_s g_ts (o_b + x_t - c~_b) with c_b the bucket mean
+    (reading R27).  ret = o (combined expert outputs, C layout); G from B1, H from B3 (C layout)."""
+    dY = np.asarray(dY, np.float64)
+    X = np.asarray(X, np.float64)
+    n, k = b.bucket.shape
+    cnt = np.diff(b.row_start).astype(np.float64)
+    Gm, Hm = np.asarray(G, np.float64), np.asarray(H, np.float64)
+    dX = np.zeros_like(dY)
+    dg = np.zeros((n, k))
+    for s in range(k):
+        bs = b.bucket[:, s]
+        gw = np.ones(n) if g is None else np.asarray(g, np.float64)[:, s]
+        dX += gw[:, None] * dY + (Hm[bs] - Gm[bs]) / cnt[bs][:, None]
+        dg[:, s] = (dY * (np.asarray(ret, np.float64)[bs] + X - np.asarray(Ct, np.float64)[bs])).sum(axis=1)
+    return dX, dg
+
+
+def lsh_layer_backward(X, zeta, b: Buckets, Ct, ret, experts, dY, g=None):
+    """Single-rank composition B1 -> B3 (per expert) -> B5 in fp64 (the exchanges B2/B4 are the
+    identity at one rank; dispatch_sim/combine_sim move G and H like c~ and o)."""
+    k = b.bucket.shape[1]
+    G = grad_compress(dY, b, k, g)
+    H = np.zeros_like(G)
+    off = 0
+    for e, me in enumerate(b.expert_rows):
+        if me:
+            W1, b1, W2, _ = experts[e]
+            H[off:off + me] = expert_ffn_vjp(np.asarray(Ct, np.float64)[off:off + me], W1, b1, W2, G[off:off + me])
+        off += me
+    dX, dg = grad_restore(dY, X, Ct, ret, G, H, b, g)
+    return G, H, dX, dg
+
