@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-uncompressed", action="store_true")
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--no-backward", action="store_true", help="skip the NEXT-1 backward timing")
     p.add_argument("--profile", action="store_true", help="minimal run for ncu: warmup + steps eager, no extras")
     return p.parse_args()
 
@@ -435,6 +436,39 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                "what": "permute -> all-to-all of every routed token -> expert FFN on n*k rows -> all-to-all -> unpermute",
                "speedup_of_lsh": bms / ms}
 
+    # ---- NEXT-1 backward of the LSH-specific steps (grad_compress, grad_restore), graph-timed ----
+    bwd = None
+    if not args.no_backward and world == 1:
+        gen = torch.Generator(device=dev).manual_seed(11)
+        dY = torch.randn(X.shape, generator=gen, device=dev).to(X.dtype)
+        Gb = torch.empty((nk, d), dtype=X.dtype, device=dev)
+        dxb = torch.empty_like(X)
+        gws = torch.empty(1 << 22, dtype=torch.uint8, device=dev)
+        parts = {"grad_compress": lambda: L.grad_compress(dY, comp, out=Gb, workspace=gws),
+                 "grad_restore": lambda: L.grad_restore(dY, X, comp.centroids, ret, Gb, Gb, comp, dx=dxb)}
+        bwd = {}
+        for nm, fn in parts.items():
+            fn()
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, stream=stream):
+                fn()
+            tt = []
+            for _ in range(args.steps):
+                flush.zero_()
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                gph.replay()
+                b_.record(stream)
+                torch.cuda.synchronize()
+                tt.append(a_.elapsed_time(b_))
+            bwd[nm + "_us"] = statistics.median(tt) * 1e3
+        sb = 2 if X.dtype == torch.bfloat16 else 4
+        bwd["grad_compress_hbm_bytes"] = (nk + m) * d * sb
+        bwd["grad_compress_gbs"] = bwd["grad_compress_hbm_bytes"] / bwd["grad_compress_us"] / 1e3
+        bwd["what"] = ("NEXT-1 (reading R27): G = per-bucket sums of dY (grad_compress) and dX = dY + (H - G)/n_b "
+                       "(grad_restore), each a CUDA-graph replay with L2 flushed; the expert's own backward and "
+                       "the two exchanges are not included (H = G stand-in)")
+
     L.check_device_error()
     # ---- the dominant kernel alone (the hash launch), CUDA-graph replay on `stream`, L2 flushed
     # before each replay, CUDA events on `stream` around the replay: its device time per launch ----
@@ -490,6 +524,7 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                         "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
                 "clocks": clk.summary(),
                 "uncompressed_baseline": unc,
+                "backward_lsh": bwd,
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
 

@@ -207,6 +207,32 @@ lshmoe_status lshmoe_restore(const void* x, const void* centroids, const void* r
                              lshmoe_dtype dtype, int64_t n, int d, const int32_t* bucket, int k,
                              const float* gate_weight, void* y, lshmoe_stream stream);
 
+/* ---- NEXT-1: backward of the compressed path (reading R27) --------------------------------------
+   The paper trains with LSH-MoE but never writes the gradient.  Reading R27: codes and
+   buckets are constants, the wire rounding c~ = RNE(mean) is straight-through, and with the
+   forward y_t = sum_s g_ts (o_b + x_t - c~_b), c_b = mean of the bucket's x:
+     lshmoe_grad_compress  G_b = sum_{(t,s) in b} g_ts dY_t        (dL/do_b), send layout [m, d]
+     (G goes to the expert's rank with lshmoe_dispatch; the expert's own backward gives
+      H_b = J_E(c~_b)^T G_b; H comes back with lshmoe_combine)
+     lshmoe_grad_restore   dX_t = sum_s [ g_ts dY_t + (H_b - G_b) / n_b ],
+                           dg_ts = dY_t . (o_b + x_t - c~_b)
+   bucket / perm / row_start are lshmoe_compress's outputs of the same forward.  Summation order of
+   G is the forward's perm order (fp32 accumulation, one rounding to dtype; grad_out_f32 nullable
+   keeps the fp32 sums).  Workspace: lshmoe_grad_compress_workspace(d) bytes, any contents. */
+lshmoe_status lshmoe_grad_compress_workspace(int d, size_t* bytes /* [host] */);
+lshmoe_status lshmoe_grad_compress(const void* dy, lshmoe_dtype dtype, int64_t n, int d,
+                                   const float* gate_weight /* nullable [n, k] */, const int32_t* bucket,
+                                   const int32_t* perm, const int32_t* row_start, int k,
+                                   void* grad_out /* [n*k, d]: rows [0, m) written */,
+                                   float* grad_out_f32 /* nullable [n*k, d] */,
+                                   void* workspace, size_t workspace_bytes, lshmoe_stream stream);
+lshmoe_status lshmoe_grad_restore(const void* dy, const void* x, const void* centroids, const void* returned,
+                                  const void* grad_c /* G [m, d] */, const void* grad_ret /* H [m, d] */,
+                                  lshmoe_dtype dtype, int64_t n, int d, const int32_t* bucket,
+                                  const int32_t* row_start, int k, const float* gate_weight /* nullable */,
+                                  void* dx /* out [n, d] */, float* dgate /* out, nullable [n, k] fp32 */,
+                                  lshmoe_stream stream);
+
 /* ---- uncompressed expert-parallel baseline (§2.2): same machinery, no LSH ---------
    lshmoe_permute: rows of x copied into send [n*k, d] grouped by expert (ascending (t, s)
    within an expert), slot int32 [n, k] = send row of copy (t, s), expert_rows [E] = n_e.

@@ -43,6 +43,10 @@ _SIGS = {
     "lshmoe_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _sz, _vp], _i32),
     "lshmoe_sp_rows": ([_i32, _i32], _i32),
     "lshmoe_sp_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _i32, _vp, _vp], _i32),
+    "lshmoe_grad_compress_workspace": ([_i32, ctypes.POINTER(_sz)], _i32),
+    "lshmoe_grad_compress": ([_vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp], _i32),
+    "lshmoe_grad_restore": ([_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _vp],
+                            _i32),
     "lshmoe_compress_workspace": ([_i64, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
     "lshmoe_compress": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                          _vp, _sz, _vp], _i32),
@@ -300,6 +304,43 @@ def compress(x: torch.Tensor, codes: torch.Tensor, experts: torch.Tensor, num_ex
                                 _ptr(out.num_rows), _ptr(out.centroids), _ptr(out.centroids_f32),
                                 _ptr(workspace), workspace.numel(), _stream(stream)), "lshmoe_compress")
     return out
+
+
+# ---- NEXT-1 backward (reading R27) -----------------------------------------------------------
+def grad_compress(dy: torch.Tensor, comp: "Compressed", gate_weight: Optional[torch.Tensor] = None,
+                  out: Optional[torch.Tensor] = None, out_f32: Optional[torch.Tensor] = None,
+                  workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """G [n*k, d] (rows [0, m) valid): per-centroid-row sums of g_ts dY_t over the forward's buckets."""
+    _require_cuda(dy)
+    n, d = dy.shape
+    k = comp.bucket.shape[1]
+    if out is None:
+        out = torch.empty((n * k, d), dtype=dy.dtype, device=dy.device)
+    b = ctypes.c_size_t(0)
+    _check(_lib.lshmoe_grad_compress_workspace(d, ctypes.byref(b)), "lshmoe_grad_compress_workspace")
+    if workspace is None or workspace.numel() < b.value:
+        workspace = torch.empty(b.value, dtype=torch.uint8, device=dy.device)
+    _check(_lib.lshmoe_grad_compress(_ptr(dy), _dt(dy), n, d, _ptr(gate_weight), _ptr(comp.bucket), _ptr(comp.perm),
+                                     _ptr(comp.row_start), k, _ptr(out), _ptr(out_f32), _ptr(workspace),
+                                     workspace.numel(), _stream(stream)), "lshmoe_grad_compress")
+    return out
+
+
+def grad_restore(dy: torch.Tensor, x: torch.Tensor, centroids: torch.Tensor, returned: torch.Tensor,
+                 grad_c: torch.Tensor, grad_ret: torch.Tensor, comp: "Compressed",
+                 gate_weight: Optional[torch.Tensor] = None, dx: Optional[torch.Tensor] = None,
+                 want_dgate: bool = False, stream=None):
+    """(dX [n, d], dgate [n, k] fp32 or None) of the compressed layer (reading R27)."""
+    _require_cuda(dy, x, centroids, returned, grad_c, grad_ret)
+    n, d = x.shape
+    k = comp.bucket.shape[1]
+    if dx is None:
+        dx = torch.empty_like(x)
+    dg = torch.empty((n, k), dtype=torch.float32, device=x.device) if want_dgate else None
+    _check(_lib.lshmoe_grad_restore(_ptr(dy), _ptr(x), _ptr(centroids), _ptr(returned), _ptr(grad_c), _ptr(grad_ret),
+                                    _dt(x), n, d, _ptr(comp.bucket), _ptr(comp.row_start), k, _ptr(gate_weight),
+                                    _ptr(dx), _ptr(dg), _stream(stream)), "lshmoe_grad_restore")
+    return dx, dg
 
 
 # ---- a6 / a8 ---------------------------------------------------------------------------------

@@ -163,6 +163,47 @@ lshmoe_status lshmoe_compress(const void* x, lshmoe_dtype dtype, int64_t n, int 
   return cuda_status(err, "lshmoe_compress");
 }
 
+lshmoe_status lshmoe_grad_compress_workspace(int d, size_t* bytes) {
+  REQUIRE(bytes != nullptr && d >= 1, LSHMOE_EINVAL, "bad arguments");
+  *bytes = grad_compress_workspace_layout(d, nullptr, nullptr, nullptr);
+  return LSHMOE_OK;
+}
+
+lshmoe_status lshmoe_grad_compress(const void* dy, lshmoe_dtype dtype, int64_t n, int d, const float* gate_weight,
+                                   const int32_t* bucket, const int32_t* perm, const int32_t* row_start, int k,
+                                   void* grad_out, float* grad_out_f32, void* workspace, size_t workspace_bytes,
+                                   lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, dtype, n, d);
+  if (st) return st;
+  REQUIRE(k >= 1, LSHMOE_EINVAL, "k < 1");
+  REQUIRE(n * k < (int64_t(1) << 31), LSHMOE_EUNSUPPORTED, "n * k >= 2^31");
+  if (n == 0) return LSHMOE_OK;
+  REQUIRE(dy && bucket && perm && row_start && grad_out, LSHMOE_EINVAL, "NULL pointer");
+  REQUIRE(aligned16(dy) && aligned16(grad_out) && (!grad_out_f32 || aligned16(grad_out_f32)), LSHMOE_EINVAL,
+          "dy / grad_out must be 16-byte aligned");
+  REQUIRE(workspace && workspace_bytes >= grad_compress_workspace_layout(d, nullptr, nullptr, nullptr), LSHMOE_EINVAL,
+          "workspace too small (see lshmoe_grad_compress_workspace)");
+  return cuda_status(launch_grad_compress(dy, dtype, n, d, gate_weight, bucket, perm, row_start, k, grad_out,
+                                          grad_out_f32, workspace, stream),
+                     "lshmoe_grad_compress");
+}
+
+lshmoe_status lshmoe_grad_restore(const void* dy, const void* x, const void* ct, const void* ret, const void* G,
+                                  const void* H, lshmoe_dtype dtype, int64_t n, int d, const int32_t* bucket,
+                                  const int32_t* row_start, int k, const float* g, void* dx, float* dg,
+                                  lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, dtype, n, d);
+  if (st) return st;
+  REQUIRE(k >= 1, LSHMOE_EINVAL, "k < 1");
+  if (n == 0) return LSHMOE_OK;
+  REQUIRE(dy && x && ct && ret && G && H && bucket && row_start && dx, LSHMOE_EINVAL, "NULL pointer");
+  REQUIRE(aligned16(dy) && aligned16(x) && aligned16(ct) && aligned16(ret) && aligned16(G) && aligned16(H) &&
+              aligned16(dx),
+          LSHMOE_EINVAL, "rows must be 16-byte aligned");
+  return cuda_status(launch_grad_restore(dy, x, ct, ret, G, H, dtype, n, d, bucket, row_start, k, g, dx, dg, stream),
+                     "lshmoe_grad_restore");
+}
+
 lshmoe_status lshmoe_restore(const void* x, const void* ct, const void* ret, lshmoe_dtype dtype, int64_t n, int d,
                              const int32_t* bucket, int k, const float* g, void* y, lshmoe_stream stream) {
   lshmoe_status st = check_token_shape(__func__, dtype, n, d);

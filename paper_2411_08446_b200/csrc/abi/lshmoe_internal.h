@@ -51,6 +51,14 @@ int launch_permute(const void* x, lshmoe_dtype dtype, int64_t n, int d, const in
 int launch_unpermute(const void* returned, lshmoe_dtype dtype, int64_t n, int d, const int32_t* slot, int k,
                      const float* g, void* y, void* stream);
 
+size_t grad_compress_workspace_layout(int d, void* base, int32_t** hdr, float** partial);
+int launch_grad_compress(const void* dy, lshmoe_dtype dtype, int64_t n, int d, const float* gw, const int32_t* bucket,
+                         const int32_t* perm, const int32_t* row_start, int k, void* grad_out, float* grad_out_f32,
+                         void* ws, void* stream);
+int launch_grad_restore(const void* dy, const void* x, const void* ct, const void* ret, const void* G, const void* H,
+                        lshmoe_dtype dtype, int64_t n, int d, const int32_t* bucket, const int32_t* row_start, int k,
+                        const float* g, void* dx, float* dg, void* stream);
+
 int launch_restore(const void* x, const void* ct, const void* ret, lshmoe_dtype dtype, int64_t n, int d,
                    const int32_t* bucket, int k, const float* g, void* y, void* stream);
 

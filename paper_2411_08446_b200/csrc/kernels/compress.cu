@@ -112,6 +112,8 @@ struct Params {
   int max_range;                   // K3: max perm entries per CTA range
   int dyn_smem;                    // K2: dynamic shared memory bytes
   int permute;                     // 1: uncompressed baseline (group by expert only)
+  int grad;                        // 1: NEXT-1 grad_compress: weighted per-row SUMS (no 1/count)
+  const float* gw;                 // grad: gate weights [nk] or nullptr (weight 1)
   int diag;                        // 1: record per-CTA globaltimer stamps (diagnostics)
 };
 
@@ -523,6 +525,23 @@ __device__ __forceinline__ void add_chunk16(float* acc, uint4 raw) {
   }
 }
 
+template <typename T>
+__device__ __forceinline__ void add_chunk16_w(float* acc, uint4 raw, float w) {   // acc += w * x (one rounding)
+  if (sizeof(T) == 2) {
+    const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[2 * i] = fmaf(w, __uint_as_float(u[i] << 16), acc[2 * i]);
+      acc[2 * i + 1] = fmaf(w, __uint_as_float(u[i] & 0xFFFF0000u), acc[2 * i + 1]);
+    }
+  } else {
+    acc[0] = fmaf(w, __uint_as_float(raw.x), acc[0]);
+    acc[1] = fmaf(w, __uint_as_float(raw.y), acc[1]);
+    acc[2] = fmaf(w, __uint_as_float(raw.z), acc[2]);
+    acc[3] = fmaf(w, __uint_as_float(raw.w), acc[3]);
+  }
+}
+
 template <int VC>
 __device__ __noinline__ void store_f32_copy(float* dst, const float* v) {   // tier-2 parity output only
 #pragma unroll
@@ -569,7 +588,7 @@ __device__ __forceinline__ void add_chunk8(float* acc, uint2 raw) {
 template <typename T>
 __device__ __forceinline__ void store_chunk8(const Params& P, int row, int ch, const float* acc, float cnt) {
   constexpr int VC = sizeof(T) == 2 ? 4 : 2;
-  const float rc = __frcp_rn(cnt);
+  const float rc = P.grad ? 1.0f : __frcp_rn(cnt);
   float v[VC];
 #pragma unroll
   for (int e = 0; e < VC; ++e) v[e] = acc[e] * rc;
@@ -603,10 +622,12 @@ extern __shared__ __align__(1024) uint8_t g_dsmem[];
 struct CentroidCtx {                     // one CTA's view of its perm range (centroid phase)
   int p_begin, p_end, range, w, lane, w_begin, w_end, tok_off;
   uint32_t prev_row;                     // row of entry w_begin - 1
+  int cut_rs, cut_re;                    // threads 0 / 1: perm extent of the range's first / last row
   __device__ uint8_t* ring() const { return g_dsmem + w * kQ * kRingSlot; }
   __device__ float* slot0() const { return reinterpret_cast<float*>(g_dsmem + kWarps * kQ * kRingSlot); }
   __device__ uint32_t* s_row() const { return reinterpret_cast<uint32_t*>(slot0() + kWarps * kWpartFloats); }
   __device__ int32_t* s_tok() const { return reinterpret_cast<int32_t*>(s_row()) + tok_off; }
+  __device__ float* s_wt(int max_range) const { return reinterpret_cast<float*>(s_tok()) + max_range; }
   __device__ uint32_t row_at(int p) const { return s_row()[p - p_begin + 1]; }
   __device__ int wbeg(int ww) const { return p_begin + range_begin(ww, range, kWarps); }
   __device__ float* wpart(int ww, int slot) const {   // slot 0: own region; slot 1: the warp's ring
@@ -652,13 +673,16 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
 #pragma unroll
     for (int t = 0; t < CPL; ++t) {
       const int c = lane + 32 * t;
-      if (full || c < ncb) add_chunk16<T>(acc[t], *reinterpret_cast<const uint4*>(st + 16 * c));
+      if (full || c < ncb) {
+        if (P.gw) add_chunk16_w<T>(acc[t], *reinterpret_cast<const uint4*>(st + 16 * c), X.s_wt(P.max_range)[p - X.p_begin]);
+        else add_chunk16<T>(acc[t], *reinterpret_cast<const uint4*>(st + 16 * c));
+      }
     }
     const uint32_t next = X.row_at(p + 1);
     if (next == row && p + 1 < w_end) continue;         // the segment goes on
     const bool head = seg_start > w_begin || X.prev_row != row;   // the row starts in this warp
     if (head && next != row) {                // the whole row lies in this warp's sub-range
-      const float rc = __frcp_rn(static_cast<float>(p + 1 - seg_start));
+      const float rc = P.grad ? 1.0f : __frcp_rn(static_cast<float>(p + 1 - seg_start));
 #pragma unroll
       for (int t = 0; t < CPL; ++t) {
         const int c = lane + 32 * t;
@@ -711,7 +735,7 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
     const int wl = range_cta(hi - 1 - X.p_begin, X.range, kWarps);
     const bool before = lo == X.p_begin && X.row_at(X.p_begin - 1) == r;
     const bool after = hi == X.p_end && X.row_at(X.p_end) == r;
-    const float rc = __frcp_rn(static_cast<float>(hi - lo));
+    const float rc = P.grad ? 1.0f : __frcp_rn(static_cast<float>(hi - lo));
 #pragma unroll
     for (int t = 0; t < CPL; ++t) {
       const int c = lane + 32 * t;
@@ -756,11 +780,29 @@ __device__ __forceinline__ int expert_at(const int* s_goff, int E, int p) {
   return lo;
 }
 
+// Threads 0 and 1 load the perm extents [rs, re) of the range's first and last rows right after
+// the index fill, so the loads are in flight during the reduction (used by merge_cut_rows).
+__device__ __forceinline__ void prefetch_cut_extent(const Params& P, CentroidCtx& X, const int* s_goff,
+                                                    const int* s_mrow, const int* s_cut) {
+  const int which = threadIdx.x;
+  if (which >= 2) return;
+  if (P.grad) {                               // row extents straight from the forward's row_start
+    const uint32_t r = X.row_at(which == 0 ? X.p_begin : X.p_end - 1);
+    X.cut_rs = ldcg(P.row_start + r);
+    X.cut_re = ldcg(P.row_start + r + 1);
+  } else {
+    const int e = s_cut[2 * which], lr = s_cut[2 * which + 1];
+    X.cut_rs = ldcg(P.rsl + s_goff[e] + lr);
+    X.cut_re = lr + 1 < s_mrow[e] ? ldcg(P.rsl + s_goff[e] + lr + 1) : s_goff[e + 1];
+  }
+}
+
 // Phase B of one CTA: its perm range's rows (global ids = row offset of the expert + local row),
 // token ids and bucket outputs, then the centroid reduction.  s_cut[0..1] receive the (expert,
 // local row) of the range's first and last entries for the cut-row merge.
 template <typename T>
-__device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_roff, int* s_cut, CentroidCtx& X) {
+__device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_roff, const int* s_mrow, int* s_cut,
+                               CentroidCtx& X) {
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
   X.p_begin = range_begin(b, P.nk, G);
   X.p_end = range_begin(b + 1, P.nk, G);
@@ -790,6 +832,7 @@ __device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_
   }
   __syncthreads();
   dstamp(P, 2, 1);
+  prefetch_cut_extent(P, X, s_goff, s_mrow, s_cut);
   X.w_begin = X.wbeg(X.w);
   X.w_end = X.wbeg(X.w + 1);
   X.prev_row = X.row_at(X.w_begin - 1);
@@ -815,36 +858,32 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
   if (X.range == 0) return;
   __threadfence();                            // publish this CTA's partials before arriving
   __syncthreads();
-  if (tid == 0) {
-    s_job[0] = s_job[4] = -1;
+  if (tid < 2) {                              // thread `which` handles one candidate row
+    const int which = tid;
+    s_job[4 * which] = -1;
     const uint32_t r0 = X.row_at(X.p_begin), rl = X.row_at(X.p_end - 1);
     const bool before = X.row_at(X.p_begin - 1) == r0;
     const bool after = X.row_at(X.p_end) == rl;
-    int nj = 0;
-    for (int which = 0; which < 2; ++which) {
-      if (which == 0 && !before) continue;
-      if (which == 1 && (!after || (before && rl == r0))) continue;
-      const int e = s_cut[2 * which], lr = s_cut[2 * which + 1];
-      const int rs = ldcg(P.rsl + s_goff[e] + lr);
-      const int re = lr + 1 < s_mrow[e] ? ldcg(P.rsl + s_goff[e] + lr + 1) : s_goff[e + 1];
+    const bool cand = which == 0 ? before : (after && !(before && rl == r0));
+    if (cand) {
+      const int rs = X.cut_rs, re = X.cut_re;
       const int b0 = range_cta(rs, P.nk, G), b1 = range_cta(re - 1, P.nk, G);
       int expected = 0;
       for (int bb = b0; bb <= b1; ++bb) expected += range_begin(bb + 1, P.nk, G) > range_begin(bb, P.nk, G);
       const int old = atomicAdd(reinterpret_cast<int*>(P.bar) + kArrive + b0, 1);   // counters start at -1
       if (old + 2 == expected) {
         __threadfence();                      // acquire the other CTAs' partials
-        s_job[4 * nj + 0] = static_cast<int>(which == 0 ? r0 : rl);
-        s_job[4 * nj + 1] = rs;
-        s_job[4 * nj + 2] = re;
-        s_job[4 * nj + 3] = b0 | (b1 << 16);
-        ++nj;
+        s_job[4 * which + 0] = static_cast<int>(which == 0 ? r0 : rl);
+        s_job[4 * which + 1] = rs;
+        s_job[4 * which + 2] = re;
+        s_job[4 * which + 3] = b0 | (b1 << 16);
       }
     }
   }
   __syncthreads();
   for (int j = 0; j < 2; ++j) {
     const int row = s_job[4 * j];
-    if (row < 0) break;
+    if (row < 0) continue;
     const int rs = s_job[4 * j + 1], re = s_job[4 * j + 2];
     const int b0 = s_job[4 * j + 3] & 0xFFFF, b1 = s_job[4 * j + 3] >> 16;
     const int nc8 = P.row_bytes / 8;
@@ -931,17 +970,76 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   if (P.diag && tid == 0 && blockIdx.x < 1024) P.bar[64 + 2 * blockIdx.x] = globaltimer_lo();
   CentroidCtx X;
   if (P.is_bf16) {
-    centroid_phase<__nv_bfloat16>(P, s_goff, s_roff, s_cut, X);
+    centroid_phase<__nv_bfloat16>(P, s_goff, s_roff, s_mrow, s_cut, X);
     dstamp(P, 2, 2);
     merge_cut_rows<__nv_bfloat16>(P, X, s_goff, s_mrow, s_cut, s_job);
   } else {
-    centroid_phase<float>(P, s_goff, s_roff, s_cut, X);
+    centroid_phase<float>(P, s_goff, s_roff, s_mrow, s_cut, X);
     dstamp(P, 2, 2);
     merge_cut_rows<float>(P, X, s_goff, s_mrow, s_cut, s_job);
   }
   __syncthreads();
   dstamp(P, 2, 3);
   if (P.diag && tid == 0 && blockIdx.x < 1024) P.bar[65 + 2 * blockIdx.x] = globaltimer_lo();
+}
+
+// ---- NEXT-1 grad_compress: G_b = sum_{(t,s) in b} g_ts dY_t over the forward's buckets --------
+// The centroid kernel's machinery with the row of perm entry p = bucket[perm[p]], the gate weight
+// of the copy staged beside its token id, and no 1/count; cut rows via the forward's row_start.
+__global__ void __launch_bounds__(kThreads, 1) grad_centroid_kernel(Params P) {
+  __shared__ int s_cut[4];
+  __shared__ int s_job[8];
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  CentroidCtx X;
+  X.p_begin = range_begin(b, P.nk, G);
+  X.p_end = range_begin(b + 1, P.nk, G);
+  X.range = X.p_end - X.p_begin;
+  if (X.range == 0) return;
+  X.lane = tid % 32;
+  X.w = tid / 32;
+  X.tok_off = P.max_range + 2;
+  uint32_t* s_row = X.s_row();
+  int32_t* s_tok = X.s_tok();
+  float* s_w = X.s_wt(P.max_range);
+  for (int i = tid; i < X.range + 2; i += kThreads) {
+    const int p = X.p_begin - 1 + i;
+    uint32_t row = 0xFFFFFFFFu;
+    if (p >= 0 && p < P.nk) {
+      const int c = __ldg(P.perm + p);
+      row = static_cast<uint32_t>(__ldg(P.bucket + c));
+      if (i >= 1 && i <= X.range) {
+        s_tok[i - 1] = c / P.k;
+        if (P.gw) s_w[i - 1] = __ldg(P.gw + c);
+      }
+    }
+    s_row[i] = row;
+  }
+  __syncthreads();
+  prefetch_cut_extent(P, X, nullptr, nullptr, nullptr);
+  X.w_begin = X.wbeg(X.w);
+  X.w_end = X.wbeg(X.w + 1);
+  X.prev_row = X.row_at(X.w_begin - 1);
+  for (int c0 = 0, cb = 0; c0 < P.nch; c0 += kBlkChunks, ++cb) {
+    const int ncb = min(kBlkChunks, P.nch - c0);
+    const int cpl = (ncb + 31) / 32;
+    if (P.is_bf16) {
+      switch (cpl) {
+        case 1: centroid_block<__nv_bfloat16, 1>(P, X, cb, c0, ncb); break;
+        case 2: centroid_block<__nv_bfloat16, 2>(P, X, cb, c0, ncb); break;
+        case 3: centroid_block<__nv_bfloat16, 3>(P, X, cb, c0, ncb); break;
+        default: centroid_block<__nv_bfloat16, 4>(P, X, cb, c0, ncb); break;
+      }
+    } else {
+      switch (cpl) {
+        case 1: centroid_block<float, 1>(P, X, cb, c0, ncb); break;
+        case 2: centroid_block<float, 2>(P, X, cb, c0, ncb); break;
+        case 3: centroid_block<float, 3>(P, X, cb, c0, ncb); break;
+        default: centroid_block<float, 4>(P, X, cb, c0, ncb); break;
+      }
+    }
+  }
+  if (P.is_bf16) merge_cut_rows<__nv_bfloat16>(P, X, nullptr, nullptr, s_cut, s_job);
+  else merge_cut_rows<float>(P, X, nullptr, nullptr, s_cut, s_job);
 }
 
 constexpr int kCentroidSmemMax = 200 * 1024;   // K3 dynamic smem + static <= 227 KB
@@ -952,8 +1050,8 @@ int centroid_max_range(int nk) {
   return (nk + G - 1) / G + 1;
 }
 // K3 shared memory: per-warp rings, warp partials, the range's index arrays.
-int centroid_smem(int max_range) {
-  return kWarps * kQ * kRingSlot + kWarps * kWpartFloats * 4 + 4 * (2 * max_range + 2);
+int centroid_smem(int max_range) {   // + the grad mode's per-entry weights
+  return kWarps * kQ * kRingSlot + kWarps * kWpartFloats * 4 + 4 * (3 * max_range + 2);
 }
 
 int g_diag = 0;                              // lshmoe_set_diagnostics
@@ -1105,6 +1203,66 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
   P.cent = static_cast<uint8_t*>(centroids);
   P.cent32 = centroids_f32;
   return launch_chain(P, st);
+}
+
+size_t grad_compress_workspace_layout(int d, void* base, int32_t** hdr, float** partial) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_hdr = take(sizeof(int32_t) * kHdr);
+  const size_t o_part = take(sizeof(float) * 2 * kMaxGrid * d);
+  if (base) {
+    *hdr = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(base) + o_hdr);
+    *partial = reinterpret_cast<float*>(static_cast<uint8_t*>(base) + o_part);
+  }
+  return off;
+}
+
+int launch_grad_compress(const void* dy, lshmoe_dtype dtype, int64_t n, int d, const float* gw, const int32_t* bucket,
+                         const int32_t* perm, const int32_t* row_start, int k, void* grad_out, float* grad_out_f32,
+                         void* ws, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nk = static_cast<int>(n * k);
+  if (nk == 0) return 0;
+  static bool configured = false;
+  if (!configured) {
+    const int err = cudaFuncSetAttribute(grad_centroid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kCentroidSmemMax);
+    if (err) return err;
+    configured = true;
+  }
+  const int max_range = centroid_max_range(nk);
+  const int smem = centroid_smem(max_range);
+  if (smem > kCentroidSmemMax) return cudaErrorInvalidValue;
+  int32_t* hdr;
+  float* partial;
+  grad_compress_workspace_layout(d, ws, &hdr, &partial);
+  int err = cudaMemsetAsync(hdr, 0xFF, sizeof(int32_t) * kHdr, st);   // arrival counters at -1
+  if (err) return err;
+  Params P{};
+  P.x = static_cast<const uint8_t*>(dy);
+  P.d = d;
+  P.row_bytes = d * (dtype == LSHMOE_F32 ? 4 : 2);
+  P.nch = P.row_bytes / 16;
+  P.is_bf16 = dtype == LSHMOE_BF16;
+  P.k = k;
+  P.nk = nk;
+  P.bucket = const_cast<int32_t*>(bucket);
+  P.perm = const_cast<int32_t*>(perm);
+  P.row_start = const_cast<int32_t*>(row_start);
+  P.cent = static_cast<uint8_t*>(grad_out);
+  P.cent32 = grad_out_f32;
+  P.bar = reinterpret_cast<unsigned*>(hdr);
+  P.partial = partial;
+  P.max_range = max_range;
+  P.grad = 1;
+  P.gw = gw;
+  grad_centroid_kernel<<<centroid_grid(), kThreads, smem, st>>>(P);
+  count_launches(1);
+  return cudaGetLastError();
 }
 
 int launch_permute(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int32_t* experts, int k, int E,
