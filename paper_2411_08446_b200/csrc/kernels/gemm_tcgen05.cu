@@ -37,17 +37,26 @@ constexpr int kEpiWarps = 8;                // two warps per TMEM lane quadrant,
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiScratch = 1024;           // per epilogue warp (bias slice)
 
-template <int BN, int kCta>
+constexpr int kMaxLocalExperts = 256;
+constexpr int kStaticSmem = 3072;           // sched tables (2 * 257 ints) + mbarriers + TMEM slot
+// kScratch: epilogue scratch bytes per epilogue warp (0 lets the ring take one more stage).
+template <int BN, int kCta, int kScratch = kEpiScratch>
 struct Cfg {
   static constexpr int kBRows = BN / kCta;  // B rows staged by each CTA
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTxBytes = kCta * kStageBytes;   // bytes the leader's full barrier waits for
-  static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
+  static constexpr int kFixed = kEpiWarps * kScratch;   // dynamic smem besides the ring
+  // 227 KB per CTA on sm_100, minus the 3 KB static block (scheduler tables + barriers) that keeps
+  // the dynamic window 1024-byte aligned for SWIZZLE_128B
+  static constexpr int kBudget = 227 * 1024 - kStaticSmem - kFixed;
+  static constexpr int kStages = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + kEpiWarps * kEpiScratch;
+  static constexpr int kSmem = kStages * kStageBytes + kFixed;
 };
+template <class Epi>
+struct EpiScratch { static constexpr int value = kEpiScratch; };
 
 struct WorkItem {
   int a_row;       // first A row of this CTA's 128-row slice
@@ -97,8 +106,6 @@ struct HashSched {
     return w;
   }
 };
-
-constexpr int kMaxLocalExperts = 256;
 
 struct FfnSched {
   const int32_t* recv_rows;  // [E_local, world]
@@ -335,20 +342,16 @@ struct BiasActEpi {
   __nv_bfloat16* out;         // [rows, N]
   int N;
   bool relu;
-  // the unit's BN bias values are staged once per warp in shared memory (broadcast reads)
-  __device__ void begin(const WorkItem& w, uint8_t* scratch) {
-    const int lane = threadIdx.x % 32;
-    const uint4* src = reinterpret_cast<const uint4*>(bias + static_cast<int64_t>(w.tag0) * N + w.tag1);
-    for (int i = lane; i < BN / 8; i += 32) reinterpret_cast<uint4*>(scratch)[i] = src[i];
-    __syncwarp();
-  }
+  int exp = 0;                // experiment (LSHMOE_FFN_EXP): 1 = no output stores, 2 = no MMAs
+  const __nv_bfloat16* bias_unit;   // this unit's BN bias values (read-only cache, warp broadcast)
+  __device__ void begin(const WorkItem& w, uint8_t*) { bias_unit = bias + static_cast<int64_t>(w.tag0) * N + w.tag1; }
   __device__ void consume(const WorkItem& w, int row, const uint32_t (&r)[32], int col0, const uint8_t* scratch) {
     if (row >= w.valid_rows) return;
-    const uint32_t* bw = reinterpret_cast<const uint32_t*>(scratch) + col0 / 2;
+    const uint32_t* bw = reinterpret_cast<const uint32_t*>(bias_unit) + col0 / 2;
     uint32_t packed[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const uint32_t b2 = bw[i];
+      const uint32_t b2 = __ldg(bw + i);
       float v0 = __uint_as_float(r[2 * i]) + __uint_as_float(b2 << 16);
       float v1 = __uint_as_float(r[2 * i + 1]) + __uint_as_float(b2 & 0xFFFF0000u);
       if (relu) {
@@ -359,29 +362,50 @@ struct BiasActEpi {
       packed[i] = *reinterpret_cast<uint32_t*>(&h);
     }
     uint4* dst = reinterpret_cast<uint4*>(out + static_cast<int64_t>(w.a_row + row) * N + w.tag1 + col0);
+    if (exp == 1) {
+      if ((packed[0] ^ packed[7] ^ packed[15]) == 0x12345678u) dst[0] = make_uint4(0, 0, 0, 0);   // keep the math live
+      return;
+    }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+    for (int i = 0; i < 2; ++i)   // 256-bit stores: each lane writes whole 32-byte sectors of its row
+      asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 2 * i), "r"(packed[8 * i]),
+                   "r"(packed[8 * i + 1]), "r"(packed[8 * i + 2]), "r"(packed[8 * i + 3]), "r"(packed[8 * i + 4]),
+                   "r"(packed[8 * i + 5]), "r"(packed[8 * i + 6]), "r"(packed[8 * i + 7])
+                   : "memory");
   }
   __device__ void finish(const WorkItem&, int, uint8_t*, int, int) {}
 };
+
+template <int BN>
+struct EpiScratch<BiasActEpi<BN>> { static constexpr int value = 0; };   // bias read via __ldg
+
+template <class Epi>
+__device__ __forceinline__ bool epi_skip_mma(const Epi&) { return false; }
+template <int BN>
+__device__ __forceinline__ bool epi_skip_mma(const BiasActEpi<BN>& e) { return e.exp == 2; }
 
 // ---- the kernel ----------------------------------------------------------------------------------
 template <int BN, int kCta, class Sched, class Epi>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                    Sched sched, Epi epi) {
-  using C = Cfg<BN, kCta>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using C = Cfg<BN, kCta, EpiScratch<Epi>::value>;
+  // Static block first (exactly kStaticSmem bytes, 1024-aligned), so the dynamic window that
+  // holds the TMA ring starts 1024-byte aligned (SWIZZLE_128B atoms) without a runtime pad.
+  __shared__ __align__(1024) uint8_t s_static[kStaticSmem];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  static_assert(8 * (2 * 8 + 4) + 8 + 2 * (kMaxLocalExperts + 1) * 4 <= kStaticSmem, "static block");
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();   // the layout assumption above must hold
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_static);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* epi_scratch = smem + C::kStages * C::kStageBytes + 256;
-  __shared__ int sched_tables[2 * (kMaxLocalExperts + 1)];
+  int* sched_tables = reinterpret_cast<int*>(s_static + 8 * (2 * 8 + 4) + 8);
+  uint8_t* epi_scratch = smem + C::kStages * C::kStageBytes;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -487,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t b0 = smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
+              if (epi_skip_mma(epi)) break;
               if (kCta == 2)
                 mma_bf16_ss_2cta(d_tmem, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), idesc,
                                  (kb | kk) != 0);
@@ -515,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = (warp - 2) / 4;                // which half of the BN columns it drains
     constexpr int kBlkPer = (BN / 32) * 4 / kEpiWarps;
     const int row = quad * 32 + lane;
-    uint8_t* scratch = epi_scratch + (warp - 2) * kEpiScratch;
+    uint8_t* scratch = epi_scratch + (warp - 2) * EpiScratch<Epi>::value;
     const uint32_t tempty_leader0 = kCta == 2 ? mapa_shared(&tempty[0], 0) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -593,14 +618,14 @@ int launch_tc(const CUtensorMap& a, const CUtensorMap& b, int K, const Sched& s,
   auto kern = tc_gemm_kernel<BN, kCta, Sched, Epi>;
   static bool configured = false;     // one attribute call per instantiation
   if (!configured) {
-    int err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, kCta>::kSmem);
+    int err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, kCta, EpiScratch<Epi>::value>::kSmem);
     if (err) return err;
     configured = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Cfg<BN, kCta>::kSmem;
+  cfg.dynamicSmemBytes = Cfg<BN, kCta, EpiScratch<Epi>::value>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -756,31 +781,32 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int cta = cta_mode("LSHMOE_FFN_CTA", 2);
   const int only = cta_mode("LSHMOE_FFN_ONLY", 0);   // experiment: 1 / 2 = launch only GEMM 1 / 2
+  const int exp = cta_mode("LSHMOE_FFN_EXP", 0);     // experiment: 1 = no output stores, 2 = no MMAs
   FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, ffn_prefetch(), nullptr, nullptr};
   const int bn1 = env_bn("LSHMOE_FFN_BN1", d_ffn, pick_bn(d_ffn));
   int err = 0;
   if (only == 2) {
   } else if (bn1 == 256) {
-    BiasActEpi<256> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true};
+    BiasActEpi<256> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true}; e1.exp = exp;
     err = launch_bn(bn1, cta, in, capacity, W1, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
   } else if (bn1 == 128) {
-    BiasActEpi<128> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true};
+    BiasActEpi<128> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true}; e1.exp = exp;
     err = launch_bn(bn1, cta, in, capacity, W1, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
   } else {
-    BiasActEpi<64> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true};
+    BiasActEpi<64> e1{static_cast<const __nv_bfloat16*>(b1), static_cast<__nv_bfloat16*>(hidden), d_ffn, true}; e1.exp = exp;
     err = launch_bn(bn1, cta, in, capacity, W1, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
   }
   if (err || only == 1) return err;
   FfnSched s2{recv_rows, E_local, world, d, 0, 0, ffn_prefetch(), nullptr, nullptr};
   const int bn2 = env_bn("LSHMOE_FFN_BN2", d, pick_bn(d));
   if (bn2 == 256) {
-    BiasActEpi<256> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false};
+    BiasActEpi<256> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false}; e2.exp = exp;
     return launch_bn(bn2, cta, hidden, capacity, W2, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, 0, st);
   } else if (bn2 == 128) {
-    BiasActEpi<128> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false};
+    BiasActEpi<128> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false}; e2.exp = exp;
     return launch_bn(bn2, cta, hidden, capacity, W2, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, 0, st);
   }
-  BiasActEpi<64> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false};
+  BiasActEpi<64> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false}; e2.exp = exp;
   return launch_bn(bn2, cta, hidden, capacity, W2, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, 0, st);
 }
 

@@ -133,8 +133,11 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
   return out;
 }
+// Remote arrive with the default .release.cta semantics (as CUTLASS's ClusterBarrier::arrive):
+// the TMEM reads it publishes are ordered by tcgen05.fence::before_thread_sync, and a .cluster
+// release would make the epilogue wait for all of its outstanding global stores (MEMBAR.GPU).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA: data lands in this CTA's shared memory, the transaction bytes are counted on the
 // barrier at the same offset in the leader CTA (rank 0): the peer bit (bit 24) is cleared.
