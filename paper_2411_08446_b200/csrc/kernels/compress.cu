@@ -494,8 +494,10 @@ constexpr int kBlkChunks = 128;          // 16-byte chunks per column block
 constexpr int kCPL = kBlkChunks / 32;    // chunks per lane per block
 constexpr int kRingSlot = 16 * kBlkChunks;
 constexpr int kWpartFloats = kBlkChunks * 8;   // one warp partial slot (fp32, up to 8 per chunk)
-constexpr int kQ = 10;                   // ring rows per warp (kQ - 1 in flight)
-static_assert(kWpartFloats * 4 <= kQ * kRingSlot, "a warp's slot-1 partial reuses its ring");
+constexpr int kQ = 10;                   // ring rows per warp at the largest (2 KB) slot
+constexpr int kRingWarp = kQ * kRingSlot;   // ring bytes per warp; slots are packed at 16*ncb bytes,
+                                            // so short rows get a deeper ring (1.5 KB rows: 13 slots)
+static_assert(kWpartFloats * 4 <= kRingWarp, "a warp's slot-1 partial reuses its ring");
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
@@ -623,29 +625,30 @@ struct CentroidCtx {                     // one CTA's view of its perm range (ce
   int p_begin, p_end, range, w, lane, w_begin, w_end, tok_off;
   uint32_t prev_row;                     // row of entry w_begin - 1
   int cut_rs, cut_re;                    // threads 0 / 1: perm extent of the range's first / last row
-  __device__ uint8_t* ring() const { return g_dsmem + w * kQ * kRingSlot; }
-  __device__ float* slot0() const { return reinterpret_cast<float*>(g_dsmem + kWarps * kQ * kRingSlot); }
+  __device__ uint8_t* ring() const { return g_dsmem + w * kRingWarp; }
+  __device__ float* slot0() const { return reinterpret_cast<float*>(g_dsmem + kWarps * kRingWarp); }
   __device__ uint32_t* s_row() const { return reinterpret_cast<uint32_t*>(slot0() + kWarps * kWpartFloats); }
   __device__ int32_t* s_tok() const { return reinterpret_cast<int32_t*>(s_row()) + tok_off; }
   __device__ float* s_wt(int max_range) const { return reinterpret_cast<float*>(s_tok()) + max_range; }
   __device__ uint32_t row_at(int p) const { return s_row()[p - p_begin + 1]; }
   __device__ int wbeg(int ww) const { return p_begin + range_begin(ww, range, kWarps); }
   __device__ float* wpart(int ww, int slot) const {   // slot 0: own region; slot 1: the warp's ring
-    return slot == 0 ? slot0() + ww * kWpartFloats : reinterpret_cast<float*>(g_dsmem + ww * kQ * kRingSlot);
+    return slot == 0 ? slot0() + ww * kWpartFloats : reinterpret_cast<float*>(g_dsmem + ww * kRingWarp);
   }
 };
 
 // One column block (chunks [c0, c0 + ncb), CPL = ceil(ncb / 32) chunks per lane) of the centroid
 // phase: stream the warp's rows through its ring, reduce segments, then combine cut rows.
-template <typename T, int CPL>
+template <typename T, int CPL, int QD = kQ>
 __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, int c0, int ncb) {
+  const int slotB = 16 * CPL * 32;           // packed ring slot (this block's row bytes, rounded to a lane round)
   constexpr int VC = 16 / sizeof(T);
   const int lane = X.lane, w = X.w, w_begin = X.w_begin, w_end = X.w_end;
   const bool full = ncb == CPL * 32;
   auto issue = [&](int p, int slot) {
     if (p < w_end) {
       const uint8_t* src = P.x + static_cast<int64_t>(X.s_tok()[p - X.p_begin]) * P.row_bytes + 16 * c0;
-      uint8_t* dst = X.ring() + slot * kRingSlot;
+      uint8_t* dst = X.ring() + slot * slotB;
 #pragma unroll
       for (int t = 0; t < CPL; ++t) {
         const int c = lane + 32 * t;
@@ -655,21 +658,21 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
     cp_async_commit();
   };
 #pragma unroll 1
-  for (int i = 0; i < kQ - 1; ++i) issue(w_begin + i, i);
+  for (int i = 0; i < QD - 1; ++i) issue(w_begin + i, i);
   float acc[CPL][VC];
 #pragma unroll
   for (int t = 0; t < CPL; ++t)
 #pragma unroll
     for (int e = 0; e < VC; ++e) acc[t][e] = 0.0f;
-  int seg_start = w_begin, rd = 0, wr = kQ - 1;   // ring slots: next to read, next to fill
+  int seg_start = w_begin, rd = 0, wr = QD - 1;   // ring slots: next to read, next to fill
   uint32_t row = w_end > w_begin ? X.row_at(w_begin) : 0u;
 #pragma unroll 1
   for (int p = w_begin; p < w_end; ++p) {
-    issue(p + kQ - 1, wr);
-    wr = wr + 1 == kQ ? 0 : wr + 1;
-    cp_async_wait<kQ - 1>();                  // entry p (this lane's chunks) has landed
-    const uint8_t* st = X.ring() + rd * kRingSlot;
-    rd = rd + 1 == kQ ? 0 : rd + 1;
+    issue(p + QD - 1, wr);
+    wr = wr + 1 == QD ? 0 : wr + 1;
+    cp_async_wait<QD - 1>();                  // entry p (this lane's chunks) has landed
+    const uint8_t* st = X.ring() + rd * slotB;
+    rd = rd + 1 == QD ? 0 : rd + 1;
 #pragma unroll
     for (int t = 0; t < CPL; ++t) {
       const int c = lane + 32 * t;
@@ -839,9 +842,9 @@ __device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_
   for (int c0 = 0, cb = 0; c0 < P.nch; c0 += kBlkChunks, ++cb) {
     const int ncb = min(kBlkChunks, P.nch - c0);
     switch ((ncb + 31) / 32) {
-      case 1: centroid_block<T, 1>(P, X, cb, c0, ncb); break;
-      case 2: centroid_block<T, 2>(P, X, cb, c0, ncb); break;
-      case 3: centroid_block<T, 3>(P, X, cb, c0, ncb); break;
+      case 1: centroid_block<T, 1, 16>(P, X, cb, c0, ncb); break;
+      case 2: centroid_block<T, 2, 16>(P, X, cb, c0, ncb); break;
+      case 3: centroid_block<T, 3, 13>(P, X, cb, c0, ncb); break;
       default: centroid_block<T, 4>(P, X, cb, c0, ncb); break;
     }
   }
@@ -1024,16 +1027,16 @@ __global__ void __launch_bounds__(kThreads, 1) grad_centroid_kernel(Params P) {
     const int cpl = (ncb + 31) / 32;
     if (P.is_bf16) {
       switch (cpl) {
-        case 1: centroid_block<__nv_bfloat16, 1>(P, X, cb, c0, ncb); break;
-        case 2: centroid_block<__nv_bfloat16, 2>(P, X, cb, c0, ncb); break;
-        case 3: centroid_block<__nv_bfloat16, 3>(P, X, cb, c0, ncb); break;
+        case 1: centroid_block<__nv_bfloat16, 1, 16>(P, X, cb, c0, ncb); break;
+        case 2: centroid_block<__nv_bfloat16, 2, 16>(P, X, cb, c0, ncb); break;
+        case 3: centroid_block<__nv_bfloat16, 3, 13>(P, X, cb, c0, ncb); break;
         default: centroid_block<__nv_bfloat16, 4>(P, X, cb, c0, ncb); break;
       }
     } else {
       switch (cpl) {
-        case 1: centroid_block<float, 1>(P, X, cb, c0, ncb); break;
-        case 2: centroid_block<float, 2>(P, X, cb, c0, ncb); break;
-        case 3: centroid_block<float, 3>(P, X, cb, c0, ncb); break;
+        case 1: centroid_block<float, 1, 16>(P, X, cb, c0, ncb); break;
+        case 2: centroid_block<float, 2, 16>(P, X, cb, c0, ncb); break;
+        case 3: centroid_block<float, 3, 13>(P, X, cb, c0, ncb); break;
         default: centroid_block<float, 4>(P, X, cb, c0, ncb); break;
       }
     }
@@ -1051,7 +1054,7 @@ int centroid_max_range(int nk) {
 }
 // K3 shared memory: per-warp rings, warp partials, the range's index arrays.
 int centroid_smem(int max_range) {   // + the grad mode's per-entry weights
-  return kWarps * kQ * kRingSlot + kWarps * kWpartFloats * 4 + 4 * (3 * max_range + 2);
+  return kWarps * kRingWarp + kWarps * kWpartFloats * 4 + 4 * (3 * max_range + 2);
 }
 
 int g_diag = 0;                              // lshmoe_set_diagnostics

@@ -73,83 +73,88 @@ __global__ void __launch_bounds__(256) unpermute_kernel(const T* __restrict__ re
   }
 }
 
-// ---- NEXT-1 grad_restore (reading R27): one warp per token row t (grid-stride), one 16-byte chunk
-// per lane per column block; the row's bucket ids, bucket sizes n_b (from the forward's row_start)
-// and gate weights are loaded once per row by lanes 0..k-1 and broadcast with shuffles; slots are
-// taken in groups of kSG so the per-slot dot products stay in registers:
-//   dX_t  = sum_s [ g_ts dY_t + (H_b - G_b) / n_b ]
-//   dg_ts = dY_t . (o_b + x_t - c~_b)          (lane partials over the row, then a warp reduction)
-constexpr int kSG = 4;
+// ---- NEXT-1 grad_restore (reading R27), two kernels:
+//   grad_x_kernel     one thread per 16-byte chunk of dX (flat, like restore_kernel):
+//                     dX_t = sum_s [ g_ts dY_t + (H_b - G_b) / n_b ],  n_b from the forward's row_start
+//   grad_gate_kernel  (only when dgate is requested) one warp per token row: dg_ts = dY_t . (o_b + x_t - c~_b),
+//                     lane partials over the row's chunks (all loads of a 32-chunk block issued
+//                     first), then a warp reduction — a fixed order, so the result is deterministic.
+template <typename T>
+__global__ void __launch_bounds__(256) grad_x_kernel(const T* __restrict__ dy, const T* __restrict__ G,
+                                                     const T* __restrict__ H, int64_t n, int d,
+                                                     const int32_t* __restrict__ bucket,
+                                                     const int32_t* __restrict__ row_start, int k,
+                                                     const float* __restrict__ g, T* __restrict__ dx) {
+  constexpr int VN = Vec<T>::N;
+  const int cpr = d / VN;
+  const int64_t total = n * cpr;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / cpr;
+    const int ch = static_cast<int>(i - t * cpr);
+    float dyv[VN], acc[VN];
+    Vec<T>::load(dy + t * d + ch * VN, dyv);
+    float gsum = 0.0f;
+#pragma unroll
+    for (int v = 0; v < VN; ++v) acc[v] = 0.0f;
+    for (int s = 0; s < k; ++s) {
+      const int64_t b = __ldg(bucket + t * k + s);
+      const float inv_n = 1.0f / static_cast<float>(__ldg(row_start + b + 1) - __ldg(row_start + b));
+      gsum += g ? __ldg(g + t * k + s) : 1.0f;
+      float gv[VN], hv[VN];
+      Vec<T>::load(G + b * d + ch * VN, gv);
+      Vec<T>::load(H + b * d + ch * VN, hv);
+#pragma unroll
+      for (int v = 0; v < VN; ++v) acc[v] += (hv[v] - gv[v]) * inv_n;
+    }
+#pragma unroll
+    for (int v = 0; v < VN; ++v) acc[v] += gsum * dyv[v];     // sum_s g_ts dY_t
+    Vec<T>::store(dx + t * d + ch * VN, acc);
+  }
+}
+
+constexpr int kGC = 4;   // 16-byte chunks per lane per column block (grad_gate_kernel)
 
 template <typename T>
-__global__ void __launch_bounds__(256) grad_restore_kernel(const T* __restrict__ dy, const T* __restrict__ x,
-                                                           const T* __restrict__ ct, const T* __restrict__ ret,
-                                                           const T* __restrict__ G, const T* __restrict__ H,
-                                                           int64_t n, int d, const int32_t* __restrict__ bucket,
-                                                           const int32_t* __restrict__ row_start, int k,
-                                                           const float* __restrict__ g, T* __restrict__ dx,
-                                                           float* __restrict__ dg) {
+__global__ void __launch_bounds__(256) grad_gate_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                        const T* __restrict__ ct, const T* __restrict__ ret,
+                                                        int64_t n, int d, const int32_t* __restrict__ bucket, int k,
+                                                        float* __restrict__ dg) {
   constexpr int VN = Vec<T>::N;
   const int cpr = d / VN;
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
   for (int64_t t = blockIdx.x * int64_t(blockDim.x / 32) + threadIdx.x / 32; t < n; t += warps) {
-    for (int s0 = 0; s0 < k; s0 += kSG) {
-      const int ns = min(kSG, k - s0);
-      int64_t bl = 0;
-      float invl = 0.0f, gl = 0.0f;
-      if (lane < ns) {
-        bl = __ldg(bucket + t * k + s0 + lane);
-        gl = g ? __ldg(g + t * k + s0 + lane) : 1.0f;
-      }
-      if (lane < ns) invl = 1.0f / static_cast<float>(__ldg(row_start + bl + 1) - __ldg(row_start + bl));
-      float dot[kSG], invs[kSG], gws[kSG];
-      int64_t bs[kSG];
+    for (int s = 0; s < k; ++s) {
+      const int64_t b = __ldg(bucket + t * k + s);
+      float dot = 0.0f;
+      for (int c0 = 0; c0 < cpr; c0 += 32 * kGC) {
+        uint4 dr[kGC], xr[kGC], cr[kGC], rr[kGC];
 #pragma unroll
-      for (int j = 0; j < kSG; ++j) {            // broadcast before the chunk loop (all lanes active)
-        dot[j] = 0.0f;
-        bs[j] = __shfl_sync(0xFFFFFFFFu, bl, j);
-        invs[j] = __shfl_sync(0xFFFFFFFFu, invl, j);
-        gws[j] = __shfl_sync(0xFFFFFFFFu, gl, j);
-      }
-      for (int ch = lane; ch < cpr; ch += 32) {
-        float dyv[VN], xv[VN], acc[VN];
-        Vec<T>::load(dy + t * d + ch * VN, dyv);
-        Vec<T>::load(x + t * d + ch * VN, xv);
-        if (s0 == 0) {
-#pragma unroll
-          for (int v = 0; v < VN; ++v) acc[v] = 0.0f;
-        } else {
-          Vec<T>::load(dx + t * d + ch * VN, acc);            // slots of earlier groups (k > kSG)
-        }
-#pragma unroll
-        for (int j = 0; j < kSG; ++j) {
-          if (j >= ns) break;
-          const int64_t b = bs[j];
-          const float inv_n = invs[j];
-          const float gw = gws[j];
-          float cv[VN], rv[VN], gv[VN], hv[VN];
-          Vec<T>::load(ct + b * d + ch * VN, cv);
-          Vec<T>::load(ret + b * d + ch * VN, rv);
-          Vec<T>::load(G + b * d + ch * VN, gv);
-          Vec<T>::load(H + b * d + ch * VN, hv);
-#pragma unroll
-          for (int v = 0; v < VN; ++v) {
-            acc[v] += gw * dyv[v] + (hv[v] - gv[v]) * inv_n;
-            dot[j] = fmaf(dyv[v], rv[v] + (xv[v] - cv[v]), dot[j]);
+        for (int j = 0; j < kGC; ++j) {
+          const int ch = c0 + j * 32 + lane;
+          if (ch < cpr) {
+            dr[j] = __ldg(reinterpret_cast<const uint4*>(dy + t * d) + ch);
+            xr[j] = __ldg(reinterpret_cast<const uint4*>(x + t * d) + ch);
+            cr[j] = __ldg(reinterpret_cast<const uint4*>(ct + b * d) + ch);
+            rr[j] = __ldg(reinterpret_cast<const uint4*>(ret + b * d) + ch);
           }
         }
-        Vec<T>::store(dx + t * d + ch * VN, acc);
-      }
-      if (dg) {
 #pragma unroll
-        for (int j = 0; j < kSG; ++j) {
-          float v = dot[j];
+        for (int j = 0; j < kGC; ++j) {
+          const int ch = c0 + j * 32 + lane;
+          if (ch >= cpr) continue;
+          float dv[VN], xv[VN], cv[VN], rv[VN];
+          Vec<T>::load(&dr[j], dv);
+          Vec<T>::load(&xr[j], xv);
+          Vec<T>::load(&cr[j], cv);
+          Vec<T>::load(&rr[j], rv);
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, off);
-          if (lane == 0 && j < ns) dg[t * k + s0 + j] = v;
+          for (int v = 0; v < VN; ++v) dot = fmaf(dv[v], rv[v] + (xv[v] - cv[v]), dot);
         }
       }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xFFFFFFFFu, dot, off);
+      if (lane == 0) dg[t * k + s] = dot;
     }
   }
 }
@@ -204,20 +209,27 @@ int launch_grad_restore(const void* dy, const void* x, const void* ct, const voi
                         lshmoe_dtype dtype, int64_t n, int d, const int32_t* bucket, const int32_t* row_start, int k,
                         const float* g, void* dx, float* dg, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int grid = static_cast<int>(std::max<int64_t>(1, (n + 7) / 8));   // one warp per row
+  const int64_t items = n * (d / (dtype == LSHMOE_BF16 ? 8 : 4));
+  const int rgrid = static_cast<int>(std::max<int64_t>(1, (n + 7) / 8));   // one warp per row
   if (dtype == LSHMOE_BF16) {
     using T = __nv_bfloat16;
-    grad_restore_kernel<T><<<grid, 256, 0, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x),
-                                                 static_cast<const T*>(ct), static_cast<const T*>(ret),
-                                                 static_cast<const T*>(G), static_cast<const T*>(H), n, d, bucket,
-                                                 row_start, k, g, static_cast<T*>(dx), dg);
+    grad_x_kernel<T><<<grid_for(items), 256, 0, st>>>(static_cast<const T*>(dy), static_cast<const T*>(G),
+                                                       static_cast<const T*>(H), n, d, bucket, row_start, k, g,
+                                                       static_cast<T*>(dx));
+    if (dg)
+      grad_gate_kernel<T><<<rgrid, 256, 0, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x),
+                                                 static_cast<const T*>(ct), static_cast<const T*>(ret), n, d, bucket,
+                                                 k, dg);
   } else {
-    grad_restore_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(x),
-                                                     static_cast<const float*>(ct), static_cast<const float*>(ret),
-                                                     static_cast<const float*>(G), static_cast<const float*>(H), n, d,
-                                                     bucket, row_start, k, g, static_cast<float*>(dx), dg);
+    grad_x_kernel<float><<<grid_for(items), 256, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(G),
+                                                           static_cast<const float*>(H), n, d, bucket, row_start, k,
+                                                           g, static_cast<float*>(dx));
+    if (dg)
+      grad_gate_kernel<float><<<rgrid, 256, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(x),
+                                                     static_cast<const float*>(ct), static_cast<const float*>(ret), n,
+                                                     d, bucket, k, dg);
   }
-  count_launches(1);
+  count_launches(dg ? 2 : 1);
   return cudaGetLastError();
 }
 
