@@ -215,7 +215,7 @@ _DIAG_WORD = 64 + 2048 + 512                      # compress.cu kDiag (int32 wor
 _DIAG_CTAS = 128                                  # CTAs recorded per kernel
 COMPRESS_DIAG_STAMPS = {"tiles": ["start", "end"],
                         "bucket": ["start", "gathered", "rows_first", "rows_all", "ranked", "end", "sized", "tilescan"],
-                        "centroid": ["start", "indexed", "reduced", "end"]}
+                        "centroid": ["start", "indexed", "reduced", "end", "w0_first_row", "w0_rows_done"]}
 
 
 def set_diagnostics(on: bool) -> None:

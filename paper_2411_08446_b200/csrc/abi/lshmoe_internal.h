@@ -35,7 +35,9 @@ struct CompressWs {            // carved from the caller's workspace by compress
   int32_t* rowl;               // [nk] local row of each perm position (permute mode: perm)
   int32_t* rsl;                // [nk] perm position of each row's first member, at grp_off[e] + row
   int32_t* gofs;               // [E] perm offset of each expert group
-  int32_t* big;                // [5][nk] phase-A arrays of groups too large for shared memory
+  int32_t* big;                // [5][8 nk] K2 slice arrays of groups too large for shared memory
+  int32_t* rtot;               // [8 nk] K2 per-(cluster rank, row) totals
+  int32_t* fcnt;               // [8 (E + 1)] K2 per-CTA first-appearance counts
   float* partial;              // [kMaxGrid][2][d] centroid partial sums of rows cut by CTA ranges
   size_t bytes;
 };

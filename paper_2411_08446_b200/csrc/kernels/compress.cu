@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "../abi/lshmoe_internal.h"
 #include "common.cuh"
@@ -44,6 +45,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kBThreads = 1024;          // K2 threads per CTA
 constexpr int kBWarps = kBThreads / 32;
 constexpr int kMaxE = 255;
+constexpr int kMaxCS = 8;                // K2 CTAs per expert (portable cluster size)
 constexpr int kMaxGrid = 512;            // K3 CTAs (one per SM) <= this
 // Workspace header (int32 words), memset to 0xFF (= -1) before every compress:
 // [2..16) stamps, [64, 64 + 2*1024) K3 per-CTA stamps, [kArrive, +kMaxGrid) arrival counters of
@@ -107,7 +109,10 @@ struct Params {
   int32_t* rowl;
   int32_t* rsl;
   int32_t* gofs;
-  int32_t* big;
+  int32_t* big;                    // [5][CS * nk] K2 slice arrays of groups too large for shared memory
+  int32_t* rtot;                   // [CS * nk] K2 per-(cluster rank, row) totals
+  int32_t* fcnt;                   // [E * CS] K2 per-CTA first-appearance counts
+  int cs;                          // K2 cluster size (CTAs per expert)
   float* partial;                  // [G][2][d] partial sums of rows cut by K3's CTA ranges
   int max_range;                   // K3: max perm entries per CTA range
   int dyn_smem;                    // K2: dynamic shared memory bytes
@@ -253,16 +258,26 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(Params P) {
   dstamp(P, 0, 1);
 }
 
-// ---- K2: per-expert ordered bucketing ------------------------------------------------------
+// ---- K2: per-expert ordered bucketing, one thread-block cluster of CS CTAs per expert ----------
+// CTA rank r of expert e's cluster owns the member positions [r*n_e/CS, (r+1)*n_e/CS) of the
+// expert's ordered copy list.  The two ordered steps that span the whole group (numbering the
+// first appearances; ranking copies within their rows) take a per-CTA partial in shared memory,
+// publish the CTA's totals to the workspace, and combine them after a cluster barrier
+// (barrier.cluster release/acquire orders the global writes of the cluster's CTAs).
 extern __shared__ __align__(1024) uint8_t g_dsmem[];
 
-// Ordered gather of expert e's copies (and their slots) from the tiles' runs.
-__device__ void gather_group(const Params& P, int e, int32_t* mem, int32_t* aux, int* s_tb, int* s_ta,
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Ordered gather of positions [s0, s1) of expert e's copy list (and their slots) from the tiles'
+// runs into mem[i - s0], aux[i - s0].
+__device__ void gather_group(const Params& P, int e, int s0, int s1, int32_t* mem, int32_t* aux, int* s_tb, int* s_ta,
                              int* s_scan) {
   const int tid = threadIdx.x;
   const int E1 = P.E + 1;
   int base = 0;
-  for (int t0 = 0; t0 < P.ntiles; t0 += kBThreads) {
+  for (int t0 = 0; t0 < P.ntiles && base < s1; t0 += kBThreads) {
     const int t = t0 + tid;
     int a = 0, cnt = 0;
     if (t < P.ntiles) {
@@ -276,15 +291,17 @@ __device__ void gather_group(const Params& P, int e, int32_t* mem, int32_t* aux,
     __syncthreads();
     const int nt = min(kBThreads, P.ntiles - t0);
     dstamp(P, 1, 7);
-    // flattened (tile, entry) space: thread owns entries i = tid + 1024 j, 8 gathers in flight;
-    // tile of entry i = the last tile with s_tb <= i (branchless search, all j interleaved)
+    // this chunk's positions [base, base + tot) intersected with [s0, s1); thread owns entries
+    // i = lo_i + tid + 1024 j; tile of entry i = the last tile with s_tb <= i - base (branchless
+    // search, the 8 entries interleaved)
+    const int lo_i = max(s0, base) - base, hi_i = min(s1, base + tot) - base;
     int top = 1;
     while (top * 2 < nt) top *= 2;
-    for (int i0 = 0; i0 < tot; i0 += 8 * kBThreads) {
+    for (int i0 = lo_i; i0 < hi_i; i0 += 8 * kBThreads) {
       int lo[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) lo[j] = 0;
-      const int nj = min(8, (tot - i0 - tid + kBThreads - 1) / kBThreads);   // entries of this thread
+      const int nj = min(8, (hi_i - i0 - tid + kBThreads - 1) / kBThreads);   // entries of this thread
       for (int step = top; step >= 1; step >>= 1) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -306,8 +323,8 @@ __device__ void gather_group(const Params& P, int e, int32_t* mem, int32_t* aux,
       for (int j = 0; j < 8; ++j) {
         const int i = i0 + j * kBThreads + tid;
         if (j < nj) {
-          mem[base + i] = cc[j];
-          aux[base + i] = ss[j];
+          mem[base + i - s0] = cc[j];
+          aux[base + i - s0] = ss[j];
         }
       }
     }
@@ -322,7 +339,8 @@ __global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
   __shared__ int s_scan[kBWarps + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  const int e = blockIdx.x;
+  const int CS = P.cs;
+  const int e = blockIdx.x / CS, r = blockIdx.x - e * CS;   // cluster (CS, 1, 1): rank = blockIdx.x % CS
   const int E1 = P.E + 1;
   pdl_wait();                               // K1's tiles and table are complete and visible
   dstamp(P, 1, 0);
@@ -339,74 +357,89 @@ __global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
     block_excl_scan<kBWarps>(a, s_scan, &goff);   // copies of experts < e = the group's perm offset
   }
   dstamp(P, 1, 6);
-  int32_t *mem, *aux, *row, *rs, *wcnt;
-  const bool in_smem = static_cast<int64_t>(20) * n_e <= P.dyn_smem;
+  const int s0 = static_cast<int>(static_cast<int64_t>(r) * n_e / CS);
+  const int s1 = static_cast<int>(static_cast<int64_t>(r + 1) * n_e / CS);
+  const int ns = s1 - s0;
+  // slice arrays: shared memory when the slice and the expert's row arrays fit, else workspace
+  // (per cluster rank: [CS][nk] regions at CS * goff + r * n_e)
+  int32_t *mem, *aux, *row;
+  const bool in_smem = static_cast<int64_t>(12) * ns + static_cast<int64_t>(8) * n_e <= P.dyn_smem;
+  const int64_t wbase = static_cast<int64_t>(CS) * goff + static_cast<int64_t>(r) * n_e;
   if (in_smem) {
-    int32_t* s = reinterpret_cast<int32_t*>(g_dsmem);
-    mem = s; aux = s + n_e; row = s + 2 * n_e; rs = s + 3 * n_e; wcnt = s + 4 * n_e;
+    int32_t* sm = reinterpret_cast<int32_t*>(g_dsmem);
+    mem = sm; aux = sm + ns; row = sm + 2 * ns;
   } else {
-    mem = P.big + goff; aux = P.big + P.nk + goff; row = P.big + 2 * P.nk + goff;
-    rs = P.big + 3 * P.nk + goff; wcnt = P.big + 4 * P.nk + goff;
+    mem = P.big + 0 * static_cast<int64_t>(CS) * P.nk + wbase;
+    aux = P.big + 1 * static_cast<int64_t>(CS) * P.nk + wbase;
+    row = P.big + 2 * static_cast<int64_t>(CS) * P.nk + wbase;
   }
-  gather_group(P, e, mem, aux, s_tb, s_ta, s_scan);
+  gather_group(P, e, s0, s1, mem, aux, s_tb, s_ta, s_scan);
   dstamp(P, 1, 1);
-  if (tid == 0) P.gofs[e] = goff;
+  if (tid == 0 && r == 0) P.gofs[e] = goff;
   if (P.permute) {                        // baseline: slot = group offset + rank in the group
-    for (int i = tid; i < n_e; i += kBThreads) {
+    for (int i = tid; i < ns; i += kBThreads) {
       const int c = mem[i];
-      P.bucket[c] = goff + i;
-      P.rowl[goff + i] = c;
+      P.bucket[c] = goff + s0 + i;
+      P.rowl[goff + s0 + i] = c;
     }
-    if (tid == 0) P.expert_rows[e] = n_e;
+    if (tid == 0 && r == 0) P.expert_rows[e] = n_e;
     return;
   }
   // first copy of every member's bucket (the table is final)
-  for (int i0 = 0; i0 < n_e; i0 += 8 * kBThreads) {
+  for (int i0 = 0; i0 < ns; i0 += 8 * kBThreads) {
     int v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int i = i0 + j * kBThreads + tid;
-      if (i < n_e) v[j] = ldcg(P.table + aux[i]);
+      if (i < ns) v[j] = ldcg(P.table + aux[i]);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int i = i0 + j * kBThreads + tid;
-      if (i < n_e) aux[i] = v[j];
+      if (i < ns) aux[i] = v[j];
     }
   }
   __syncthreads();
-  // local row ids of the first appearances, in member order: warp w owns a contiguous span,
-  // counts its firsts by ballots, a block scan gives each warp its base, a second pass numbers.
-  const int span = ((n_e + kBWarps - 1) / kBWarps + 31) & ~31;
-  const int w0 = min(n_e, warp * span), w1 = min(n_e, w0 + span);
+  // local row ids of the first appearances, in member order: warps own contiguous spans of the
+  // slice and count by ballots; the CTA's count is published, the cluster's prefix is its base
+  const int span = ((ns + kBWarps - 1) / kBWarps + 31) & ~31;
+  const int w0 = min(ns, warp * span), w1 = min(ns, w0 + span);
   int nf = 0;
   for (int b = w0; b < w1; b += 32) {
     const int i = b + lane;
     nf += __popc(__ballot_sync(0xFFFFFFFFu, i < w1 && aux[i] == mem[i]));
   }
-  int m_e;
-  int lr = block_excl_scan<kBWarps>(lane == 0 ? nf : 0, s_scan, &m_e);
-  lr = __shfl_sync(0xFFFFFFFFu, lr, 0);
+  int cta_f;
+  int lr = block_excl_scan<kBWarps>(lane == 0 ? nf : 0, s_scan, &cta_f);
+  if (tid == 0) P.fcnt[blockIdx.x] = cta_f;
+  cluster_barrier();
+  int m_e = 0, fbase = 0;
+  for (int q = 0; q < CS; ++q) {
+    const int v = ldcg(P.fcnt + e * CS + q);
+    if (q < r) fbase += v;
+    m_e += v;
+  }
+  lr = __shfl_sync(0xFFFFFFFFu, lr, 0) + fbase;
   for (int b = w0; b < w1; b += 32) {
     const int i = b + lane;
     const bool f = i < w1 && aux[i] == mem[i];
     const unsigned fb = __ballot_sync(0xFFFFFFFFu, f);
     if (f) {
-      const int r = lr + __popc(fb & lt);
-      row[i] = r;
-      P.rowid[mem[i]] = r;
+      const int rr = lr + __popc(fb & lt);
+      row[i] = rr;
+      P.rowid[mem[i]] = rr;
     }
     lr += __popc(fb);
   }
-  __syncthreads();
+  cluster_barrier();                       // every CTA's first appearances have their row ids
   dstamp(P, 1, 2);
-  for (int i0 = 0; i0 < n_e; i0 += 8 * kBThreads) {   // the other members look their row up
+  for (int i0 = 0; i0 < ns; i0 += 8 * kBThreads) {   // the other members look their row up
     int v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int i = i0 + j * kBThreads + tid;
       v[j] = -1;
-      if (i < n_e && aux[i] != mem[i]) v[j] = ldcg(P.rowid + aux[i]);
+      if (i < ns && aux[i] != mem[i]) v[j] = ldcg(P.rowid + aux[i]);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -414,70 +447,91 @@ __global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
       if (v[j] >= 0) row[i] = v[j];
     }
   }
-  // rank inside rows: W warps own contiguous sub-ranges; per-(warp, row) counters
+  // rank inside rows over the slice: W warps own contiguous sub-ranges; per-(warp, row) counters;
+  // rs[m_e] holds the row sizes and then the row starts (every CTA of the cluster computes them)
+  int32_t *rs, *wcnt;
   int W;
   if (in_smem) {
-    W = static_cast<int>(min(static_cast<int64_t>(kBWarps), (P.dyn_smem - static_cast<int64_t>(16) * n_e) / (4 * max(m_e, 1))));
+    int32_t* sm = reinterpret_cast<int32_t*>(g_dsmem);
+    rs = sm + 3 * ns;
+    wcnt = rs + m_e;
+    W = static_cast<int>(min(static_cast<int64_t>(kBWarps),
+                             (P.dyn_smem - static_cast<int64_t>(12) * ns - static_cast<int64_t>(4) * m_e) /
+                                 (4 * max(m_e, 1))));
+    if (W < 1) W = 1;   // (12 ns + 8 n_e <= dyn_smem guarantees room for W = 1)
   } else {
-    W = min(kBWarps, P.dyn_smem / (4 * max(m_e, 1)));
-    if (W >= 1) wcnt = reinterpret_cast<int32_t*>(g_dsmem);
-    else W = 1;                            // counters stay in the workspace
+    rs = P.big + 3 * static_cast<int64_t>(CS) * P.nk + wbase;
+    wcnt = P.big + 4 * static_cast<int64_t>(CS) * P.nk + wbase;
+    W = 1;
   }
-  const int sub = (n_e + W - 1) / W;
+  const int sub = (ns + W - 1) / W;
   for (int i = tid; i < W * m_e; i += kBThreads) wcnt[i] = 0;
   __syncthreads();
   dstamp(P, 1, 3);
   if (warp < W) {
     int32_t* wc = wcnt + warp * m_e;
-    const int b0 = warp * sub, b1 = min(n_e, b0 + sub);
+    const int b0 = warp * sub, b1 = min(ns, b0 + sub);
     for (int base = b0; base < b1; base += 32) {
       const int i = base + lane;
       const bool ok = i < b1;
-      const int r = ok ? row[i] : -1;
-      const unsigned peers = __match_any_sync(0xFFFFFFFFu, r);
+      const int rr = ok ? row[i] : -1;
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, rr);
       const int leader = __ffs(peers) - 1;
-      const int b = ok ? wc[r] : 0;
+      const int b = ok ? wc[rr] : 0;
       __syncwarp();
-      if (ok && lane == leader) wc[r] = b + __popc(peers);
+      if (ok && lane == leader) wc[rr] = b + __popc(peers);
       __syncwarp();
       if (ok) aux[i] = b + __popc(peers & lt);
     }
   }
   __syncthreads();
   dstamp(P, 1, 4);
-  for (int r = tid; r < m_e; r += kBThreads) {   // warp prefixes per row; row sizes
+  int32_t* tot = P.rtot + static_cast<int64_t>(CS) * goff;   // [CS][m_e] this cluster's per-CTA row totals
+  for (int q = tid; q < m_e; q += kBThreads) {   // warp prefixes per row; this CTA's row totals
     int run = 0;
     for (int w = 0; w < W; ++w) {
-      const int v = wcnt[w * m_e + r];
-      wcnt[w * m_e + r] = run;
+      const int v = wcnt[w * m_e + q];
+      wcnt[w * m_e + q] = run;
       run += v;
     }
-    rs[r] = run;
+    tot[static_cast<int64_t>(r) * m_e + q] = run;
+  }
+  cluster_barrier();                       // all CTAs' row totals are published
+  for (int q = tid; q < m_e; q += kBThreads) {   // rows: size over the cluster; earlier CTAs' share
+    int size = 0, before = 0;
+    for (int c = 0; c < CS; ++c) {
+      const int v = ldcg(tot + static_cast<int64_t>(c) * m_e + q);
+      if (c < r) before += v;
+      size += v;
+    }
+    rs[q] = size;
+    for (int w = 0; w < W; ++w) wcnt[w * m_e + q] += before;
   }
   __syncthreads();
   {                                              // row starts: ordered scan of the row sizes
     const int rper = (m_e + kBThreads - 1) / kBThreads;
     const int r0 = min(m_e, tid * rper), r1 = min(m_e, r0 + rper);
     int sz = 0;
-    for (int r = r0; r < r1; ++r) sz += rs[r];
-    int tot;
-    int run = block_excl_scan<kBWarps>(sz, s_scan, &tot);
-    for (int r = r0; r < r1; ++r) {
-      const int v = rs[r];
-      rs[r] = run;
-      P.rsl[goff + r] = goff + run;
+    for (int q = r0; q < r1; ++q) sz += rs[q];
+    int total;
+    int run = block_excl_scan<kBWarps>(sz, s_scan, &total);
+    for (int q = r0; q < r1; ++q) {
+      const int v = rs[q];
+      rs[q] = run;
+      if (r == 0) P.rsl[goff + q] = goff + run;
       run += v;
     }
   }
   __syncthreads();
-  for (int i = tid; i < n_e; i += kBThreads) {
-    const int r = row[i];
-    const int pos = goff + rs[r] + wcnt[(i / sub) * m_e + r] + aux[i];
+  for (int i = tid; i < ns; i += kBThreads) {
+    const int q = row[i];
+    const int pos = goff + rs[q] + wcnt[(i / sub) * m_e + q] + aux[i];
     P.perm[pos] = mem[i];
-    P.rowl[pos] = r;
+    P.rowl[pos] = q;
   }
-  if (tid == 0) P.expert_rows[e] = m_e;
+  if (tid == 0 && r == 0) P.expert_rows[e] = m_e;
   dstamp(P, 1, 5);
+  cluster_barrier();                       // no CTA leaves while a peer may still read its totals
 }
 
 // ---- centroid phase ------------------------------------------------------------------------
@@ -671,6 +725,7 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
     issue(p + QD - 1, wr);
     wr = wr + 1 == QD ? 0 : wr + 1;
     cp_async_wait<QD - 1>();                  // entry p (this lane's chunks) has landed
+    if (p == w_begin && cb == 0 && X.w == 0) dstamp(P, 2, 4);   // diagnostics: first row landed
     const uint8_t* st = X.ring() + rd * slotB;
     rd = rd + 1 == QD ? 0 : rd + 1;
 #pragma unroll
@@ -711,6 +766,7 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
     row = next;
   }
   cp_async_wait<0>();                         // the ring is free: it may hold the slot-1 partial
+  if (cb == 0 && X.w == 0) dstamp(P, 2, 5);   // diagnostics: warp 0's rows reduced
   const int nrows = w_end - w_begin;
   const uint32_t r_last = X.row_at(w_end - 1);
   const bool cut_end = nrows > 0 && X.row_at(w_end) == r_last;
@@ -1057,21 +1113,37 @@ int centroid_smem(int max_range) {   // + the grad mode's per-entry weights
   return kWarps * kRingWarp + kWarps * kWpartFloats * 4 + 4 * (3 * max_range + 2);
 }
 
+// K2 CTAs per expert: the largest power of two CS <= kMaxCS for which all E clusters of CS CTAs
+// are co-resident (cudaOccupancyMaxActiveClusters: a cluster needs CS SMs of one GPC), so the
+// experts run in one wave.  LSHMOE_BUCKET_CS overrides, for experiments.
+int bucket_cluster_size(int E);
+
 int g_diag = 0;                              // lshmoe_set_diagnostics
 bool diag_enabled() { return g_diag != 0; }
 
 template <typename K>
-int launch_pdl(K kernel, int grid, int block, int smem, cudaStream_t st, const Params& p, bool pdl) {
+int launch_pdl(K kernel, int grid, int block, int smem, cudaStream_t st, const Params& p, bool pdl, int cluster = 1) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   const int err = cudaLaunchKernelEx(&cfg, kernel, p);
   count_launches(1);
   return err;
@@ -1092,10 +1164,44 @@ int launch_chain(const Params& P, cudaStream_t st) {
   p.max_range = max_range;
   p.dyn_smem = kBucketSmem;
   p.diag = diag_enabled() ? 1 : 0;
+  p.cs = bucket_cluster_size(P.E);
   int err = launch_pdl(tile_kernel, P.ntiles, kThreads, 0, st, p, false);
-  if (!err) err = launch_pdl(bucket_kernel, P.E, kBThreads, kBucketSmem, st, p, true);
+  if (!err) err = launch_pdl(bucket_kernel, P.E * p.cs, kBThreads, kBucketSmem, st, p, true, p.cs);
   if (!err) err = launch_pdl(centroid_kernel, centroid_grid(), kThreads, P.permute ? 0 : csmem, st, p, true);
   return err;
+}
+
+int bucket_cluster_size(int E) {
+  static int cached_E = -1, cached_cs = 1;
+  if (E == cached_E) return cached_cs;
+  int cs = 1;
+  for (int c = 2; c <= kMaxCS; c *= 2) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(E * c);
+    cfg.blockDim = dim3(kBThreads);
+    cfg.dynamicSmemBytes = kBucketSmem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, bucket_kernel, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      break;
+    }
+    if (n >= E) cs = c;
+    else break;
+  }
+  if (const char* env = getenv("LSHMOE_BUCKET_CS")) {
+    const int v = atoi(env);
+    if (v == 1 || v == 2 || v == 4 || v == 8) cs = v;
+  }
+  cached_E = E;
+  cached_cs = cs;
+  return cs;
 }
 
 }  // namespace
@@ -1131,7 +1237,9 @@ size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, Com
   const size_t o_rowl = take(sizeof(int32_t) * nk);
   const size_t o_rsl = take(sizeof(int32_t) * nk);
   const size_t o_gofs = take(sizeof(int32_t) * (E + 1));
-  const size_t o_big = take(sizeof(int32_t) * 5 * nk);
+  const size_t o_big = take(sizeof(int32_t) * 5 * kMaxCS * nk);
+  const size_t o_rtot = take(sizeof(int32_t) * kMaxCS * nk);
+  const size_t o_fcnt = take(sizeof(int32_t) * kMaxCS * (E + 1));
   const size_t o_part = take(sizeof(float) * 2 * kMaxGrid * d);
   if (ws) {
     uint8_t* b = static_cast<uint8_t*>(base);
@@ -1146,6 +1254,8 @@ size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, Com
     ws->rsl = reinterpret_cast<int32_t*>(b + o_rsl);
     ws->gofs = reinterpret_cast<int32_t*>(b + o_gofs);
     ws->big = reinterpret_cast<int32_t*>(b + o_big);
+    ws->rtot = reinterpret_cast<int32_t*>(b + o_rtot);
+    ws->fcnt = reinterpret_cast<int32_t*>(b + o_fcnt);
     ws->partial = reinterpret_cast<float*>(b + o_part);
     ws->bytes = off;
   }
@@ -1176,6 +1286,8 @@ static Params base_params(const void* x, lshmoe_dtype dtype, int64_t n, int d, c
   P.rsl = ws.rsl;
   P.gofs = ws.gofs;
   P.big = ws.big;
+  P.rtot = ws.rtot;
+  P.fcnt = ws.fcnt;
   P.partial = ws.partial;
   return P;
 }
