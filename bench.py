@@ -469,22 +469,32 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                "what": "permute -> all-to-all of every routed token -> expert FFN on n*k rows -> all-to-all -> unpermute",
                "speedup_of_lsh": bms / ms}
 
-    # ---- NEXT-1 backward of the LSH-specific steps (grad_compress, grad_restore), graph-timed ----
+    # ---- NEXT-1 backward (reading R27): grad_compress -> dispatch(G) -> expert backward (dX path)
+    # -> combine(H) -> grad_restore, graph-timed as one chain and per part, L2 flushed before each ----
     bwd = None
     if not args.no_backward and world == 1:
         gen = torch.Generator(device=dev).manual_seed(11)
         dY = torch.randn(X.shape, generator=gen, device=dev).to(X.dtype)
         Gb = torch.empty((nk, d), dtype=X.dtype, device=dev)
+        Hb = torch.empty((cap, d), dtype=X.dtype, device=dev)
+        dhid = torch.empty((cap, cfg.d_ffn), dtype=X.dtype, device=dev)
         dxb = torch.empty_like(X)
         gws = torch.empty(1 << 22, dtype=torch.uint8, device=dev)
+        W2T = W2.transpose(1, 2).contiguous()
+        W1T = W1.transpose(1, 2).contiguous()
         parts = {"grad_compress": lambda: L.grad_compress(dY, comp, out=Gb, workspace=gws),
-                 "grad_restore": lambda: L.grad_restore(dY, X, comp.centroids, ret, Gb, Gb, comp, dx=dxb)}
-        bwd = {}
-        for nm, fn in parts.items():
-            fn()
+                 "dispatch": lambda: L.dispatch(comm, Gb, comp.expert_rows, cfg.E, Gb, rr),
+                 "expert_backward": lambda: L.expert_ffn_backward(Gb, rr, W2T, W1T, hid, out=Hb, dhidden=dhid),
+                 "combine": lambda: L.combine(comm, Hb, comp.expert_rows, cfg.E, Hb),
+                 "grad_restore": lambda: L.grad_restore(dY, X, comp.centroids, ret, Gb, Hb, comp, dx=dxb)}
+
+        def graph_time(fns):
+            for fn in fns:
+                fn()
             gph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gph, stream=stream):
-                fn()
+                for fn in fns:
+                    fn()
             tt = []
             for _ in range(args.steps):
                 flush.zero_()
@@ -494,13 +504,18 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 b_.record(stream)
                 torch.cuda.synchronize()
                 tt.append(a_.elapsed_time(b_))
-            bwd[nm + "_us"] = statistics.median(tt) * 1e3
+            return statistics.median(tt) * 1e3
+
+        bwd = {nm + "_us": graph_time([fn]) for nm, fn in parts.items()}
+        bwd["chain_us"] = graph_time(list(parts.values()))
+        bwd["tokens_per_s"] = n / (bwd["chain_us"] / 1e6)
         sb = 2 if X.dtype == torch.bfloat16 else 4
         bwd["grad_compress_hbm_bytes"] = (nk + m) * d * sb
         bwd["grad_compress_gbs"] = bwd["grad_compress_hbm_bytes"] / bwd["grad_compress_us"] / 1e3
-        bwd["what"] = ("NEXT-1 (reading R27): G = per-bucket sums of dY (grad_compress) and dX = dY + (H - G)/n_b "
-                       "(grad_restore), each a CUDA-graph replay with L2 flushed; the expert's own backward and "
-                       "the two exchanges are not included (H = G stand-in)")
+        bwd["what"] = ("NEXT-1 (reading R27) dX path: G = per-bucket sums of dY -> exchange -> H = J_E(c~)^T G "
+                       "(expert backward, transposed weights, relu' from the forward's hidden) -> exchange -> "
+                       "dX = sum_s g dY + (H - G)/n_b; weight gradients not computed; each a CUDA-graph replay "
+                       "with L2 flushed")
 
     L.check_device_error()
     # ---- the dominant kernel alone (the hash launch), CUDA-graph replay on `stream`, L2 flushed

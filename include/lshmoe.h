@@ -219,6 +219,17 @@ lshmoe_status lshmoe_restore(const void* x, const void* centroids, const void* r
    bucket / perm / row_start are lshmoe_compress's outputs of the same forward.  Summation order of
    G is the forward's perm order (fp32 accumulation, one rounding to dtype; grad_out_f32 nullable
    keeps the fp32 sums).  Workspace: lshmoe_grad_compress_workspace(d) bytes, any contents. */
+/* The expert's backward for the dX path (H = J_E(c~)^T G for E(c) = W2 relu(W1 c + b1) + b2,
+   weight gradients not computed): dh = (G W2) * [h > 0], H = dh W1, as two grouped GEMMs over the
+   same recv_rows segments as lshmoe_expert_ffn.  W2T [E_local, d_ffn, d] = W2^T and W1T
+   [E_local, d, d_ffn] = W1^T per expert (the transposed copies a training framework keeps for its
+   backward; K-major for TMA); hidden = the forward's post-ReLU activations [capacity, d_ffn];
+   dhidden [capacity, d_ffn] scratch; grad_in (H) [capacity, d] out.  bf16: tcgen05, fp32
+   accumulation, dh rounded to bf16; f32: SIMT. */
+lshmoe_status lshmoe_expert_ffn_backward(const void* grad_out, lshmoe_dtype dtype, int d, int d_ffn,
+                                         const int32_t* recv_rows, int experts_local, int world,
+                                         const void* W2T, const void* W1T, const void* hidden, void* dhidden,
+                                         int64_t capacity, void* grad_in, lshmoe_stream stream);
 lshmoe_status lshmoe_grad_compress_workspace(int d, size_t* bytes /* [host] */);
 lshmoe_status lshmoe_grad_compress(const void* dy, lshmoe_dtype dtype, int64_t n, int d,
                                    const float* gate_weight /* nullable [n, k] */, const int32_t* bucket,

@@ -43,6 +43,8 @@ _SIGS = {
     "lshmoe_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _sz, _vp], _i32),
     "lshmoe_sp_rows": ([_i32, _i32], _i32),
     "lshmoe_sp_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _i32, _vp, _vp], _i32),
+    "lshmoe_expert_ffn_backward": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp],
+                                   _i32),
     "lshmoe_grad_compress_workspace": ([_i32, ctypes.POINTER(_sz)], _i32),
     "lshmoe_grad_compress": ([_vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp], _i32),
     "lshmoe_grad_restore": ([_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _vp],
@@ -323,6 +325,26 @@ def grad_compress(dy: torch.Tensor, comp: "Compressed", gate_weight: Optional[to
     _check(_lib.lshmoe_grad_compress(_ptr(dy), _dt(dy), n, d, _ptr(gate_weight), _ptr(comp.bucket), _ptr(comp.perm),
                                      _ptr(comp.row_start), k, _ptr(out), _ptr(out_f32), _ptr(workspace),
                                      workspace.numel(), _stream(stream)), "lshmoe_grad_compress")
+    return out
+
+
+def expert_ffn_backward(grad_out: torch.Tensor, recv_rows: torch.Tensor, W2T: torch.Tensor, W1T: torch.Tensor,
+                        hidden: torch.Tensor, out: Optional[torch.Tensor] = None,
+                        dhidden: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """H = J_E(c~)^T G per received row (dX path of the expert's backward, reading R27).
+    W2T [E_local, d_ffn, d], W1T [E_local, d, d_ffn] (transposed weights); hidden = the forward's
+    post-ReLU activations (expert_ffn's `hidden`)."""
+    _require_cuda(grad_out, recv_rows, W2T, W1T, hidden)
+    cap, d = grad_out.shape
+    E_local, d_ffn = W2T.shape[0], W2T.shape[1]
+    world = recv_rows.shape[1]
+    if out is None:
+        out = torch.empty_like(grad_out)
+    if dhidden is None:
+        dhidden = torch.empty((cap, d_ffn), dtype=grad_out.dtype, device=grad_out.device)
+    _check(_lib.lshmoe_expert_ffn_backward(_ptr(grad_out), _dt(grad_out), d, d_ffn, _ptr(recv_rows), E_local, world,
+                                           _ptr(W2T), _ptr(W1T), _ptr(hidden), _ptr(dhidden), cap, _ptr(out),
+                                           _stream(stream)), "lshmoe_expert_ffn_backward")
     return out
 
 

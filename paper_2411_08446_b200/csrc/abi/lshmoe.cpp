@@ -163,6 +163,25 @@ lshmoe_status lshmoe_compress(const void* x, lshmoe_dtype dtype, int64_t n, int 
   return cuda_status(err, "lshmoe_compress");
 }
 
+lshmoe_status lshmoe_expert_ffn_backward(const void* grad_out, lshmoe_dtype dtype, int d, int d_ffn,
+                                         const int32_t* recv_rows, int experts_local, int world, const void* W2T,
+                                         const void* W1T, const void* hidden, void* dhidden, int64_t capacity,
+                                         void* grad_in, lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, dtype, capacity, d);
+  if (st) return st;
+  REQUIRE(d_ffn >= 1 && experts_local >= 1 && world >= 1, LSHMOE_EINVAL, "bad sizes");
+  if (dtype == LSHMOE_BF16) REQUIRE(d_ffn % 64 == 0, LSHMOE_EUNSUPPORTED, "bf16 FFN needs d_ffn % 64 == 0");
+  if (dtype == LSHMOE_F32) REQUIRE(d_ffn % 4 == 0, LSHMOE_EUNSUPPORTED, "f32 FFN needs d_ffn % 4 == 0");
+  if (capacity == 0) return LSHMOE_OK;
+  REQUIRE(grad_out && recv_rows && W2T && W1T && hidden && dhidden && grad_in, LSHMOE_EINVAL, "NULL pointer");
+  REQUIRE(aligned16(grad_out) && aligned16(hidden) && aligned16(dhidden) && aligned16(grad_in) && aligned16(W1T) &&
+              aligned16(W2T),
+          LSHMOE_EINVAL, "operands must be 16-byte aligned");
+  return cuda_status(launch_expert_ffn_backward(grad_out, dtype, d, d_ffn, recv_rows, experts_local, world, W2T, W1T,
+                                                hidden, dhidden, capacity, grad_in, stream),
+                     "lshmoe_expert_ffn_backward");
+}
+
 lshmoe_status lshmoe_grad_compress_workspace(int d, size_t* bytes) {
   REQUIRE(bytes != nullptr && d >= 1, LSHMOE_EINVAL, "bad arguments");
   *bytes = grad_compress_workspace_layout(d, nullptr, nullptr, nullptr);

@@ -72,6 +72,16 @@ int launch_expert_ffn(const void* in, lshmoe_dtype dtype, int d, int d_ffn, cons
                       int experts_local, int world, const void* W1, const void* b1, const void* W2,
                       const void* b2, void* hidden, int64_t capacity, void* out, void* stream);
 
+int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, int E_local, int world,
+                    const void* W1, const void* b1, const void* W2, const void* b2, void* hidden, int64_t capacity,
+                    void* out, void* stream);
+int launch_ffn_bwd_bf16(const void* G, int d, int d_ffn, const int32_t* recv_rows, int E_local, int world,
+                        const void* W2T, const void* W1T, const void* hidden, void* dhidden, int64_t capacity,
+                        void* H, void* stream);
+int launch_expert_ffn_backward(const void* grad_out, lshmoe_dtype dtype, int d, int d_ffn, const int32_t* recv_rows,
+                               int E_local, int world, const void* W2T, const void* W1T, const void* hidden,
+                               void* dhidden, int64_t capacity, void* grad_in, void* stream);
+
 int read_and_clear_device_error(int* value, void* stream);
 void set_compress_diag(int on);   // per-CTA globaltimer stamps in the compress workspace header
 void count_launches(int n);   // kernels launched by this library (lshmoe_kernel_launches)

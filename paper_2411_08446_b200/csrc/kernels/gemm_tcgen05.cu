@@ -343,23 +343,44 @@ struct BiasActEpi {
   int N;
   bool relu;
   int exp = 0;                // experiment (LSHMOE_FFN_EXP): 1 = no output stores, 2 = no MMAs
+  const __nv_bfloat16* mask = nullptr;   // NEXT-1 backward: out *= [mask > 0] (the forward's hidden), no bias
   const __nv_bfloat16* bias_unit;   // this unit's BN bias values (read-only cache, warp broadcast)
-  __device__ void begin(const WorkItem& w, uint8_t*) { bias_unit = bias + static_cast<int64_t>(w.tag0) * N + w.tag1; }
+  __device__ void begin(const WorkItem& w, uint8_t*) {
+    bias_unit = bias ? bias + static_cast<int64_t>(w.tag0) * N + w.tag1 : nullptr;
+  }
   __device__ void consume(const WorkItem& w, int row, const uint32_t (&r)[32], int col0, const uint8_t* scratch) {
     if (row >= w.valid_rows) return;
-    const uint32_t* bw = reinterpret_cast<const uint32_t*>(bias_unit) + col0 / 2;
     uint32_t packed[16];
+    if (mask) {                 // backward: acc * relu'(pre), relu'(pre) = [h > 0] from the saved h
+      const uint4* mrow = reinterpret_cast<const uint4*>(mask + static_cast<int64_t>(w.a_row + row) * N + w.tag1 + col0);
+      uint32_t mw[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const uint32_t b2 = __ldg(bw + i);
-      float v0 = __uint_as_float(r[2 * i]) + __uint_as_float(b2 << 16);
-      float v1 = __uint_as_float(r[2 * i + 1]) + __uint_as_float(b2 & 0xFFFF0000u);
-      if (relu) {
-        v0 = fmaxf(v0, 0.0f);
-        v1 = fmaxf(v1, 0.0f);
+      for (int i = 0; i < 4; ++i) {
+        const uint4 m4 = __ldg(mrow + i);
+        mw[4 * i] = m4.x; mw[4 * i + 1] = m4.y; mw[4 * i + 2] = m4.z; mw[4 * i + 3] = m4.w;
       }
-      __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
-      packed[i] = *reinterpret_cast<uint32_t*>(&h);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const bool p0 = __uint_as_float(mw[i] << 16) > 0.0f, p1 = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.0f;
+        const float v0 = p0 ? __uint_as_float(r[2 * i]) : 0.0f;
+        const float v1 = p1 ? __uint_as_float(r[2 * i + 1]) : 0.0f;
+        __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
+        packed[i] = *reinterpret_cast<uint32_t*>(&h);
+      }
+    } else {
+      const uint32_t* bw = reinterpret_cast<const uint32_t*>(bias_unit) + col0 / 2;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t b2 = bias ? __ldg(bw + i) : 0u;
+        float v0 = __uint_as_float(r[2 * i]) + __uint_as_float(b2 << 16);
+        float v1 = __uint_as_float(r[2 * i + 1]) + __uint_as_float(b2 & 0xFFFF0000u);
+        if (relu) {
+          v0 = fmaxf(v0, 0.0f);
+          v1 = fmaxf(v1, 0.0f);
+        }
+        __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
+        packed[i] = *reinterpret_cast<uint32_t*>(&h);
+      }
     }
     uint4* dst = reinterpret_cast<uint4*>(out + static_cast<int64_t>(w.a_row + row) * N + w.tag1 + col0);
     if (exp == 1) {
@@ -772,6 +793,47 @@ int launch_sp_hash_bf16(const void* x, int64_t n, int d, const void* normals, in
     case 128: return launch_sp_np<128>(x, n, d, normals, q, b, codes, st);
     default: return launch_sp_np<256>(x, n, d, normals, q, b, codes, st);
   }
+}
+
+// NEXT-1 expert backward (reading R27's H = J_E(c~)^T G, dX path only): two grouped TN GEMMs on
+// the forward's machinery with the caller's transposed weights —
+//   dh = (G W2) * [h > 0]   B = W2^T [E_local, d_ffn, d], K = d, mask = the forward's hidden h
+//   H  = dh W1              B = W1^T [E_local, d, d_ffn], K = d_ffn, no bias
+int launch_ffn_bwd_bf16(const void* G, int d, int d_ffn, const int32_t* recv_rows, int E_local, int world,
+                        const void* W2T, const void* W1T, const void* hidden, void* dhidden, int64_t capacity,
+                        void* H, void* stream) {
+  if (E_local > kMaxLocalExperts) return cudaErrorInvalidValue;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cta = cta_mode("LSHMOE_FFN_CTA", 2);
+  const __nv_bfloat16* hmask = static_cast<const __nv_bfloat16*>(hidden);
+  FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, 0, nullptr, nullptr};
+  int err;
+  const int bn1 = pick_bn(d_ffn);
+  if (bn1 == 256) {
+    BiasActEpi<256> e1{nullptr, static_cast<__nv_bfloat16*>(dhidden), d_ffn, false};
+    e1.mask = hmask;
+    err = launch_bn(bn1, cta, G, capacity, W2T, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
+  } else if (bn1 == 128) {
+    BiasActEpi<128> e1{nullptr, static_cast<__nv_bfloat16*>(dhidden), d_ffn, false};
+    e1.mask = hmask;
+    err = launch_bn(bn1, cta, G, capacity, W2T, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
+  } else {
+    BiasActEpi<64> e1{nullptr, static_cast<__nv_bfloat16*>(dhidden), d_ffn, false};
+    e1.mask = hmask;
+    err = launch_bn(bn1, cta, G, capacity, W2T, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
+  }
+  if (err) return err;
+  FfnSched s2{recv_rows, E_local, world, d, 0, 0, 0, nullptr, nullptr};
+  const int bn2 = pick_bn(d);
+  if (bn2 == 256) {
+    BiasActEpi<256> e2{nullptr, static_cast<__nv_bfloat16*>(H), d, false};
+    return launch_bn(bn2, cta, dhidden, capacity, W1T, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, 0, st);
+  } else if (bn2 == 128) {
+    BiasActEpi<128> e2{nullptr, static_cast<__nv_bfloat16*>(H), d, false};
+    return launch_bn(bn2, cta, dhidden, capacity, W1T, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, 0, st);
+  }
+  BiasActEpi<64> e2{nullptr, static_cast<__nv_bfloat16*>(H), d, false};
+  return launch_bn(bn2, cta, dhidden, capacity, W1T, static_cast<int64_t>(E_local) * d, d_ffn, s2, e2, 0, st);
 }
 
 int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, int E_local, int world,

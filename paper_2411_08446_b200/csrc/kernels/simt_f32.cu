@@ -102,9 +102,12 @@ __global__ void __launch_bounds__(kTok) sp_hash_f32_kernel(const float* __restri
 
 // One thread per output element of one GEMM layer over rows segmented by expert:
 // out[r][o] = act(sum_i W[e][o][i] * in[r][i] + b[e][o]).  Segment table recomputed per CTA.
+// b nullable (no bias); mask nullable: out *= [mask[r][o] > 0] (NEXT-1: relu' from the forward's
+// saved hidden activations).
 __global__ void ffn_f32_layer_kernel(const float* __restrict__ in, int K, int N, const int32_t* __restrict__ recv_rows,
                                      int E_local, int world, const float* __restrict__ W, const float* __restrict__ b,
-                                     float* __restrict__ out, int64_t capacity, int relu) {
+                                     float* __restrict__ out, int64_t capacity, int relu,
+                                     const float* __restrict__ mask = nullptr) {
   __shared__ int seg_end[257];
   if (threadIdx.x == 0) {
     int rows = 0;
@@ -123,7 +126,8 @@ __global__ void ffn_f32_layer_kernel(const float* __restrict__ in, int K, int N,
     const float* xi = in + static_cast<int64_t>(r) * K;
     float acc = 0.0f;
     for (int i = 0; i < K; ++i) acc = fmaf(w[i], xi[i], acc);
-    acc += b[static_cast<int64_t>(e) * N + o];
+    if (b) acc += b[static_cast<int64_t>(e) * N + o];
+    if (mask && !(mask[static_cast<int64_t>(r) * N + o] > 0.0f)) acc = 0.0f;
     out[static_cast<int64_t>(r) * N + o] = relu ? fmaxf(acc, 0.0f) : acc;
   }
 }
@@ -177,6 +181,28 @@ int launch_expert_ffn(const void* in, lshmoe_dtype dtype, int d, int d_ffn, cons
   ffn_f32_layer_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(hidden), d_ffn, d, recv_rows, E_local, world,
                                             static_cast<const float*>(W2), static_cast<const float*>(b2),
                                             static_cast<float*>(out), capacity, 0);
+  count_launches(2);
+  return cudaGetLastError();
+}
+
+int launch_expert_ffn_backward(const void* grad_out, lshmoe_dtype dtype, int d, int d_ffn, const int32_t* recv_rows,
+                               int E_local, int world, const void* W2T, const void* W1T, const void* hidden,
+                               void* dhidden, int64_t capacity, void* grad_in, void* stream) {
+  if (dtype == LSHMOE_BF16)
+    return launch_ffn_bwd_bf16(grad_out, d, d_ffn, recv_rows, E_local, world, W2T, W1T, hidden, dhidden, capacity,
+                               grad_in, stream);
+  if (E_local > 256) return cudaErrorInvalidValue;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = 4 * device_sm_count();
+  // dh = (G W2) * [h > 0]  (W2T = W2^T per expert, [d_ffn, d]);  H = dh W1  (W1T = W1^T, [d, d_ffn])
+  ffn_f32_layer_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(grad_out), d, d_ffn, recv_rows, E_local, world,
+                                            static_cast<const float*>(W2T), nullptr, static_cast<float*>(dhidden),
+                                            capacity, 0, static_cast<const float*>(hidden));
+  int err = cudaGetLastError();
+  if (err) return err;
+  ffn_f32_layer_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(dhidden), d_ffn, d, recv_rows, E_local, world,
+                                            static_cast<const float*>(W1T), nullptr, static_cast<float*>(grad_in),
+                                            capacity, 0, nullptr);
   count_launches(2);
   return cudaGetLastError();
 }

@@ -100,3 +100,49 @@ def test_backward_f32_giant_bucket_spans_ctas(L):
     assert row_rel_err(f64(G[:b.m]), Go) <= 1e-5
     G2 = L.grad_compress(dY.cuda(), comp)
     assert torch.equal(G[:b.m], G2[:b.m])            # deterministic (rows past m are unused)
+
+
+@pytest.mark.parametrize("cfgname", ["C1", "C2"])
+def test_expert_ffn_backward(L, cfgname):
+    """lshmoe_expert_ffn_backward (H = J_E(c~)^T G, the dX path of the expert's backward) vs the
+    oracle's expert_ffn_vjp on the same received rows (world 1: recv = centroid layout).  A row whose
+    fp64 pre-activation has an element within 1e-5 (relative) of zero is a relu' near-tie (the GPU's
+    fp32 pre-activation may take the other side) and is reported, not compared."""
+    cfg = CONFIGS[cfgname]
+    case = make_case(L, cfg, seed=0, sanitize=True)
+    b = O.bucketize(case.codes, case.zeta.numpy(), cfg.E)
+    Ct = O.round_to_dtype(O.centroids(f64(case.X), b, cfg.k), cfg.dtype)
+    m = b.m
+    dt = case.X.dtype
+    ex = make_experts(cfg, 0)
+    W1 = torch.stack([ex[e][0] for e in range(cfg.E)]).cuda()
+    b1 = torch.stack([ex[e][1] for e in range(cfg.E)]).cuda()
+    W2 = torch.stack([ex[e][2] for e in range(cfg.E)]).cuda()
+    b2 = torch.stack([ex[e][3] for e in range(cfg.E)]).cuda()
+    W2T = W2.transpose(1, 2).contiguous()
+    W1T = W1.transpose(1, 2).contiguous()
+    rr = torch.from_numpy(b.expert_rows.astype(np.int32)).view(cfg.E, 1).cuda()
+    rng = np.random.default_rng(7)
+    Gh = torch.from_numpy(rng.standard_normal((m, cfg.d))).to(torch.float32).to(dt)
+    recv = torch.from_numpy(Ct).to(torch.float32).to(dt).cuda()
+    hid = torch.empty((m, cfg.d_ffn), dtype=dt, device="cuda")
+    L.expert_ffn(recv, rr, W1, b1, W2, b2, hidden=hid)
+    H = L.expert_ffn_backward(Gh.cuda(), rr, W2T, W1T, hid)
+    torch.cuda.synchronize()
+    Ho = np.zeros((m, cfg.d))
+    near = np.zeros(m, dtype=bool)
+    off = 0
+    for e, me in enumerate(b.expert_rows):
+        if me:
+            w1, bb1, w2, _ = (f64(t) for t in ex[e])
+            Ho[off:off + me] = O.expert_ffn_vjp(Ct[off:off + me], w1, bb1, w2, f64(Gh[off:off + me]))
+            pre = Ct[off:off + me] @ w1.T + bb1
+            near[off:off + me] = (np.abs(pre) < 1e-5 * np.abs(pre).max(axis=1, keepdims=True)).any(axis=1)
+        off += me
+    Hg = f64(H)
+    ok = ~near
+    tol = 1e-5 if cfg.dtype == "f32" else 2e-2
+    err = row_rel_err(Hg[ok], Ho[ok])
+    print(f"[expert bwd {cfgname}] m={m} rows with relu' near-ties={int(near.sum())} err={err:.2e}")
+    assert err <= tol
+    assert ok.sum() >= 0.5 * m
