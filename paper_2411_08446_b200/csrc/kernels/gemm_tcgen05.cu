@@ -163,13 +163,23 @@ struct FfnSched {
     }
     __syncthreads();
   }
+  int order;        // 0: units expert-major (e, mt, nt); 1: N-tile-major (nt, e, mt)
   __device__ int units() const { return tiles_pre[E_local]; }
   __device__ WorkItem get(int u, int rank) const {
-    int e = 0;
-    while (tiles_pre[e + 1] <= u) ++e;
+    int e = 0, mt, nt;
     const int ntn = N / bn;
-    const int local = u - tiles_pre[e];
-    const int mt = local / ntn, nt = local - mt * ntn;
+    if (order == 0) {
+      while (tiles_pre[e + 1] <= u) ++e;
+      const int local = u - tiles_pre[e];
+      mt = local / ntn;
+      nt = local - mt * ntn;
+    } else {                 // tiles_pre[e] / ntn = M-tiles of the experts before e
+      const int T = tiles_pre[E_local] / ntn;
+      nt = u / T;
+      const int j = u - nt * T;
+      while (tiles_pre[e + 1] / ntn <= j) ++e;
+      mt = j - tiles_pre[e] / ntn;
+    }
     WorkItem w;
     w.a_row = seg_start[e] + mt * bm + rank * BM;
     w.b_row0 = e * N + nt * bn;
@@ -705,6 +715,11 @@ int cta_mode(const char* env_name, int dflt) {
   return dflt;
 }
 
+int ffn_order() {   // experiment override LSHMOE_FFN_ORDER (0 expert-major, 1 N-tile-major)
+  const char* env = getenv("LSHMOE_FFN_ORDER");
+  return env ? atoi(env) : 0;
+}
+
 int ffn_prefetch() {   // experiment override LSHMOE_FFN_PF (k-blocks); default 0 (measured: no gain)
   const char* env = getenv("LSHMOE_FFN_PF");
   return env ? atoi(env) : 0;
@@ -806,7 +821,7 @@ int launch_ffn_bwd_bf16(const void* G, int d, int d_ffn, const int32_t* recv_row
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int cta = cta_mode("LSHMOE_FFN_CTA", 2);
   const __nv_bfloat16* hmask = static_cast<const __nv_bfloat16*>(hidden);
-  FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, 0, nullptr, nullptr};
+  FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, 0, nullptr, nullptr, ffn_order()};
   int err;
   const int bn1 = pick_bn(d_ffn);
   if (bn1 == 256) {
@@ -823,7 +838,7 @@ int launch_ffn_bwd_bf16(const void* G, int d, int d_ffn, const int32_t* recv_row
     err = launch_bn(bn1, cta, G, capacity, W2T, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
   }
   if (err) return err;
-  FfnSched s2{recv_rows, E_local, world, d, 0, 0, 0, nullptr, nullptr};
+  FfnSched s2{recv_rows, E_local, world, d, 0, 0, 0, nullptr, nullptr, ffn_order()};
   const int bn2 = pick_bn(d);
   if (bn2 == 256) {
     BiasActEpi<256> e2{nullptr, static_cast<__nv_bfloat16*>(H), d, false};
@@ -844,7 +859,7 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
   const int cta = cta_mode("LSHMOE_FFN_CTA", 2);
   const int only = cta_mode("LSHMOE_FFN_ONLY", 0);   // experiment: 1 / 2 = launch only GEMM 1 / 2
   const int exp = cta_mode("LSHMOE_FFN_EXP", 0);     // experiment: 1 = no output stores, 2 = no MMAs
-  FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, ffn_prefetch(), nullptr, nullptr};
+  FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, ffn_prefetch(), nullptr, nullptr, ffn_order()};
   const int bn1 = env_bn("LSHMOE_FFN_BN1", d_ffn, pick_bn(d_ffn));
   int err = 0;
   if (only == 2) {
@@ -859,7 +874,7 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
     err = launch_bn(bn1, cta, in, capacity, W1, static_cast<int64_t>(E_local) * d_ffn, d, s1, e1, 0, st);
   }
   if (err || only == 1) return err;
-  FfnSched s2{recv_rows, E_local, world, d, 0, 0, ffn_prefetch(), nullptr, nullptr};
+  FfnSched s2{recv_rows, E_local, world, d, 0, 0, ffn_prefetch(), nullptr, nullptr, ffn_order()};
   const int bn2 = env_bn("LSHMOE_FFN_BN2", d, pick_bn(d));
   if (bn2 == 256) {
     BiasActEpi<256> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false}; e2.exp = exp;

@@ -103,15 +103,15 @@ def main():
         m = int(comp.num_rows.item())
         fl = 4.0 * m * cfg.d * cfg.d_ffn
         for only in ("1", "2"):
-            for cta, bn, pf, ex in (("2", "256", "0", "0"), ("2", "256", "0", "1"), ("2", "256", "0", "2"),
-                                    ("1", "256", "0", "0"), ("1", "256", "0", "1"), ("1", "256", "0", "2")):
+            for cta, bn, od, ex in (("2", "256", "0", "0"), ("2", "256", "1", "0"), ("1", "256", "0", "0"),
+                                    ("1", "256", "1", "0"), ("2", "128", "1", "0")):
                     os.environ.update(LSHMOE_FFN_CTA=cta, LSHMOE_FFN_BN1=bn, LSHMOE_FFN_BN2=bn, LSHMOE_FFN_ONLY=only,
-                                      LSHMOE_FFN_PF=pf, LSHMOE_FFN_EXP=ex)
+                                      LSHMOE_FFN_ORDER=od, LSHMOE_FFN_EXP=ex)
                     for fl_ in ((flush, None) if ex == "0" else (flush,)):
                         med, mn = timeit(lambda: L.expert_ffn(comp.centroids, rr, *W, out=out, hidden=hid), flush=fl_)
-                        print(f"ffn GEMM{only} cta={cta} bn={bn} exp={ex} flush={fl_ is not None}: median {med:.1f} us  "
+                        print(f"ffn GEMM{only} cta={cta} bn={bn} order={od} flush={fl_ is not None}: median {med:.1f} us  "
                               f"min {mn:.1f} us  {fl / 2 / med / 1e6:.0f} TFLOP/s  (m={m})", flush=True)
-        for k in ("LSHMOE_FFN_CTA", "LSHMOE_FFN_BN1", "LSHMOE_FFN_BN2", "LSHMOE_FFN_ONLY", "LSHMOE_FFN_PF", "LSHMOE_FFN_EXP"):
+        for k in ("LSHMOE_FFN_CTA", "LSHMOE_FFN_BN1", "LSHMOE_FFN_BN2", "LSHMOE_FFN_ONLY", "LSHMOE_FFN_ORDER", "LSHMOE_FFN_EXP"):
             os.environ.pop(k)
         med, mn = timeit(lambda: L.expert_ffn(comp.centroids, rr, *W, out=out, hidden=hid), flush=None)
         print(f"ffn default, NO L2 flush (weights L2-resident): median {med:.1f} us  {fl / med / 1e6:.0f} TFLOP/s",
