@@ -38,8 +38,9 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--q", type=int, default=None, help="override the number of hash functions")
     p.add_argument("--impl", default="lsh", choices=["lsh", "reference"])
-    p.add_argument("--hash", default="cp", choices=["cp", "sp"],
-                   help="hash family: cross-polytope (paper default, Eq. 3) or spherical-plane (NEXT-3)")
+    p.add_argument("--hash", default="cp", choices=["cp", "sp", "cp8"],
+                   help="hash family: cross-polytope (paper default, Eq. 3), spherical-plane (NEXT-3), or "
+                        "cross-polytope on e4m3 operands (NEXT-2 fp8 option)")
     p.add_argument("--sp-bits", type=int, default=12, help="sign bits per SP hash function")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-uncompressed", action="store_true")
@@ -164,6 +165,8 @@ def workload_config(cfg, world, args=None):
     hashing = "cross-polytope (Eq. 3)"
     if args is not None and args.hash == "sp":
         hashing = f"spherical-plane sign bits, {args.sp_bits} per hash (NEXT-3)"
+    if args is not None and args.hash == "cp8":
+        hashing = "cross-polytope on e4m3-quantised x and R (NEXT-2 fp8 option, reading R28)"
     return {"workload": f"{cfg.name}: {cfg.note}", "hash": hashing, "tokens_per_gpu": cfg.n, "d_model": cfg.d,
             "experts": cfg.E,
             "experts_per_gpu": cfg.E // world, "top_k": cfg.k, "hash_functions": cfg.q, "d_ffn": cfg.d_ffn,
@@ -258,17 +261,21 @@ def main():
 def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, zeta_cpu, X, zeta, R, codes, comp, ws,
               cap, recv, rr, hid, eo, ret, y, flush, stream, W1, b1, W2, b2, dist):
     import torch
-    from lshmoe_inputs import make_experts
+    from lshmoe_inputs import make_experts, rotation_seed
     n, k, d = cfg.n, cfg.k, cfg.d
     nk = n * k
 
     Nrm = L.sp_normals(R, args.sp_bits) if args.hash == "sp" else None
+    R8 = L.rotation_e4m3(cfg.d, cfg.q, rotation_seed(args.seed)).to(dev) if args.hash == "cp8" else None
+    x8 = torch.empty((n, d), dtype=torch.uint8, device=dev) if args.hash == "cp8" else None
 
     def make_stages(Xb, zb, yb):
         """The six calls of one step on token / gate / output buffers (Xb, zb, yb); the
         intermediates (codes, compressed rows, exchange and FFN buffers) are shared."""
         if args.hash == "sp":
             h = lambda: L.sp_hash(Xb, Nrm, cfg.q, args.sp_bits, codes)   # noqa: E731
+        elif args.hash == "cp8":
+            h = lambda: (L.quantize_e4m3(Xb, out=x8), L.hash_e4m3(x8, R8, codes))   # noqa: E731
         else:
             h = lambda: L.hash(Xb, R, codes)   # noqa: E731
         return [
@@ -532,7 +539,15 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     torch.cuda.synchronize()
     hash_dev_ms = statistics.median(a.elapsed_time(b) for a, b in hev)
     pk = peaks()
-    if args.hash == "sp":
+    if args.hash == "cp8":
+        flops = 2.0 * n * cfg.q * d * d
+        achieved = flops / (hash_dev_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": "quantize_e4m3 + tc_gemm_kernel<ArgmaxEpi, e4m3> (lshmoe_hash_e4m3)",
+                "achieved": achieved, "peak": 2 * pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / (2 * pk["bf16_tflops"]), "traffic": None,
+                "per_launch": {"flops": flops, "avg_ms": hash_dev_ms, "eager_stage_ms": hash_ms},
+                "peak_source": pk["source"] + " bf16 dense (burst) x 2 (the guide's fp8:bf16 nominal ratio)"}
+    elif args.hash == "sp":
         nbytes = n * d * 2 + L.sp_rows(cfg.q, args.sp_bits) * d * 2 + n * cfg.q * 2
         achieved = nbytes / (hash_dev_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": "tc_gemm_kernel<SignBitsEpi> (lshmoe_sp_hash)", "achieved": achieved,

@@ -106,6 +106,20 @@ lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d,
                           const void* rotation, int q, int16_t* codes,
                           void* workspace, size_t workspace_bytes, lshmoe_stream stream);
 
+/* ---- NEXT-2 fp8 option: cross-polytope hash on e4m3 operands (reading R28) ---
+   Eq. 3's argmax is invariant to a positive scale of x and, per hash function, of R_j, so both are
+   scaled by the largest power of two that keeps their max magnitude <= 448 and rounded to e4m3
+   (RNE); the codes are Eq. 3 on those values, computed on kind::f8f6f4 tensor cores (exact e4m3
+   products, fp32 accumulation).  This is a different hash of x than lshmoe_hash's (decisions within
+   the e4m3 rounding of a tie may differ) and halves the rotation's tensor-core time.
+   lshmoe_rotation_e4m3: [host] out q*d*d bytes, from the fp32 lshmoe_rotation of the same seed.
+   lshmoe_quantize_e4m3: x bf16 [n, d] -> x8 [n, d] bytes, per-row power-of-two scale; d % 64 == 0.
+   lshmoe_hash_e4m3: codes int16 [n, q] from x8 and R8 (device); workspace as lshmoe_hash's. */
+lshmoe_status lshmoe_rotation_e4m3(int d, int q, uint64_t rotation_seed, uint8_t* out /* [host] */);
+lshmoe_status lshmoe_quantize_e4m3(const void* x, int64_t n, int d, uint8_t* x8, lshmoe_stream stream);
+lshmoe_status lshmoe_hash_e4m3(const uint8_t* x8, int64_t n, int d, const uint8_t* rotation8, int q, int16_t* codes,
+                               void* workspace, size_t workspace_bytes, lshmoe_stream stream);
+
 /* ---- NEXT-3: spherical-plane (SP) hash, the paper's other evaluated family (§4.5) --
    The paper gives no construction; SPEC's sign-bit reading (reading R26): hash
    function j owns the b unit normals in rows j*b .. j*b+b-1 of `normals`, and

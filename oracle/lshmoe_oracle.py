@@ -14,6 +14,8 @@ The functions follow Algorithm 1 (App. A "Framework of LSH-MoE") ste
 
   O1  rotation(d, q, seed)            random rotation R_j of Eq. 3            [pinned]
   O2  cp_hash(X, R)                   Eq. 3 cross-polytope hash           [pinned]
+  O2" e4m3 quantisation + cp_hash     NEXT-2's fp8 rotation option: codes of the
+                                      e4m3-rounded, power-of-two-scaled x and R_j (reading R28) [pinned]
   O2' sp_hash(X, N, q, b)             §4.5 spherical-plane hashing (P:L474-479), SPEC's
                                       sign-bit construction (reading R26)   [pinned]
   O3  group_by_expert(zeta, E)        Alg. 1 L3 "Dispatch X into {X_i}"        [pinned]
@@ -47,7 +49,8 @@ import numpy as np
 __all__ = [
     "GAMMA", "splitmix64_stream", "irwin_hall_gaussian", "rotation_fp64", "rotation",
     "round_to_dtype", "f32_to_bf16_bits", "bf16_bits_to_f64", "to_stored",
-    "cp_hash", "sp_hash", "sp_normals", "group_by_expert", "bucketize", "Buckets", "centroids", "expert_ffn",
+    "cp_hash", "sp_hash", "sp_normals", "e4m3_values", "round_e4m3", "pow2_scale_e4m3",
+    "quantize_tokens_e4m3", "quantize_rotation_e4m3", "group_by_expert", "bucketize", "Buckets", "centroids", "expert_ffn",
     "dispatch_sim", "combine_sim", "restore", "moe_dense", "lsh_layer", "lsh_layer_ranks",
     "LayerResult", "ulp_bf16", "grad_compress", "expert_ffn_vjp", "grad_restore", "lsh_layer_backward",
 ]
@@ -200,6 +203,61 @@ def cp_hash(X: np.ndarray, R: np.ndarray):
             with np.errstate(invalid="ignore", divide="ignore"):
                 margins[:, j] = np.where(amax > 0, (amax - second) / np.where(amax > 0, amax, 1.0), 0.0)
     return codes, margins
+
+
+# ---------------------------------------------------------------------------------------------
+# O2". NEXT-2's fp8 option ("optionally fp8 (kind::f8f6f4) rotation to halve
+# the hash cost (codes then defined on fp8-rounded values)").  Reading R28: Eq. 3's argmax is
+# invariant to a positive scale of x and, per hash function, of R_j, so each token and each R_j
+# is scaled by the largest power of two 2^k with max|v| * 2^k <= 448 (e4m3's largest finite value)
+# and rounded to e4m3 (round to nearest, ties to even); the codes are Eq. 3 evaluated exactly on
+# those values.  R_j's source is the fp32-stored rotation (O1).
+# ---------------------------------------------------------------------------------------------
+def e4m3_values() -> np.ndarray:
+    """The 127 non-negative finite e4m3 (e4m3fn) values in code order 0x00..0x7E."""
+    vals = []
+    for code in range(0x7F):
+        e, m = code >> 3, code & 7
+        vals.append(m * 2.0 ** -9 if e == 0 else (1 + m / 8.0) * 2.0 ** (e - 7))
+    return np.array(vals)
+
+
+def round_e4m3(a: np.ndarray) -> np.ndarray:
+    """Nearest e4m3 value (ties to the even code), |a| <= 448; by search in the value table."""
+    a = np.asarray(a, dtype=np.float64)
+    if np.any(np.abs(a) > 448):
+        raise ValueError("|a| > 448")
+    tab = e4m3_values()
+    mag = np.abs(a)
+    hi = np.searchsorted(tab, mag, side="left").clip(0, len(tab) - 1)   # first value >= mag
+    lo = np.maximum(hi - 1, 0)
+    dlo, dhi = mag - tab[lo], tab[hi] - mag
+    pick_hi = (dhi < dlo) | ((dhi == dlo) & (hi % 2 == 0) & (hi != lo))
+    out = np.where(pick_hi, tab[hi], tab[lo])
+    out = np.where(mag == tab[hi], tab[hi], out)
+    return np.where(a < 0, -out, out)
+
+
+def pow2_scale_e4m3(vmax: float) -> float:
+    """Largest 2^k with vmax * 2^k <= 448 (1 for vmax == 0)."""
+    if vmax == 0:
+        return 1.0
+    f, e = math.frexp(vmax)                 # vmax = f * 2^e, f in [0.5, 1)
+    k = (9 - e) if f <= 0.875 else (8 - e)   # 448 = 0.875 * 2^9
+    return math.ldexp(1.0, k)
+
+
+def quantize_tokens_e4m3(X: np.ndarray) -> np.ndarray:
+    """Per-token power-of-two scale, then e4m3 (values as fp64)."""
+    X = np.asarray(X, np.float64)
+    sc = np.array([pow2_scale_e4m3(float(np.abs(r).max())) for r in X])
+    return round_e4m3(X * sc[:, None])
+
+
+def quantize_rotation_e4m3(R32: np.ndarray) -> np.ndarray:
+    """Per-hash power-of-two scale of the fp32-stored R_j, then e4m3 (values as fp64)."""
+    R32 = np.asarray(R32, np.float64)
+    return np.stack([round_e4m3(Rj * pow2_scale_e4m3(float(np.abs(Rj).max()))) for Rj in R32])
 
 
 # ---------------------------------------------------------------------------------------------

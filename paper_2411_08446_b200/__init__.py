@@ -41,6 +41,9 @@ _SIGS = {
     "lshmoe_rotation": ([_i32, _i32, _u64, _i32, _vp], _i32),
     "lshmoe_hash_workspace": ([_i64, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
     "lshmoe_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _sz, _vp], _i32),
+    "lshmoe_rotation_e4m3": ([_i32, _i32, _u64, _vp], _i32),
+    "lshmoe_quantize_e4m3": ([_vp, _i64, _i32, _vp, _vp], _i32),
+    "lshmoe_hash_e4m3": ([_vp, _i64, _i32, _vp, _i32, _vp, _vp, _sz, _vp], _i32),
     "lshmoe_sp_rows": ([_i32, _i32], _i32),
     "lshmoe_sp_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _i32, _vp, _vp], _i32),
     "lshmoe_expert_ffn_backward": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp],
@@ -167,6 +170,40 @@ def hash(x: torch.Tensor, R: torch.Tensor, codes: Optional[torch.Tensor] = None,
     wsb = 0 if workspace is None else workspace.numel()
     _check(_lib.lshmoe_hash(_ptr(x), _dt(x), n, d, _ptr(R), q, _ptr(codes), _ptr(workspace), wsb, _stream(stream)),
            "lshmoe_hash")
+    return codes
+
+
+def rotation_e4m3(d: int, q: int, seed: int) -> torch.Tensor:
+    """e4m3 bytes uint8 [q, d, d] of the power-of-two-scaled fp32 rotations (reading R28), host."""
+    out = torch.empty((q, d, d), dtype=torch.uint8)
+    _check(_lib.lshmoe_rotation_e4m3(d, q, ctypes.c_uint64(seed), ctypes.c_void_p(out.data_ptr())),
+           "lshmoe_rotation_e4m3")
+    return out
+
+
+def quantize_e4m3(x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """x bf16 [n, d] -> e4m3 bytes uint8 [n, d], per-row power-of-two scale (reading R28)."""
+    _require_cuda(x)
+    n, d = x.shape
+    if out is None:
+        out = torch.empty((n, d), dtype=torch.uint8, device=x.device)
+    _check(_lib.lshmoe_quantize_e4m3(_ptr(x), n, d, _ptr(out), _stream(stream)), "lshmoe_quantize_e4m3")
+    return out
+
+
+def hash_e4m3(x8: torch.Tensor, R8: torch.Tensor, codes: Optional[torch.Tensor] = None,
+              workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Cross-polytope codes int16 [n, q] of e4m3 tokens under e4m3 rotations (NEXT-2 fp8 option)."""
+    _require_cuda(x8, R8)
+    n, d = x8.shape
+    q = R8.shape[0]
+    if codes is None:
+        codes = torch.empty((n, q), dtype=torch.int16, device=x8.device)
+    if workspace is None:
+        workspace = hash_workspace(n, d, q, torch.bfloat16, x8.device)
+    wsb = 0 if workspace is None else workspace.numel()
+    _check(_lib.lshmoe_hash_e4m3(_ptr(x8), n, d, _ptr(R8), q, _ptr(codes), _ptr(workspace), wsb, _stream(stream)),
+           "lshmoe_hash_e4m3")
     return codes
 
 

@@ -105,6 +105,36 @@ lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, c
   return cuda_status(err, "lshmoe_hash");
 }
 
+lshmoe_status lshmoe_rotation_e4m3(int d, int q, uint64_t seed, uint8_t* out) {
+  REQUIRE(d >= 1 && q >= 1, LSHMOE_EINVAL, "d < 1 or q < 1");
+  REQUIRE(q <= LSHMOE_MAX_Q, LSHMOE_EUNSUPPORTED, "q > LSHMOE_MAX_Q");
+  REQUIRE(out != nullptr, LSHMOE_EINVAL, "out is NULL");
+  return rotation_e4m3_host(d, q, seed, out);
+}
+
+lshmoe_status lshmoe_quantize_e4m3(const void* x, int64_t n, int d, uint8_t* x8, lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, LSHMOE_BF16, n, d);
+  if (st) return st;
+  if (n == 0) return LSHMOE_OK;
+  REQUIRE(x && x8 && aligned16(x) && aligned16(x8), LSHMOE_EINVAL, "x / x8 NULL or misaligned");
+  return cuda_status(launch_quantize_e4m3(x, n, d, x8, stream), "lshmoe_quantize_e4m3");
+}
+
+lshmoe_status lshmoe_hash_e4m3(const uint8_t* x8, int64_t n, int d, const uint8_t* R8, int q, int16_t* codes,
+                               void* workspace, size_t workspace_bytes, lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, LSHMOE_BF16, n, d);
+  if (st) return st;
+  REQUIRE(q >= 1, LSHMOE_EINVAL, "q < 1");
+  REQUIRE(q <= LSHMOE_MAX_Q, LSHMOE_EUNSUPPORTED, "q > LSHMOE_MAX_Q");
+  REQUIRE(d % 128 == 0, LSHMOE_EUNSUPPORTED, "e4m3 hash needs d % 128 == 0");
+  if (n == 0) return LSHMOE_OK;
+  REQUIRE(x8 && R8 && codes && aligned16(x8) && aligned16(R8), LSHMOE_EINVAL, "NULL or misaligned pointer");
+  const size_t need = hash_workspace_bytes(n, d, q);
+  REQUIRE(workspace_bytes >= need, LSHMOE_EINVAL, "workspace too small (see lshmoe_hash_workspace)");
+  REQUIRE(need == 0 || (workspace && aligned16(workspace)), LSHMOE_EINVAL, "workspace NULL or misaligned");
+  return cuda_status(launch_hash_e4m3(x8, n, d, R8, q, codes, workspace, stream), "lshmoe_hash_e4m3");
+}
+
 int lshmoe_sp_rows(int q, int b) { return (q >= 1 && b >= 1 && q * b <= 256) ? sp_rows(q, b) : 0; }
 
 lshmoe_status lshmoe_sp_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, const void* normals, int q, int b,

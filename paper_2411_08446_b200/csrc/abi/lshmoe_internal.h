@@ -15,6 +15,9 @@ lshmoe_status cuda_status(int cuda_err, const char* what);   // ECUDA with cudaG
 
 // ---- host ---------------------------------------------------------------------------------
 lshmoe_status rotation_host(int d, int q, uint64_t seed, lshmoe_dtype dtype, void* out);
+lshmoe_status rotation_e4m3_host(int d, int q, uint64_t seed, uint8_t* out);
+int launch_quantize_e4m3(const void* x, int64_t n, int d, uint8_t* out, void* stream);
+int launch_hash_e4m3(const void* x8, int64_t n, int d, const void* R8, int q, int16_t* codes, void* ws, void* stream);
 
 // ---- launchers (csrc/kernels/*.cu); all return cudaError_t as int -------------------------
 int launch_hash_f32(const float* x, int64_t n, int d, const float* R, int q, int16_t* codes, void* stream);

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #include "lshmoe_internal.h"
@@ -99,6 +100,48 @@ lshmoe_status rotation_host(int d, int q, uint64_t seed, lshmoe_dtype dtype, voi
         for (int k = 0; k < d; ++k)
           o[static_cast<size_t>(i) * d + k] = f32_to_bf16_rne(static_cast<float>(Q[static_cast<size_t>(k) * d + i]));
     }
+  }
+  return LSHMOE_OK;
+}
+
+
+// NEXT-2 fp8 option (reading R28): R_j (the fp32-stored rotation) scaled by the largest 2^k with
+// max|R_j| * 2^k <= 448 and rounded to e4m3 (round to nearest, ties to even).
+static uint8_t f32_to_e4m3_rne(float f) {   // |f| <= 448
+  const double a = std::fabs(static_cast<double>(f));
+  const uint8_t sign = f < 0 ? 0x80 : 0;
+  if (a == 0.0) return sign;
+  if (a < 0.015625) {                          // below 2^-6: subnormal grid m * 2^-9
+    const double m = std::nearbyint(a * 512.0);   // ties to even (default rounding mode)
+    return static_cast<uint8_t>(sign | static_cast<uint8_t>(m));   // m == 8 is the first normal (0x08)
+  }
+  int e;
+  const double fr = std::frexp(a, &e);         // a = fr * 2^e, fr in [0.5, 1)
+  int ue = e - 1;                              // a = (2 fr) * 2^ue, 2 fr in [1, 2)
+  double m = std::nearbyint((2.0 * fr - 1.0) * 8.0);
+  if (m == 8.0) {
+    m = 0.0;
+    ++ue;
+  }
+  return static_cast<uint8_t>(sign | static_cast<uint8_t>(((ue + 7) << 3) | static_cast<int>(m)));
+}
+
+lshmoe_status rotation_e4m3_host(int d, int q, uint64_t seed, uint8_t* out) {
+  std::vector<float> R(static_cast<size_t>(q) * d * d);
+  lshmoe_status st = rotation_host(d, q, seed, LSHMOE_F32, R.data());
+  if (st != LSHMOE_OK) return st;
+  const size_t nn = static_cast<size_t>(d) * d;
+  for (int j = 0; j < q; ++j) {
+    const float* Rj = R.data() + j * nn;
+    float vmax = 0.0f;
+    for (size_t i = 0; i < nn; ++i) vmax = std::max(vmax, std::fabs(Rj[i]));
+    int k = 0;
+    if (vmax > 0.0f) {
+      int e;
+      const double fr = std::frexp(static_cast<double>(vmax), &e);
+      k = fr <= 0.875 ? 9 - e : 8 - e;
+    }
+    for (size_t i = 0; i < nn; ++i) out[j * nn + i] = f32_to_e4m3_rne(std::ldexp(Rj[i], k));
   }
   return LSHMOE_OK;
 }

@@ -416,7 +416,10 @@ template <int BN>
 __device__ __forceinline__ bool epi_skip_mma(const BiasActEpi<BN>& e) { return e.exp == 2; }
 
 // ---- the kernel ----------------------------------------------------------------------------------
-template <int BN, int kCta, class Sched, class Epi>
+// kEB: operand element bytes — 2 = bf16 (kind::f16, 16-element MMA K), 1 = e4m3 (kind::f8f6f4,
+// 32-element MMA K).  A k-block is always 128 bytes of K per row (one SWIZZLE_128B atom row), so
+// the shared-memory layout, descriptors and byte offsets are the same for both.
+template <int BN, int kCta, class Sched, class Epi, int kEB = 2>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                    Sched sched, Epi epi) {
@@ -440,7 +443,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int kblocks = K / BK;
+  constexpr int kBKe = 128 / kEB;            // K elements per k-block
+  const int kblocks = K / kBKe;
   const int rank = kCta == 2 ? static_cast<int>(cluster_ctarank()) : 0;
   const bool leader = rank == 0;
   const int cluster = blockIdx.x / kCta;
@@ -485,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (sched.prefetch_b > 0 && pu < units) pw = sched.get(pu, rank);
       auto prefetch_next = [&]() {
         if (sched.prefetch_b == 0 || pu >= units) return;
-        tma_prefetch_l2_2d(&tmB, pkb * BK, pw.b_row0 + pc * BN + rank * C::kBRows);
+        tma_prefetch_l2_2d(&tmB, pkb * kBKe, pw.b_row0 + pc * BN + rank * C::kBRows);
         if (++pkb == kblocks) {
           pkb = 0;
           if (++pc == pw.nchunks) {
@@ -505,12 +509,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             if (kCta == 2) {
               if (leader) mbar_arrive_expect_tx(&full[stage], C::kTxBytes);
-              tma_load_2d_2sm(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, w.a_row);
-              tma_load_2d_2sm(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, brow);
+              tma_load_2d_2sm(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBKe, w.a_row);
+              tma_load_2d_2sm(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBKe, brow);
             } else {
               mbar_arrive_expect_tx(&full[stage], C::kTxBytes);
-              tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * BK, w.a_row);
-              tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, brow);
+              tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBKe, w.a_row);
+              tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBKe, brow);
             }
             if (++stage == C::kStages) {
               stage = 0;
@@ -524,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===== MMA issuer (one thread of the leader CTA) =====
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(BM * kCta, BN);
+      constexpr uint32_t idesc = kEB == 1 ? idesc_e4m3_f32(BM * kCta, BN) : idesc_bf16_f32(BM * kCta, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -543,7 +547,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               if (epi_skip_mma(epi)) break;
-              if (kCta == 2)
+              if (kEB == 1)             // 32 e4m3 = 32 bytes of K per instruction
+                mma_fp8_ss(d_tmem, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), idesc,
+                           (kb | kk) != 0);
+              else if (kCta == 2)
                 mma_bf16_ss_2cta(d_tmem, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), idesc,
                                  (kb | kk) != 0);
               else
@@ -630,23 +637,25 @@ EncodeTiledFn encode_fn() {
 }
 
 // bf16 row-major [rows, cols] tensor, box {64 cols, box_rows rows}, SWIZZLE_128B.
-int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows) {
+// Row-major [rows, cols] tensor of bf16 (eb = 2) or bytes (eb = 1, e4m3), box {128 bytes of cols,
+// box_rows rows}, SWIZZLE_128B.
+int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows, int eb = 2) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * eb};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / eb), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(m, eb == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : cudaErrorInvalidValue;
 }
 
-template <int BN, int kCta, class Sched, class Epi>
+template <int BN, int kCta, class Sched, class Epi, int kEB = 2>
 int launch_tc(const CUtensorMap& a, const CUtensorMap& b, int K, const Sched& s, const Epi& e, int grid,
               cudaStream_t st) {
-  auto kern = tc_gemm_kernel<BN, kCta, Sched, Epi>;
+  auto kern = tc_gemm_kernel<BN, kCta, Sched, Epi, kEB>;
   static bool configured = false;     // one attribute call per instantiation
   if (!configured) {
     int err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, kCta, EpiScratch<Epi>::value>::kSmem);
@@ -771,6 +780,43 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
   }
   return launch_bn(bn, cta, x, n, R, static_cast<int64_t>(q) * d, d, s, e, s.m_tiles * q * (s.split ? d / bn : 1),
                    static_cast<cudaStream_t>(stream));
+}
+
+// NEXT-2 fp8 option (reading R28): the same hash kernel on e4m3 operands (x8 [n, d] from
+// lshmoe_quantize_e4m3, R8 [q*d, d] from lshmoe_rotation_e4m3), kind::f8f6f4 MMAs, 128-element
+// k-blocks (half as many as bf16), the argmax epilogue unchanged.
+int launch_hash_e4m3(const void* x8, int64_t n, int d, const void* R8, int q, int16_t* codes, void* ws, void* stream) {
+  const int bn = pick_bn(d);
+  HashSched s{};
+  s.n = static_cast<int>(n);
+  s.q = q;
+  s.d = d;
+  s.bn = bn;
+  s.bm = BM;
+  s.m_tiles = static_cast<int>((n + BM - 1) / BM);
+  ArgmaxEpi e{};
+  e.codes = codes;
+  e.q = q;
+  e.rows_pad = static_cast<int>(((n + 255) / 256) * 256);
+  s.split = (d > bn) && ws && cta_mode("LSHMOE_HASH_SPLIT", 1) == 1 ? 1 : 0;
+  if (s.split) {
+    const size_t counters = ((sizeof(int) * (e.rows_pad / BM) * q) + 255) & ~size_t(255);
+    e.counter = static_cast<int*>(ws);
+    e.partial = reinterpret_cast<uint2*>(static_cast<uint8_t*>(ws) + counters);
+  }
+  CUtensorMap ma, mb;
+  int err = make_map(&ma, x8, n, d, BM, 1);
+  if (err) return err;
+  err = make_map(&mb, R8, static_cast<int64_t>(q) * d, d, bn, 1);
+  if (err) return err;
+  const int units = s.m_tiles * q * (s.split ? d / bn : 1);
+  const int grid = std::min(device_sm_count(), units);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (bn) {
+    case 256: return launch_tc<256, 1, HashSched, ArgmaxEpi, 1>(ma, mb, d, s, e, grid, st);
+    case 128: return launch_tc<128, 1, HashSched, ArgmaxEpi, 1>(ma, mb, d, s, e, grid, st);
+    default: return launch_tc<64, 1, HashSched, ArgmaxEpi, 1>(ma, mb, d, s, e, grid, st);
+  }
 }
 
 // NEXT-3: SP hash.  B = the normals, rows q*b (the buffer holds sp_rows(q, b) >= q*b rows; rows
