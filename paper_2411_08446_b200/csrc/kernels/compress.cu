@@ -915,9 +915,10 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
   constexpr int VC = sizeof(T) == 2 ? 4 : 2;
   const int G = gridDim.x, tid = threadIdx.x;
   if (X.range == 0) return;
-  __threadfence();                            // publish this CTA's partials before arriving
-  __syncthreads();
-  if (tid < 2) {                              // thread `which` handles one candidate row
+  __syncthreads();                            // the CTA's partial writes precede the arrivals (bar.sync),
+  if (tid < 2) {                              // and the arriving thread's gpu fence is cumulative
+    __threadfence();                          // publish this CTA's partials before arriving
+    // thread `which` handles one candidate row
     const int which = tid;
     s_job[4 * which] = -1;
     const uint32_t r0 = X.row_at(X.p_begin), rl = X.row_at(X.p_end - 1);
