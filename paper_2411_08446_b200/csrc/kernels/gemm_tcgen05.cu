@@ -197,6 +197,7 @@ struct FfnSched {
 struct ArgmaxEpi {
   int16_t* codes;
   int q;
+  int exp = 0;        // experiment (LSHMOE_HASH_EXP): 1 = skip the argmax scan, 2 = skip the MMAs
   uint2* partial;     // [nparts][rows_pad][q] (|y| bits, index | sign << 31) of each slice
   int* counter;       // [slices][q] arrival counters, zero at rest (reset by the last arrival)
   int rows_pad;
@@ -265,6 +266,10 @@ struct ArgmaxEpi {
     codes[static_cast<int64_t>(t) * q + w.tag1] = static_cast<int16_t>((bi >> 31) ? -(idx + 1) : (idx + 1));
   }
   __device__ void consume(const WorkItem&, int /*row*/, const uint32_t (&r)[32], int col0, const uint8_t*) {
+    if (exp == 1) {
+      if (r[0] == 0x7FC00001u && r[31] == 0x7FC00001u) cb[0] = 1.0f;   // keep the TMEM load live
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const float v = __uint_as_float(r[i]);
@@ -414,6 +419,7 @@ template <class Epi>
 __device__ __forceinline__ bool epi_skip_mma(const Epi&) { return false; }
 template <int BN>
 __device__ __forceinline__ bool epi_skip_mma(const BiasActEpi<BN>& e) { return e.exp == 2; }
+__device__ __forceinline__ bool epi_skip_mma(const ArgmaxEpi& e) { return e.exp == 2; }
 
 // ---- the kernel ----------------------------------------------------------------------------------
 // kEB: operand element bytes — 2 = bf16 (kind::f16, 16-element MMA K), 1 = e4m3 (kind::f8f6f4,
@@ -768,6 +774,7 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
   ArgmaxEpi e{};
   e.codes = codes;
   e.q = q;
+  e.exp = cta_mode("LSHMOE_HASH_EXP", 0);
   e.rows_pad = static_cast<int>(((n + 255) / 256) * 256);
   // Slice split (one unit per BN slice of the d coordinates, slices merged by the last arrival)
   // evens out the persistent grid's last wave: C2 86.1 vs 90.2 us per launch, CUDA-graph timing in
@@ -797,6 +804,7 @@ int launch_hash_e4m3(const void* x8, int64_t n, int d, const void* R8, int q, in
   ArgmaxEpi e{};
   e.codes = codes;
   e.q = q;
+  e.exp = cta_mode("LSHMOE_HASH_EXP", 0);
   e.rows_pad = static_cast<int>(((n + 255) / 256) * 256);
   s.split = (d > bn) && ws && cta_mode("LSHMOE_HASH_SPLIT", 1) == 1 ? 1 : 0;
   if (s.split) {

@@ -43,7 +43,23 @@ def main():
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
     codes = torch.empty((cfg.n, cfg.q), dtype=torch.int16, device="cuda")
     flops = 2.0 * cfg.n * cfg.q * cfg.d * cfg.d
+    if what in ("hash8",):
+        R8 = L.rotation_e4m3(cfg.d, cfg.q, rotation_seed(0)).cuda()
+        x8 = L.quantize_e4m3(X)
+        for ex in ("0", "1", "2"):
+            os.environ["LSHMOE_HASH_EXP"] = ex
+            med, mn = timeit(lambda: L.hash_e4m3(x8, R8, codes), flush=flush)
+            print(f"hash_e4m3 exp={ex}: median {med:.1f} us  min {mn:.1f} us  {flops / med / 1e6:.0f} TFLOP/s", flush=True)
+        os.environ.pop("LSHMOE_HASH_EXP")
     if what in ("hash", "all"):
+        for cta in ("1", "2"):
+            for ex in ("1", "2"):
+                os.environ["LSHMOE_HASH_EXP"] = ex
+                os.environ["LSHMOE_HASH_CTA"] = cta
+                med, mn = timeit(lambda: L.hash(X, R, codes), flush=flush)
+                print(f"hash cta={cta} exp={ex} (1: no argmax scan, 2: no MMA): median {med:.1f} us", flush=True)
+        os.environ.pop("LSHMOE_HASH_EXP")
+        os.environ.pop("LSHMOE_HASH_CTA")
         for split in ("1", "2"):
             for cta in ("1", "2"):
                 os.environ["LSHMOE_HASH_SPLIT"] = split
