@@ -1,0 +1,34 @@
+#!/bin/bash
+# Round evidence in one GPU session: full -m gpu suite, smoke, the default bench line (with the
+# CPU baseline), the reference arm, the SP / fp8 variants, C3-C5 lines, the C5 hash-count sweep,
+# the ncu launch list of one step and --set full captures of the step's kernels.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+TAG=${TAG:-final}
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_${TAG}.log 2>&1 || { echo build failed; exit 1; }
+if [ -z "$SKIP_TESTS" ]; then
+  timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/tests_${TAG}.log; cat gpurun_out/tests_${TAG}.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.log 2>&1; echo "smoke rc=$?"
+fi
+nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv -lms 200 > gpurun_out/clocks_${TAG}.csv 2>&1 &
+SMI=$!
+timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench rc=$?"
+kill $SMI 2>/dev/null
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err; echo "ref rc=$?"
+for h in sp cp8; do
+  timeout 600 python bench.py --hash $h --no-cpu-baseline > gpurun_out/bench_${TAG}_$h.json 2> gpurun_out/bench_${TAG}_$h.err; echo "bench $h rc=$?"
+done
+for c in C3 C4 C5; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_${TAG}_$c.json 2> gpurun_out/bench_${TAG}_$c.err; echo "bench $c rc=$?"
+done
+for q in 1 2 3 4 5 6 7 8; do
+  timeout 600 python bench.py --config C5 --q $q --no-cpu-baseline --no-backward --steps 10 > gpurun_out/qsweep_${TAG}_q$q.json 2> gpurun_out/qsweep_${TAG}_q$q.err; echo "q=$q rc=$?"
+done
+if [ -z "$SKIP_NCU" ]; then
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
+     python bench.py --profile --steps 2 --warmup 3 > gpurun_out/ncu_launch_${TAG}.log 2>&1; echo "ncu launches rc=$?"
+  for K in ${KERNELS:-HashSched tile_kernel bucket_kernel centroid_kernel FfnSched restore_kernel}; do
+    timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:$K -s 2 -c 1 \
+       -o gpurun_out/prof_${TAG}_${K} python bench.py --profile --steps 1 --warmup 3 > gpurun_out/ncu_${TAG}_${K}.log 2>&1; echo "ncu $K rc=$?"
+  done
+fi
