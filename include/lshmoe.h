@@ -106,6 +106,18 @@ lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d,
                           const void* rotation, int q, int16_t* codes,
                           void* workspace, size_t workspace_bytes, lshmoe_stream stream);
 
+/* ---- NEXT-2: gate + hash in one projection (reading R29) ---------------
+   One tcgen05 pass over x computes the q cross-polytope codes (as lshmoe_hash) and the gate of
+   Eq. 1-2: scores s = W_g x (bf16 products, fp32 accumulation), the k largest (ties to
+   the smaller expert id), slots in ascending expert id, weights = softmax over the k selected
+   scores.  rotation_gate [q*d + E, d] bf16 = the q rotations followed by the E rows of W_g.
+   Outputs: codes int16 [n, q]; zeta int32 [n, k]; gate_weight float [n, k].  bf16 only; E <= 256
+   (d <= 256: E <= d), k <= 8.  Workspace as lshmoe_hash's.  Scores within 1e-5 (relative) of the
+   k-th/(k+1)-th boundary are near-ties that may resolve differently from exact arithmetic. */
+lshmoe_status lshmoe_gate_hash(const void* x, int64_t n, int d, const void* rotation_gate, int q, int num_experts,
+                               int k, int16_t* codes, int32_t* zeta, float* gate_weight, void* workspace,
+                               size_t workspace_bytes, lshmoe_stream stream);
+
 /* ---- NEXT-2 fp8 option: cross-polytope hash on e4m3 operands (reading R28) ---
    Eq. 3's argmax is invariant to a positive scale of x and, per hash function, of R_j, so both are
    scaled by the largest power of two that keeps their max magnitude <= 448 and rounded to e4m3

@@ -16,6 +16,8 @@ The functions follow Algorithm 1 (App. A "Framework of LSH-MoE") ste
   O2  cp_hash(X, R)                   Eq. 3 cross-polytope hash           [pinned]
   O2" e4m3 quantisation + cp_hash     NEXT-2's fp8 rotation option: codes of the
                                       e4m3-rounded, power-of-two-scaled x and R_j (reading R28) [pinned]
+  O0  gate_topk(X, Wg, k)             the gate of Eq. 1-2 as a linear scorer + top-k
+                                      + softmax; NEXT-2 fuses it into the hash pass     [pinned]
   O2' sp_hash(X, N, q, b)             §4.5 spherical-plane hashing (P:L474-479), SPEC's
                                       sign-bit construction (reading R26)   [pinned]
   O3  group_by_expert(zeta, E)        Alg. 1 L3 "Dispatch X into {X_i}"        [pinned]
@@ -49,7 +51,7 @@ import numpy as np
 __all__ = [
     "GAMMA", "splitmix64_stream", "irwin_hall_gaussian", "rotation_fp64", "rotation",
     "round_to_dtype", "f32_to_bf16_bits", "bf16_bits_to_f64", "to_stored",
-    "cp_hash", "sp_hash", "sp_normals", "e4m3_values", "round_e4m3", "pow2_scale_e4m3",
+    "cp_hash", "sp_hash", "sp_normals", "gate_topk", "e4m3_values", "round_e4m3", "pow2_scale_e4m3",
     "quantize_tokens_e4m3", "quantize_rotation_e4m3", "group_by_expert", "bucketize", "Buckets", "centroids", "expert_ffn",
     "dispatch_sim", "combine_sim", "restore", "moe_dense", "lsh_layer", "lsh_layer_ranks",
     "LayerResult", "ulp_bf16", "grad_compress", "expert_ffn_vjp", "grad_restore", "lsh_layer_backward",
@@ -203,6 +205,28 @@ def cp_hash(X: np.ndarray, R: np.ndarray):
             with np.errstate(invalid="ignore", divide="ignore"):
                 margins[:, j] = np.where(amax > 0, (amax - second) / np.where(amax > 0, amax, 1.0), 0.0)
     return codes, margins
+
+
+# ---------------------------------------------------------------------------------------------
+# O0. The gate (Eq. 1-2: G(x) = TopK(softmax(x W_g)) selects k of the N experts and
+# weights them).  Reading R29 (NEXT-2 "gate + hash in one projection"): scores s = W_g x in exact
+# arithmetic on the stored values; the k largest, ties to the smaller expert id; slots in ascending
+# expert id; weights = softmax over the k selected scores (S:L260 order).  margin = the
+# gap between the k-th and (k+1)-th largest score over max |s| (near-tie if < 1e-5).
+# ---------------------------------------------------------------------------------------------
+def gate_topk(X: np.ndarray, Wg: np.ndarray, k: int):
+    """-> zeta int32 [n, k] (ascending ids), g fp64 [n, k], margin fp64 [n]."""
+    S = np.asarray(X, np.float64) @ np.asarray(Wg, np.float64).T
+    n, E = S.shape
+    order = np.argsort(-S, axis=1, kind="stable")        # equal scores keep the smaller id first
+    top = np.sort(order[:, :k], axis=1)
+    sel = np.take_along_axis(S, top, axis=1)
+    ex = np.exp(sel - sel.max(axis=1, keepdims=True))
+    g = ex / ex.sum(axis=1, keepdims=True)
+    srt = -np.sort(-S, axis=1)
+    scale = np.maximum(np.abs(S).max(axis=1), 1e-300)
+    margin = (srt[:, k - 1] - srt[:, k]) / scale if k < E else np.ones(n)
+    return top.astype(np.int32), g, margin
 
 
 # ---------------------------------------------------------------------------------------------

@@ -41,6 +41,7 @@ _SIGS = {
     "lshmoe_rotation": ([_i32, _i32, _u64, _i32, _vp], _i32),
     "lshmoe_hash_workspace": ([_i64, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
     "lshmoe_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _sz, _vp], _i32),
+    "lshmoe_gate_hash": ([_vp, _i64, _i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp], _i32),
     "lshmoe_rotation_e4m3": ([_i32, _i32, _u64, _vp], _i32),
     "lshmoe_quantize_e4m3": ([_vp, _i64, _i32, _vp, _vp], _i32),
     "lshmoe_hash_e4m3": ([_vp, _i64, _i32, _vp, _i32, _vp, _vp, _sz, _vp], _i32),
@@ -171,6 +172,26 @@ def hash(x: torch.Tensor, R: torch.Tensor, codes: Optional[torch.Tensor] = None,
     _check(_lib.lshmoe_hash(_ptr(x), _dt(x), n, d, _ptr(R), q, _ptr(codes), _ptr(workspace), wsb, _stream(stream)),
            "lshmoe_hash")
     return codes
+
+
+def gate_hash(x: torch.Tensor, RG: torch.Tensor, q: int, num_experts: int, k: int, stream=None):
+    """NEXT-2 (reading R29): (codes [n, q], zeta [n, k], gate_weight [n, k]) in one pass over x.
+    RG [q*d + E, d] = the rotations followed by the gate's E scorer rows (see rotation_gate)."""
+    _require_cuda(x, RG)
+    n, d = x.shape
+    codes = torch.empty((n, q), dtype=torch.int16, device=x.device)
+    zeta = torch.empty((n, k), dtype=torch.int32, device=x.device)
+    gw = torch.empty((n, k), dtype=torch.float32, device=x.device)
+    ws = hash_workspace(n, d, q, x.dtype, x.device)
+    _check(_lib.lshmoe_gate_hash(_ptr(x), n, d, _ptr(RG), q, num_experts, k, _ptr(codes), _ptr(zeta), _ptr(gw),
+                                 _ptr(ws), 0 if ws is None else ws.numel(), _stream(stream)), "lshmoe_gate_hash")
+    return codes, zeta, gw
+
+
+def rotation_gate(R: torch.Tensor, Wg: torch.Tensor) -> torch.Tensor:
+    """[q*d + E, d]: the rotations R [q, d, d] stacked over the gate scorer W_g [E, d] (data movement)."""
+    q, d = R.shape[0], R.shape[2]
+    return torch.cat([R.reshape(q * d, d), Wg.to(R.dtype)], dim=0).contiguous()
 
 
 def rotation_e4m3(d: int, q: int, seed: int) -> torch.Tensor:

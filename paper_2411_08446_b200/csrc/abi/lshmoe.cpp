@@ -105,6 +105,22 @@ lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, c
   return cuda_status(err, "lshmoe_hash");
 }
 
+lshmoe_status lshmoe_gate_hash(const void* x, int64_t n, int d, const void* RG, int q, int E, int k, int16_t* codes,
+                               int32_t* zeta, float* gw, void* workspace, size_t workspace_bytes, lshmoe_stream stream) {
+  lshmoe_status st = check_token_shape(__func__, LSHMOE_BF16, n, d);
+  if (st) return st;
+  REQUIRE(q >= 1 && E >= 1 && k >= 1 && k <= E, LSHMOE_EINVAL, "bad q / E / k (k <= E, S:L228)");
+  REQUIRE(q <= LSHMOE_MAX_Q && k <= 8 && E <= (d < 256 ? d : 256), LSHMOE_EUNSUPPORTED,
+          "gate_hash needs q <= LSHMOE_MAX_Q, k <= 8, E <= min(d, 256)");
+  if (n == 0) return LSHMOE_OK;
+  REQUIRE(x && RG && codes && zeta && gw && aligned16(x) && aligned16(RG), LSHMOE_EINVAL, "NULL or misaligned pointer");
+  const size_t need = hash_workspace_bytes(n, d, q);
+  REQUIRE(workspace_bytes >= need, LSHMOE_EINVAL, "workspace too small (see lshmoe_hash_workspace)");
+  REQUIRE(need == 0 || (workspace && aligned16(workspace)), LSHMOE_EINVAL, "workspace NULL or misaligned");
+  return cuda_status(launch_gate_hash_bf16(x, n, d, RG, q, E, k, codes, zeta, gw, workspace, stream),
+                     "lshmoe_gate_hash");
+}
+
 lshmoe_status lshmoe_rotation_e4m3(int d, int q, uint64_t seed, uint8_t* out) {
   REQUIRE(d >= 1 && q >= 1, LSHMOE_EINVAL, "d < 1 or q < 1");
   REQUIRE(q <= LSHMOE_MAX_Q, LSHMOE_EUNSUPPORTED, "q > LSHMOE_MAX_Q");

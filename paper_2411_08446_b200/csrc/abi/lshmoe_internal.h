@@ -17,6 +17,8 @@ lshmoe_status cuda_status(int cuda_err, const char* what);   // ECUDA with cudaG
 lshmoe_status rotation_host(int d, int q, uint64_t seed, lshmoe_dtype dtype, void* out);
 lshmoe_status rotation_e4m3_host(int d, int q, uint64_t seed, uint8_t* out);
 int launch_quantize_e4m3(const void* x, int64_t n, int d, uint8_t* out, void* stream);
+int launch_gate_hash_bf16(const void* x, int64_t n, int d, const void* RG, int q, int E, int k, int16_t* codes,
+                          int32_t* zeta, float* gw, void* ws, void* stream);
 int launch_hash_e4m3(const void* x8, int64_t n, int d, const void* R8, int q, int16_t* codes, void* ws, void* stream);
 
 // ---- launchers (csrc/kernels/*.cu); all return cudaError_t as int -------------------------

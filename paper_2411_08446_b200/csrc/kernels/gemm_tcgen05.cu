@@ -75,34 +75,40 @@ struct HashSched {
   int n, q, d, bn, bm;
   int prefetch_b;   // 0: the rotations are L2-resident
   int m_tiles;
+  int gate;         // NEXT-2: 1 = one extra unit per token tile for the gate scores (B rows q*d ..)
   __device__ void init(void*) {}
   int split;   // 1: one unit per BN slice; 0: one unit covers all d / BN slices (no merge)
-  __device__ int units() const { return m_tiles * q * (split ? d / bn : 1); }
+  __device__ int units() const { return m_tiles * (q * (split ? d / bn : 1) + gate); }
   __device__ WorkItem get(int u, int rank) const {
     WorkItem w;
-    if (!split) {
-      const int mt = u / q, j = u - mt * q;
-      w.a_row = mt * bm + rank * BM;
-      w.b_row0 = j * d;
-      w.nchunks = d / bn;
-      w.valid_rows = min(BM, n - w.a_row);
-      w.tag0 = (mt * (bm / BM) + rank) * q + j;
-      w.tag1 = j;
+    const int np = split ? d / bn : 1;
+    const int upt = q * np + gate;             // units per token tile: slices fastest, then j, then the gate
+    const int mt = u / upt, r = u - mt * upt;
+    w.a_row = mt * bm + rank * BM;
+    w.valid_rows = min(BM, n - w.a_row);
+    if (r == q * np) {                         // the gate unit: scores of the E experts (<= BN columns)
+      w.b_row0 = q * d;
+      w.nchunks = 1;
+      w.tag0 = -1;
+      w.tag1 = q;
       w.part = 0;
       w.nparts = 1;
       return w;
     }
-    const int np = d / bn;
-    const int c = u % np, rest = u / np;       // slice fastest, then j: one token tile at a time
-    const int j = rest % q, mt = rest / q;
-    w.a_row = mt * bm + rank * BM;
-    w.b_row0 = j * d + c * bn;
-    w.nchunks = 1;
-    w.valid_rows = min(BM, n - w.a_row);
+    const int j = r / np, c = r - j * np;
     w.tag0 = (mt * (bm / BM) + rank) * q + j;   // this CTA's 128-token slice x hash j
     w.tag1 = j;
-    w.part = c;
-    w.nparts = np;
+    if (!split) {
+      w.b_row0 = j * d;
+      w.nchunks = d / bn;
+      w.part = 0;
+      w.nparts = 1;
+    } else {
+      w.b_row0 = j * d + c * bn;
+      w.nchunks = 1;
+      w.part = c;
+      w.nparts = np;
+    }
     return w;
   }
 };
@@ -194,9 +200,18 @@ struct FfnSched {
 };
 
 // ---- epilogues -------------------------------------------------------------------------------
+constexpr int kMaxGateK = 8;
+
 struct ArgmaxEpi {
   int16_t* codes;
   int q;
+  // NEXT-2 gate (reading R29), active on units with tag1 == q when zeta != nullptr: the thread
+  // keeps its row's top-k (score, expert) over the columns < E of its half, ties to the smaller id.
+  int32_t* zeta = nullptr;    // [n, k] ascending expert ids
+  float* gw = nullptr;        // [n, k] softmax over the k selected scores
+  int E = 0, k = 0;
+  float gs[kMaxGateK];
+  int gi[kMaxGateK];
   int exp = 0;        // experiment (LSHMOE_HASH_EXP): 1 = skip the argmax scan, 2 = skip the MMAs
   uint2* partial;     // [nparts][rows_pad][q] (|y| bits, index | sign << 31) of each slice
   int* counter;       // [slices][q] arrival counters, zero at rest (reset by the last arrival)
@@ -214,6 +229,32 @@ struct ArgmaxEpi {
     for (int k = 0; k < 4; ++k) {
       cb[k] = -1.0f;
       ci[k] = 0;
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxGateK; ++i) {
+      gs[i] = -INFINITY;
+      gi[i] = 0x7FFFFFFF;
+    }
+  }
+  // insert (s, id) into the descending top list (ids arrive ascending, so a tie never displaces)
+  __device__ void gate_insert(float sc, int id) {
+    if (!(sc > gs[k - 1])) return;
+#pragma unroll
+    for (int i = kMaxGateK - 1; i > 0; --i) {
+      if (i >= k) continue;
+      const bool shift = sc > gs[i - 1];
+      const bool here = !shift && sc > gs[i];
+      if (shift) {
+        gs[i] = gs[i - 1];
+        gi[i] = gi[i - 1];
+      } else if (here) {
+        gs[i] = sc;
+        gi[i] = id;
+      }
+    }
+    if (sc > gs[0]) {
+      gs[0] = sc;
+      gi[0] = id;
     }
   }
   __device__ void merge_chains() {
@@ -265,7 +306,13 @@ struct ArgmaxEpi {
     const int idx = static_cast<int>(bi & 0x7FFFFFFFu);
     codes[static_cast<int64_t>(t) * q + w.tag1] = static_cast<int16_t>((bi >> 31) ? -(idx + 1) : (idx + 1));
   }
-  __device__ void consume(const WorkItem&, int /*row*/, const uint32_t (&r)[32], int col0, const uint8_t*) {
+  __device__ void consume(const WorkItem& w, int /*row*/, const uint32_t (&r)[32], int col0, const uint8_t*) {
+    if (zeta && w.tag1 == q) {
+#pragma unroll 1
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < E) gate_insert(__uint_as_float(r[i]), col0 + i);
+      return;
+    }
     if (exp == 1) {
       if (r[0] == 0x7FC00001u && r[31] == 0x7FC00001u) cb[0] = 1.0f;   // keep the TMEM load live
       return;
@@ -283,7 +330,57 @@ struct ArgmaxEpi {
     }
   }
   // half: which half of the unit's columns this thread scanned (8 epilogue warps) or 0.
+  // Gate unit: the two column halves' lists meet in shared memory, the merged top-k is written in
+  // ascending expert id with softmax weights.
+  __device__ void finish_gate(const WorkItem& w, int row, uint8_t* scratch, int half, int nthr) {
+    float* ls = reinterpret_cast<float*>(scratch);                 // [128][kMaxGateK]
+    int* li = reinterpret_cast<int*>(scratch + 128 * kMaxGateK * 4);
+    if (half == 1)
+#pragma unroll
+      for (int i = 0; i < kMaxGateK; ++i) {
+        ls[row * kMaxGateK + i] = gs[i];
+        li[row * kMaxGateK + i] = gi[i];
+      }
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    if (half == 0 && row < w.valid_rows) {
+      for (int i = 0; i < k; ++i) {          // the other half's ids are all larger: insert keeps order
+        const float sc = ls[row * kMaxGateK + i];
+        const int id = li[row * kMaxGateK + i];
+        if (id != 0x7FFFFFFF) gate_insert(sc, id);
+      }
+      // ascending expert id, then softmax over the selected scores
+      int ids[kMaxGateK];
+      float scs[kMaxGateK];
+#pragma unroll
+      for (int i = 0; i < kMaxGateK; ++i) {
+        ids[i] = gi[i];
+        scs[i] = gs[i];
+      }
+      for (int a = 1; a < k; ++a)
+        for (int b = a; b > 0 && ids[b] < ids[b - 1]; --b) {
+          const int ti = ids[b]; ids[b] = ids[b - 1]; ids[b - 1] = ti;
+          const float tf = scs[b]; scs[b] = scs[b - 1]; scs[b - 1] = tf;
+        }
+      float mx = scs[0];
+      for (int i = 1; i < k; ++i) mx = fmaxf(mx, scs[i]);
+      float ex[kMaxGateK], sum = 0.0f;
+      for (int i = 0; i < k; ++i) {
+        ex[i] = expf(scs[i] - mx);
+        sum += ex[i];
+      }
+      const int64_t t = w.a_row + row;
+      for (int i = 0; i < k; ++i) {
+        zeta[t * k + i] = ids[i];
+        gw[t * k + i] = ex[i] / sum;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+  }
   __device__ void finish(const WorkItem& w, int row, uint8_t* scratch, int half, int nthr) {
+    if (zeta && w.tag1 == q) {
+      finish_gate(w, row, scratch, half, nthr);
+      return;
+    }
     merge_chains();
     if (nthr > 128) {   // combine the two column halves of each row; the lower half wins ties
       uint2* mb = reinterpret_cast<uint2*>(scratch + 64);
@@ -787,6 +884,37 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
   }
   return launch_bn(bn, cta, x, n, R, static_cast<int64_t>(q) * d, d, s, e, s.m_tiles * q * (s.split ? d / bn : 1),
                    static_cast<cudaStream_t>(stream));
+}
+
+// NEXT-2 gate + hash in one pass over x (reading R29): B = [R ; W_g] ([q*d + E, d]); per token
+// tile one extra unit scores the E experts (one BN-wide chunk; rows past q*d + E read as zeros by
+// TMA) and its epilogue writes the top-k experts and softmax weights instead of a code.
+int launch_gate_hash_bf16(const void* x, int64_t n, int d, const void* RG, int q, int E, int k, int16_t* codes,
+                          int32_t* zeta, float* gw, void* ws, void* stream) {
+  const int bn = pick_bn(d);
+  if (E > bn || k > kMaxGateK || k > E) return cudaErrorInvalidValue;
+  HashSched s{};
+  s.n = static_cast<int>(n);
+  s.q = q;
+  s.d = d;
+  s.gate = 1;
+  s.m_tiles = static_cast<int>((n + BM - 1) / BM);
+  ArgmaxEpi e{};
+  e.codes = codes;
+  e.q = q;
+  e.zeta = zeta;
+  e.gw = gw;
+  e.E = E;
+  e.k = k;
+  e.rows_pad = static_cast<int>(((n + 255) / 256) * 256);
+  s.split = (d > bn) && ws ? 1 : 0;
+  if (s.split) {
+    const size_t counters = ((sizeof(int) * (e.rows_pad / BM) * q) + 255) & ~size_t(255);
+    e.counter = static_cast<int*>(ws);
+    e.partial = reinterpret_cast<uint2*>(static_cast<uint8_t*>(ws) + counters);
+  }
+  return launch_bn(bn, 1, x, n, RG, static_cast<int64_t>(q) * d + E, d, s, e,
+                   s.m_tiles * (q * (s.split ? d / bn : 1) + 1), static_cast<cudaStream_t>(stream));
 }
 
 // NEXT-2 fp8 option (reading R28): the same hash kernel on e4m3 operands (x8 [n, d] from
