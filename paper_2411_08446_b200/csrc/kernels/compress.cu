@@ -273,22 +273,26 @@ __device__ __forceinline__ void cluster_barrier() {
 // Ordered gather of positions [s0, s1) of expert e's copy list (and their slots) from the tiles'
 // runs into mem[i - s0], aux[i - s0].
 __device__ void gather_group(const Params& P, int e, int s0, int s1, int32_t* mem, int32_t* aux, int* s_tb, int* s_ta,
-                             int* s_scan) {
+                             int* s_scan, int staged_total) {   // staged_total >= 0: single chunk pre-staged
   const int tid = threadIdx.x;
   const int E1 = P.E + 1;
   int base = 0;
   for (int t0 = 0; t0 < P.ntiles && base < s1; t0 += kBThreads) {
-    const int t = t0 + tid;
-    int a = 0, cnt = 0;
-    if (t < P.ntiles) {
-      a = ldcg(P.tile_off + static_cast<int64_t>(t) * E1 + e);
-      cnt = ldcg(P.tile_off + static_cast<int64_t>(t) * E1 + e + 1) - a;
-    }
     int tot;
-    const int excl = block_excl_scan<kBWarps>(cnt, s_scan, &tot);
-    s_tb[tid] = excl;
-    s_ta[tid] = a;
-    __syncthreads();
+    if (staged_total >= 0) {               // the caller's sizing scan already staged this chunk
+      tot = staged_total;
+    } else {
+      const int t = t0 + tid;
+      int a = 0, cnt = 0;
+      if (t < P.ntiles) {
+        a = ldcg(P.tile_off + static_cast<int64_t>(t) * E1 + e);
+        cnt = ldcg(P.tile_off + static_cast<int64_t>(t) * E1 + e + 1) - a;
+      }
+      const int excl = block_excl_scan<kBWarps>(cnt, s_scan, &tot);
+      s_tb[tid] = excl;
+      s_ta[tid] = a;
+      __syncthreads();
+    }
     const int nt = min(kBThreads, P.ntiles - t0);
     dstamp(P, 1, 7);
     // this chunk's positions [base, base + tot) intersected with [s0, s1); thread owns entries
@@ -346,6 +350,7 @@ __global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
   dstamp(P, 1, 0);
   // group size and offset: one column of the tile offsets
   int n_e, goff;
+  const bool staged = P.ntiles <= kBThreads;   // one chunk of tiles: the sizing scan stages the runs
   {
     int cnt = 0, a = 0;
     for (int t = tid; t < P.ntiles; t += kBThreads) {
@@ -353,7 +358,11 @@ __global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
       cnt += ldcg(P.tile_off + static_cast<int64_t>(t) * E1 + e + 1) - x0;
       a += x0;
     }
-    block_excl_scan<kBWarps>(cnt, s_scan, &n_e);
+    const int excl = block_excl_scan<kBWarps>(cnt, s_scan, &n_e);
+    if (staged) {                          // tile t's run of expert e: [s_ta[t], +cnt) at member s_tb[t]
+      s_tb[tid] = excl;
+      s_ta[tid] = a;
+    }
     block_excl_scan<kBWarps>(a, s_scan, &goff);   // copies of experts < e = the group's perm offset
   }
   dstamp(P, 1, 6);
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
     aux = P.big + 1 * static_cast<int64_t>(CS) * P.nk + wbase;
     row = P.big + 2 * static_cast<int64_t>(CS) * P.nk + wbase;
   }
-  gather_group(P, e, s0, s1, mem, aux, s_tb, s_ta, s_scan);
+  gather_group(P, e, s0, s1, mem, aux, s_tb, s_ta, s_scan, staged ? n_e : -1);
   dstamp(P, 1, 1);
   if (tid == 0 && r == 0) P.gofs[e] = goff;
   if (P.permute) {                        // baseline: slot = group offset + rank in the group
