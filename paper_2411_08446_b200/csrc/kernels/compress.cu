@@ -266,8 +266,13 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(Params P) {
 // (barrier.cluster release/acquire orders the global writes of the cluster's CTAs).
 extern __shared__ __align__(1024) uint8_t g_dsmem[];
 
+// Cluster barrier publishing this CTA's global writes: bar.sync orders them before thread 0's
+// gpu-scope fence (cumulative), whose relaxed arrive + the peers' acquiring wait form the release /
+// acquire pair — one MEMBAR per CTA instead of a release arrive (MEMBAR.GPU) in every thread.
 __device__ __forceinline__ void cluster_barrier() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence();
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // Ordered gather of positions [s0, s1) of expert e's copy list (and their slots) from the tiles'
@@ -539,8 +544,7 @@ __global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
     P.rowl[pos] = q;
   }
   if (tid == 0 && r == 0) P.expert_rows[e] = m_e;
-  dstamp(P, 1, 5);
-  cluster_barrier();                       // no CTA leaves while a peer may still read its totals
+  dstamp(P, 1, 5);                         // (the exchanges go through global memory: no exit barrier)
 }
 
 // ---- centroid phase ------------------------------------------------------------------------
