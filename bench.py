@@ -236,7 +236,7 @@ def main():
     nk = n * k
     codes = torch.empty((n, cfg.q), dtype=torch.int16, device=dev)
     comp = L.alloc_compressed(n, k, cfg.E, d, X.dtype, dev)
-    ws = torch.empty(L.compress_workspace_bytes(n, k, cfg.E, cfg.q, d, X.dtype), dtype=torch.uint8, device=dev)
+    ws = torch.full((L.compress_workspace_bytes(n, k, cfg.E, cfg.q, d, X.dtype),), 255, dtype=torch.uint8, device=dev)
     cap = nk * world
     recv = comp.centroids if world == 1 else torch.empty((cap, d), dtype=X.dtype, device=dev)
     # world 1: recv aliases the centroids and recv_rows [E, 1] aliases expert_rows (no copies)
@@ -486,7 +486,7 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
         Hb = torch.empty((cap, d), dtype=X.dtype, device=dev)
         dhid = torch.empty((cap, cfg.d_ffn), dtype=X.dtype, device=dev)
         dxb = torch.empty_like(X)
-        gws = torch.empty(1 << 22, dtype=torch.uint8, device=dev)
+        gws = torch.full((1 << 22,), 255, dtype=torch.uint8, device=dev)
         W2T = W2.transpose(1, 2).contiguous()
         W1T = W1.transpose(1, 2).contiguous()
         parts = {"grad_compress": lambda: L.grad_compress(dY, comp, out=Gb, workspace=gws),

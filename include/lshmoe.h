@@ -147,7 +147,10 @@ lshmoe_status lshmoe_sp_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d
                              int16_t* codes, lshmoe_stream stream);
 
 /* ---- a3-a5: group by expert, bucketize, centroid means -------------------------------------
-   Bytes of device workspace lshmoe_compress needs for these sizes. */
+   Bytes of device workspace lshmoe_compress needs for these sizes.  The workspace must be filled
+   with 0xFF bytes once before its first use (e.g. cudaMemset(ws, 0xFF, bytes)); every call leaves
+   its hash table and arrival counters back in that state, so no per-call clearing is launched.
+   It must not be shared by calls in flight on different streams. */
 lshmoe_status lshmoe_compress_workspace(int64_t n, int k, int num_experts, int q, int d,
                                         lshmoe_dtype dtype, size_t* bytes /* [host] out */);
 
@@ -244,7 +247,8 @@ lshmoe_status lshmoe_restore(const void* x, const void* centroids, const void* r
                            dg_ts = dY_t . (o_b + x_t - c~_b)
    bucket / perm / row_start are lshmoe_compress's outputs of the same forward.  Summation order of
    G is the forward's perm order (fp32 accumulation, one rounding to dtype; grad_out_f32 nullable
-   keeps the fp32 sums).  Workspace: lshmoe_grad_compress_workspace(d) bytes, any contents. */
+   keeps the fp32 sums).  Workspace: lshmoe_grad_compress_workspace(d) bytes, filled with 0xFF once
+   before first use and left so by every call (arrival counters of rows cut by CTA ranges). */
 /* The expert's backward for the dX path (H = J_E(c~)^T G for E(c) = W2 relu(W1 c + b1) + b2,
    weight gradients not computed): dh = (G W2) * [h > 0], H = dh W1, as two grouped GEMMs over the
    same recv_rows segments as lshmoe_expert_ffn.  W2T [E_local, d_ffn, d] = W2^T and W1T

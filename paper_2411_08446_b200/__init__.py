@@ -337,6 +337,21 @@ def compress_workspace_bytes(n: int, k: int, E: int, q: int, d: int, dtype: torc
     return b.value
 
 
+_COMPRESS_WS = {}
+
+
+def compress_workspace(n: int, k: int, E: int, q: int, d: int, dtype: torch.dtype, device) -> torch.Tensor:
+    """A compress workspace at rest (0xFF-filled, as lshmoe_compress requires before first use),
+    cached per device and size.  Calls leave it at rest; do not share it across concurrent streams."""
+    nbytes = max(compress_workspace_bytes(n, k, E, q, d, dtype), 16)
+    key = (str(device), nbytes)
+    ws = _COMPRESS_WS.get(key)
+    if ws is None:
+        ws = torch.full((nbytes,), 255, dtype=torch.uint8, device=device)
+        _COMPRESS_WS[key] = ws
+    return ws
+
+
 def alloc_compressed(n: int, k: int, E: int, d: int, dtype: torch.dtype, device, with_f32: bool = False) -> Compressed:
     nk = n * k
     i32 = dict(dtype=torch.int32, device=device)
@@ -358,7 +373,7 @@ def compress(x: torch.Tensor, codes: torch.Tensor, experts: torch.Tensor, num_ex
         out = alloc_compressed(n, k, num_experts, d, x.dtype, x.device, with_f32)
     wsb = compress_workspace_bytes(n, k, num_experts, q, d, x.dtype)
     if workspace is None or workspace.numel() < wsb:
-        workspace = torch.empty(max(wsb, 16), dtype=torch.uint8, device=x.device)
+        workspace = compress_workspace(n, k, num_experts, q, d, x.dtype, x.device)
     _check(_lib.lshmoe_compress(_ptr(x), _dt(x), n, d, _ptr(codes), q, _ptr(experts), k, num_experts,
                                 _ptr(out.bucket), _ptr(out.perm), _ptr(out.row_start), _ptr(out.expert_rows),
                                 _ptr(out.num_rows), _ptr(out.centroids), _ptr(out.centroids_f32),
@@ -379,7 +394,11 @@ def grad_compress(dy: torch.Tensor, comp: "Compressed", gate_weight: Optional[to
     b = ctypes.c_size_t(0)
     _check(_lib.lshmoe_grad_compress_workspace(d, ctypes.byref(b)), "lshmoe_grad_compress_workspace")
     if workspace is None or workspace.numel() < b.value:
-        workspace = torch.empty(b.value, dtype=torch.uint8, device=dy.device)
+        key = (str(dy.device), "grad", b.value)
+        workspace = _COMPRESS_WS.get(key)
+        if workspace is None:
+            workspace = torch.full((b.value,), 255, dtype=torch.uint8, device=dy.device)   # at rest
+            _COMPRESS_WS[key] = workspace
     _check(_lib.lshmoe_grad_compress(_ptr(dy), _dt(dy), n, d, _ptr(gate_weight), _ptr(comp.bucket), _ptr(comp.perm),
                                      _ptr(comp.row_start), k, _ptr(out), _ptr(out_f32), _ptr(workspace),
                                      workspace.numel(), _stream(stream)), "lshmoe_grad_compress")

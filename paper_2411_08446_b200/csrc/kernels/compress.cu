@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(Params P) {
   const unsigned lt = (1u << lane) - 1u;
   const int E1 = P.E + 1;
   const int t = blockIdx.x;
+  pdl_wait();                                // the hash kernel's codes (and every earlier write) are visible
   dstamp(P, 0, 0);
   const int c = t * kTile + tid;
   const bool ok = c < P.nk;
@@ -946,6 +947,7 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
       const int old = atomicAdd(reinterpret_cast<int*>(P.bar) + kArrive + b0, 1);   // counters start at -1
       if (old + 2 == expected) {
         __threadfence();                      // acquire the other CTAs' partials
+        reinterpret_cast<int*>(P.bar)[kArrive + b0] = -1;   // leave the counter at rest for the next call
         s_job[4 * which + 0] = static_cast<int>(which == 0 ? r0 : rl);
         s_job[4 * which + 1] = rs;
         s_job[4 * which + 2] = re;
@@ -1013,6 +1015,9 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   const int tid = threadIdx.x;
   pdl_wait();                                // K2's perm, rows and counts are complete
   dstamp(P, 2, 0);
+  if (!P.permute)                             // K2 was the table's last reader: leave it at rest (-1)
+    for (int64_t i = blockIdx.x * int64_t(kThreads) + tid; i <= P.mask; i += int64_t(gridDim.x) * kThreads)
+      P.table[i] = -1;
   if (P.permute) {
     if (P.is_bf16) gather_rows<__nv_bfloat16>(P);
     else gather_rows<float>(P);
@@ -1179,7 +1184,7 @@ int launch_chain(const Params& P, cudaStream_t st) {
   p.dyn_smem = kBucketSmem;
   p.diag = diag_enabled() ? 1 : 0;
   p.cs = bucket_cluster_size(P.E);
-  int err = launch_pdl(tile_kernel, P.ntiles, kThreads, 0, st, p, false);
+  int err = launch_pdl(tile_kernel, P.ntiles, kThreads, 0, st, p, true);
   if (!err) err = launch_pdl(bucket_kernel, P.E * p.cs, kBThreads, kBucketSmem, st, p, true, p.cs);
   if (!err) err = launch_pdl(centroid_kernel, centroid_grid(), kThreads, P.permute ? 0 : csmem, st, p, true);
   return err;
@@ -1319,8 +1324,9 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
     if ((err = cudaMemsetAsync(num_rows, 0, sizeof(int32_t), st))) return err;
     return cudaMemsetAsync(row_start, 0, sizeof(int32_t), st);
   }
-  // header (arrival counters, stamps: -1) and hash table slots (-1) in one memset
-  if ((err = cudaMemsetAsync(ws.hdr, 0xFF, sizeof(int32_t) * (kHdr + ws.table_size), st))) return err;
+  // The workspace is at rest between calls (hash table slots and arrival counters -1: K3 resets
+  // the table, the last arriver its counter); the diagnostics stamps are cleared only when on.
+  if (diag_enabled() && (err = cudaMemsetAsync(ws.hdr, 0xFF, sizeof(int32_t) * kHdr, st))) return err;
   Params P = base_params(x, dtype, n, d, experts, k, E, ws);
   P.codes = codes;
   P.q = q;
@@ -1369,8 +1375,7 @@ int launch_grad_compress(const void* dy, lshmoe_dtype dtype, int64_t n, int d, c
   int32_t* hdr;
   float* partial;
   grad_compress_workspace_layout(d, ws, &hdr, &partial);
-  int err = cudaMemsetAsync(hdr, 0xFF, sizeof(int32_t) * kHdr, st);   // arrival counters at -1
-  if (err) return err;
+  int err = 0;                                 // arrival counters are at rest (-1) between calls
   Params P{};
   P.x = static_cast<const uint8_t*>(dy);
   P.d = d;

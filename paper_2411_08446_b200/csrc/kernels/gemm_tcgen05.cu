@@ -202,7 +202,9 @@ struct FfnSched {
 // ---- epilogues -------------------------------------------------------------------------------
 constexpr int kMaxGateK = 8;
 
-struct ArgmaxEpi {
+// kGate: the NEXT-2 gate+hash variant (compiled separately so the plain hash keeps its registers).
+template <bool kGate>
+struct ArgmaxEpiT {
   int16_t* codes;
   int q;
   // NEXT-2 gate (reading R29), active on units with tag1 == q when zeta != nullptr: the thread
@@ -224,7 +226,7 @@ struct ArgmaxEpi {
   float best;
   int bidx;
   bool bneg;
-  __device__ void begin(const WorkItem&, uint8_t*) {
+  __device__ __forceinline__ void begin(const WorkItem&, uint8_t*) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       cb[k] = -1.0f;
@@ -236,12 +238,13 @@ struct ArgmaxEpi {
       gi[i] = 0x7FFFFFFF;
     }
   }
-  // insert (s, id) into the descending top list (ids arrive ascending, so a tie never displaces)
-  __device__ void gate_insert(float sc, int id) {
-    if (!(sc > gs[k - 1])) return;
+  // insert (s, id) into the descending top-kMaxGateK list (ids arrive ascending, so a tie never
+  // displaces); the first k entries are the top-k.  Every index is a compile-time constant so the
+  // lists stay in registers.
+  __device__ __forceinline__ void gate_insert(float sc, int id) {
+    if (!(sc > gs[kMaxGateK - 1])) return;
 #pragma unroll
     for (int i = kMaxGateK - 1; i > 0; --i) {
-      if (i >= k) continue;
       const bool shift = sc > gs[i - 1];
       const bool here = !shift && sc > gs[i];
       if (shift) {
@@ -257,7 +260,7 @@ struct ArgmaxEpi {
       gi[0] = id;
     }
   }
-  __device__ void merge_chains() {
+  __device__ __forceinline__ void merge_chains() {
     best = cb[0];
     bidx = ci[0];
 #pragma unroll
@@ -274,7 +277,7 @@ struct ArgmaxEpi {
   // Slice merge: every slice stores its per-row winner; the last slice of (tile, j) to arrive
   // merges the nparts winners in slice order (strict '>': an earlier slice keeps ties, so the
   // result equals one ascending scan over all d coordinates) and writes the code.
-  __device__ void finish_split(const WorkItem& w, int row, uint8_t* shared_flag, int half, int nthr) {
+  __device__ __forceinline__ void finish_split(const WorkItem& w, int row, uint8_t* shared_flag, int half, int nthr) {
     const int t = w.a_row + row;
     if (half == 0 && t >= 0 && t < rows_pad)
       partial[(static_cast<int64_t>(w.part) * rows_pad + t) * q + w.tag1] =
@@ -306,12 +309,14 @@ struct ArgmaxEpi {
     const int idx = static_cast<int>(bi & 0x7FFFFFFFu);
     codes[static_cast<int64_t>(t) * q + w.tag1] = static_cast<int16_t>((bi >> 31) ? -(idx + 1) : (idx + 1));
   }
-  __device__ void consume(const WorkItem& w, int /*row*/, const uint32_t (&r)[32], int col0, const uint8_t*) {
-    if (zeta && w.tag1 == q) {
-#pragma unroll 1
-      for (int i = 0; i < 32; ++i)
-        if (col0 + i < E) gate_insert(__uint_as_float(r[i]), col0 + i);
-      return;
+  __device__ __forceinline__ void consume(const WorkItem& w, int /*row*/, const uint32_t (&r)[32], int col0, const uint8_t*) {
+    if constexpr (kGate) {
+      if (w.tag1 == q) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < E) gate_insert(__uint_as_float(r[i]), col0 + i);
+        return;
+      }
     }
     if (exp == 1) {
       if (r[0] == 0x7FC00001u && r[31] == 0x7FC00001u) cb[0] = 1.0f;   // keep the TMEM load live
@@ -332,7 +337,7 @@ struct ArgmaxEpi {
   // half: which half of the unit's columns this thread scanned (8 epilogue warps) or 0.
   // Gate unit: the two column halves' lists meet in shared memory, the merged top-k is written in
   // ascending expert id with softmax weights.
-  __device__ void finish_gate(const WorkItem& w, int row, uint8_t* scratch, int half, int nthr) {
+  __device__ __forceinline__ void finish_gate(const WorkItem& w, int row, uint8_t* scratch, int half, int nthr) {
     float* ls = reinterpret_cast<float*>(scratch);                 // [128][kMaxGateK]
     int* li = reinterpret_cast<int*>(scratch + 128 * kMaxGateK * 4);
     if (half == 1)
@@ -343,43 +348,53 @@ struct ArgmaxEpi {
       }
     asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
     if (half == 0 && row < w.valid_rows) {
-      for (int i = 0; i < k; ++i) {          // the other half's ids are all larger: insert keeps order
+      // (every loop below has a compile-time trip count: the arrays stay in registers)
+#pragma unroll
+      for (int i = 0; i < kMaxGateK; ++i) {  // the other half's ids are all larger: insert keeps order
         const float sc = ls[row * kMaxGateK + i];
         const int id = li[row * kMaxGateK + i];
         if (id != 0x7FFFFFFF) gate_insert(sc, id);
       }
-      // ascending expert id, then softmax over the selected scores
       int ids[kMaxGateK];
       float scs[kMaxGateK];
 #pragma unroll
       for (int i = 0; i < kMaxGateK; ++i) {
-        ids[i] = gi[i];
+        ids[i] = i < k ? gi[i] : 0x7FFFFFFF;
         scs[i] = gs[i];
       }
-      for (int a = 1; a < k; ++a)
-        for (int b = a; b > 0 && ids[b] < ids[b - 1]; --b) {
-          const int ti = ids[b]; ids[b] = ids[b - 1]; ids[b - 1] = ti;
-          const float tf = scs[b]; scs[b] = scs[b - 1]; scs[b - 1] = tf;
-        }
-      float mx = scs[0];
-      for (int i = 1; i < k; ++i) mx = fmaxf(mx, scs[i]);
-      float ex[kMaxGateK], sum = 0.0f;
-      for (int i = 0; i < k; ++i) {
-        ex[i] = expf(scs[i] - mx);
+#pragma unroll
+      for (int pass = 0; pass < kMaxGateK - 1; ++pass)   // ascending expert id (odd-even network)
+#pragma unroll
+        for (int j = pass & 1; j + 1 < kMaxGateK; j += 2)
+          if (ids[j] > ids[j + 1]) {
+            const int ti = ids[j]; ids[j] = ids[j + 1]; ids[j + 1] = ti;
+            const float tf = scs[j]; scs[j] = scs[j + 1]; scs[j + 1] = tf;
+          }
+      float mx = -INFINITY, ex[kMaxGateK], sum = 0.0f;
+#pragma unroll
+      for (int i = 0; i < kMaxGateK; ++i)
+        if (i < k) mx = fmaxf(mx, scs[i]);
+#pragma unroll
+      for (int i = 0; i < kMaxGateK; ++i) {
+        ex[i] = i < k ? expf(scs[i] - mx) : 0.0f;
         sum += ex[i];
       }
       const int64_t t = w.a_row + row;
-      for (int i = 0; i < k; ++i) {
-        zeta[t * k + i] = ids[i];
-        gw[t * k + i] = ex[i] / sum;
-      }
+#pragma unroll
+      for (int i = 0; i < kMaxGateK; ++i)
+        if (i < k) {
+          zeta[t * k + i] = ids[i];
+          gw[t * k + i] = ex[i] / sum;
+        }
     }
     asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
   }
-  __device__ void finish(const WorkItem& w, int row, uint8_t* scratch, int half, int nthr) {
-    if (zeta && w.tag1 == q) {
-      finish_gate(w, row, scratch, half, nthr);
-      return;
+  __device__ __forceinline__ void finish(const WorkItem& w, int row, uint8_t* scratch, int half, int nthr) {
+    if constexpr (kGate) {
+      if (w.tag1 == q) {
+        finish_gate(w, row, scratch, half, nthr);
+        return;
+      }
     }
     merge_chains();
     if (nthr > 128) {   // combine the two column halves of each row; the lower half wins ties
@@ -406,6 +421,9 @@ struct ArgmaxEpi {
     }
   }
 };
+
+using ArgmaxEpi = ArgmaxEpiT<false>;
+using GateArgmaxEpi = ArgmaxEpiT<true>;
 
 // SignBitsEpi — NEXT-3, spherical-plane hashing (§4.5; SPEC's sign-bit reading
 // S:L124-132, reading R26): Y = X N^T with the q*b unit normals as B rows (one BN-wide unit holds
@@ -516,7 +534,8 @@ template <class Epi>
 __device__ __forceinline__ bool epi_skip_mma(const Epi&) { return false; }
 template <int BN>
 __device__ __forceinline__ bool epi_skip_mma(const BiasActEpi<BN>& e) { return e.exp == 2; }
-__device__ __forceinline__ bool epi_skip_mma(const ArgmaxEpi& e) { return e.exp == 2; }
+template <bool G>
+__device__ __forceinline__ bool epi_skip_mma(const ArgmaxEpiT<G>& e) { return e.exp == 2; }
 
 // ---- the kernel ----------------------------------------------------------------------------------
 // kEB: operand element bytes — 2 = bf16 (kind::f16, 16-element MMA K), 1 = e4m3 (kind::f8f6f4,
@@ -899,7 +918,7 @@ int launch_gate_hash_bf16(const void* x, int64_t n, int d, const void* RG, int q
   s.d = d;
   s.gate = 1;
   s.m_tiles = static_cast<int>((n + BM - 1) / BM);
-  ArgmaxEpi e{};
+  GateArgmaxEpi e{};
   e.codes = codes;
   e.q = q;
   e.zeta = zeta;

@@ -78,7 +78,7 @@ def main():
         med, mn = timeit(lambda: torch.matmul(A, A), flush=flush)
         print(f"cuBLAS 8192^3: median {med:.1f} us  {2 * 8192 ** 3 / med / 1e6:.0f} TFLOP/s", flush=True)
     if what in ("compress", "all"):
-        ws = torch.empty(L.compress_workspace_bytes(cfg.n, cfg.k, cfg.E, cfg.q, cfg.d, X.dtype), dtype=torch.uint8,
+        ws = torch.full((L.compress_workspace_bytes(cfg.n, cfg.k, cfg.E, cfg.q, cfg.d, X.dtype),), 255, dtype=torch.uint8,
                          device="cuda")
         L.hash(X, R, codes)
         comp = L.alloc_compressed(cfg.n, cfg.k, cfg.E, cfg.d, X.dtype, "cuda")

@@ -17,7 +17,7 @@ Xd, zd = X.cuda(), zeta.cuda()
 R = L.rotation(cfg.d, cfg.q, rotation_seed(0), X.dtype).cuda()
 codes = L.hash(Xd, R)
 nk = cfg.n * cfg.k
-ws = torch.empty(L.compress_workspace_bytes(cfg.n, cfg.k, cfg.E, cfg.q, cfg.d, X.dtype), dtype=torch.uint8, device="cuda")
+ws = torch.full((L.compress_workspace_bytes(cfg.n, cfg.k, cfg.E, cfg.q, cfg.d, X.dtype),), 255, dtype=torch.uint8, device="cuda")
 out = L.alloc_compressed(cfg.n, cfg.k, cfg.E, cfg.d, X.dtype, "cuda")
 G = torch.cuda.get_device_properties(0).multi_processor_count
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]

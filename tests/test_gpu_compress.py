@@ -163,3 +163,24 @@ def test_compress_hot_expert_full_c2(L):
     codes = make_codes(cfg.n, cfg.q, cfg.d, 3, C=cfg.C, p_noise=0.08)
     zeta = make_zipf_gate(cfg.n, 1, cfg.E, 3, hot=0.3)
     _compress_and_check(L, X, codes, zeta, cfg.E, "bf16", "C2-hot", repeat=False)
+
+
+def test_compress_leaves_workspace_at_rest(L):
+    """The contract of include/lshmoe.h: the workspace is 0xFF-filled before first use and every call
+    leaves its header (arrival counters) and hash table back at 0xFF, so calls need no clearing."""
+    cfg = CONFIGS["C2"]
+    case = make_case(L, cfg, seed=1, sanitize=False)
+    ws = torch.full((L.compress_workspace_bytes(cfg.n, 1, cfg.E, cfg.q, cfg.d, torch.bfloat16),), 255,
+                    dtype=torch.uint8, device="cuda")
+    Xd, cd, zd = case.X.cuda(), torch.from_numpy(case.codes).cuda(), case.zeta.cuda()
+    a = L.compress(Xd, cd, zd, cfg.E, workspace=ws)
+    perm_a = a.perm.clone()
+    torch.cuda.synchronize()
+    hdr_ints = 64 + 2048 + 512 + 16 * 512            # compress.cu kHdr
+    tsize = 1024
+    while tsize < 2 * cfg.n:
+        tsize *= 2
+    rest = ws[:4 * (hdr_ints + tsize)]
+    assert int((rest != 255).sum()) == 0
+    b = L.compress(Xd, cd, zd, cfg.E, workspace=ws)
+    assert torch.equal(b.perm, perm_a)

@@ -172,7 +172,7 @@ def test_baseline_permute_unpermute(L):
     send = torch.empty((n * k, 128), dtype=torch.bfloat16, device="cuda")
     slot = torch.empty((n, k), dtype=torch.int32, device="cuda")
     er = torch.empty(E, dtype=torch.int32, device="cuda")
-    ws = torch.empty(L.compress_workspace_bytes(n, k, E, 2, 128, torch.bfloat16), dtype=torch.uint8, device="cuda")
+    ws = L.compress_workspace(n, k, E, 2, 128, torch.bfloat16, "cuda")
     L.permute(X, case.zeta.cuda(), E, send, slot, er, ws)
     rr = er.view(E, 1).clone()
     eo = L.expert_ffn(send, rr, *stack_experts(ex, range(E), "cuda"))
