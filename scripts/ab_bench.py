@@ -145,6 +145,19 @@ def main():
         med, mn = timeit(torch_ffn, flush=flush)
         print(f"cuBLAS per-expert FFN (torch.addmm x{2 * cfg.E}): median {med:.1f} us  {fl / med / 1e6:.0f} TFLOP/s",
               flush=True)
+        if hasattr(torch, "_grouped_mm"):   # library grouped GEMM (the FFN's two layers, no bias/act)
+            offs_t = torch.tensor(offs[1:], dtype=torch.int32, device="cuda")
+            W1t = W[0].transpose(1, 2)          # [E, d, d_ffn] views: out = A @ W1^T per group
+            W2t = W[2].transpose(1, 2)
+            a = comp.centroids[:m]
+            try:
+                def grouped():
+                    h = torch._grouped_mm(a, W1t, offs=offs_t)
+                    torch._grouped_mm(h, W2t, offs=offs_t)
+                med, mn = timeit(grouped, flush=flush)
+                print(f"torch._grouped_mm x2 (no bias/ReLU): median {med:.1f} us  {fl / med / 1e6:.0f} TFLOP/s", flush=True)
+            except Exception as ex:   # noqa: BLE001
+                print("torch._grouped_mm unavailable:", str(ex)[:200])
 
 
 if __name__ == "__main__":
