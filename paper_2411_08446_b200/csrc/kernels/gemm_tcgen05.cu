@@ -846,6 +846,14 @@ int cta_mode(const char* env_name, int dflt) {
   return dflt;
 }
 
+// Switches that make a kernel skip work (wrong results, timing experiments only) are honoured only
+// when LSHMOE_EXPERIMENTS=1 is set as well, so a stray variable cannot corrupt a production run.
+int experiment_mode(const char* env_name) {
+  const char* on = getenv("LSHMOE_EXPERIMENTS");
+  if (!on || on[0] != '1') return 0;
+  return cta_mode(env_name, 0);
+}
+
 int ffn_order() {   // experiment override LSHMOE_FFN_ORDER (0 expert-major, 1 N-tile-major)
   const char* env = getenv("LSHMOE_FFN_ORDER");
   return env ? atoi(env) : 0;
@@ -890,7 +898,7 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
   ArgmaxEpi e{};
   e.codes = codes;
   e.q = q;
-  e.exp = cta_mode("LSHMOE_HASH_EXP", 0);
+  e.exp = experiment_mode("LSHMOE_HASH_EXP");
   e.rows_pad = static_cast<int>(((n + 255) / 256) * 256);
   // Slice split (one unit per BN slice of the d coordinates, slices merged by the last arrival)
   // evens out the persistent grid's last wave: C2 86.1 vs 90.2 us per launch, CUDA-graph timing in
@@ -951,7 +959,7 @@ int launch_hash_e4m3(const void* x8, int64_t n, int d, const void* R8, int q, in
   ArgmaxEpi e{};
   e.codes = codes;
   e.q = q;
-  e.exp = cta_mode("LSHMOE_HASH_EXP", 0);
+  e.exp = experiment_mode("LSHMOE_HASH_EXP");
   e.rows_pad = static_cast<int>(((n + 255) / 256) * 256);
   s.split = (d > bn) && ws && cta_mode("LSHMOE_HASH_SPLIT", 1) == 1 ? 1 : 0;
   if (s.split) {
@@ -1058,8 +1066,8 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
   if (E_local > kMaxLocalExperts) return cudaErrorInvalidValue;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int cta = cta_mode("LSHMOE_FFN_CTA", 2);
-  const int only = cta_mode("LSHMOE_FFN_ONLY", 0);   // experiment: 1 / 2 = launch only GEMM 1 / 2
-  const int exp = cta_mode("LSHMOE_FFN_EXP", 0);     // experiment: 1 = no output stores, 2 = no MMAs
+  const int only = experiment_mode("LSHMOE_FFN_ONLY");   // experiment: 1 / 2 = launch only GEMM 1 / 2
+  const int exp = experiment_mode("LSHMOE_FFN_EXP");     // experiment: 1 = no output stores, 2 = no MMAs
   FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, ffn_prefetch(), nullptr, nullptr, ffn_order()};
   const int bn1 = env_bn("LSHMOE_FFN_BN1", d_ffn, pick_bn(d_ffn));
   int err = 0;

@@ -2,6 +2,8 @@
 L2 flushed before every timed launch.  Usage: python scripts/ab_bench.py [hash|ffn|all]"""
 import os
 import statistics
+
+os.environ.setdefault("LSHMOE_EXPERIMENTS", "1")   # honour the work-skipping experiment switches
 import sys
 
 import torch

@@ -184,3 +184,15 @@ def test_compress_leaves_workspace_at_rest(L):
     assert int((rest != 255).sum()) == 0
     b = L.compress(Xd, cd, zd, cfg.E, workspace=ws)
     assert torch.equal(b.perm, perm_a)
+
+
+def test_compress_max_q_and_many_experts(L):
+    """The envelope: q = LSHMOE_MAX_Q = 16 hash functions per key, E = 255 experts (one expert
+    digit short of the tile grouping's 256), k = 3."""
+    from lshmoe_inputs import make_codes, make_zipf_gate
+    n, k, E, q = 6000, 3, 255, 16
+    cfg = small_cfg(n=n, k=k, E=E, q=q, d=128)
+    X = make_tokens(cfg, 4)
+    codes = make_codes(n, q, 128, 4, C=40, p_noise=0.02)
+    zeta = make_zipf_gate(n, k, E, 4)
+    _compress_and_check(L, X, codes, zeta, E, "bf16", "q=16,E=255")
