@@ -131,3 +131,51 @@ def test_backward_singletons_equal_dense_moe_backward():
             Y = Y + mask * torch.from_numpy(g[:, s:s + 1]) * (torch.relu(Xt @ W1.T + b1) @ W2.T + b2)
     (Y * torch.from_numpy(dY)).sum().backward()
     np.testing.assert_allclose(dX, Xt.grad.numpy(), rtol=1e-10, atol=1e-10)
+
+
+def test_backward_multi_rank_exchange_is_w_invariant():
+    """NEXT-1 across ranks: G travels to the expert owners with dispatch_sim, H = J_E^T G is
+    computed there, combine_sim brings H back; each rank's dX equals its single-rank backward
+    (clustering is per source rank, so the exchanges only move rows) — for w = 2 and 4."""
+    rng = np.random.default_rng(11)
+    E, k, d, d_ffn, q = 4, 2, 8, 12, 2
+    experts = {e: (rng.standard_normal((d_ffn, d)) / np.sqrt(d), 0.3 * rng.standard_normal(d_ffn),
+                   rng.standard_normal((d, d_ffn)) / np.sqrt(d_ffn), 0.1 * rng.standard_normal(d)) for e in range(E)}
+    R = np.stack([np.linalg.qr(rng.standard_normal((d, d)))[0] for _ in range(q)])
+    for w in (2, 4):
+        per = []
+        for r in range(w):
+            X = rng.standard_normal((40, d))
+            X[20:] = X[:20] * (1 + 1e-3 * rng.standard_normal((20, 1)))
+            zeta = np.stack([np.sort(rng.choice(E, size=k, replace=False)) for _ in range(40)]).astype(np.int32)
+            g = rng.random((40, k)) + 0.1
+            b = O.bucketize(O.cp_hash(X, R)[0], zeta, E)
+            C = O.centroids(X, b, k)
+            dY = rng.standard_normal((40, d))
+            per.append((X, zeta, g, b, C, dY))
+        # forward outputs o per rank via the simulated exchange, then the backward chain
+        recv, rr = O.dispatch_sim([p[4] for p in per], [p[3].expert_rows for p in per], E)
+        epr = E // w
+        outs, Hs = [], []
+        G_by_rank = [O.grad_compress(p[5], p[3], k, p[2]) for p in per]
+        Grecv, _ = O.dispatch_sim(G_by_rank, [p[3].expert_rows for p in per], E)
+        for p_ in range(w):
+            o = np.zeros_like(recv[p_])
+            h = np.zeros_like(recv[p_])
+            pos = 0
+            for el in range(epr):
+                e = p_ * epr + el
+                n_e = int(rr[p_][el].sum())
+                W1, b1, W2, b2 = experts[e]
+                o[pos:pos + n_e] = O.expert_ffn(recv[p_][pos:pos + n_e], W1, b1, W2, b2)
+                h[pos:pos + n_e] = O.expert_ffn_vjp(recv[p_][pos:pos + n_e], W1, b1, W2, Grecv[p_][pos:pos + n_e])
+                pos += n_e
+            outs.append(o)
+            Hs.append(h)
+        ret = O.combine_sim(outs, [p[3].expert_rows for p in per], E)
+        Hback = O.combine_sim(Hs, [p[3].expert_rows for p in per], E)
+        for r, (X, zeta, g, b, C, dY) in enumerate(per):
+            dX, dg = O.grad_restore(dY, X, C, ret[r], G_by_rank[r], Hback[r], b, g)
+            _, _, dX1, dg1 = O.lsh_layer_backward(X, zeta, b, C, ret[r], experts, dY, g)
+            np.testing.assert_allclose(dX, dX1, rtol=0, atol=1e-12)
+            np.testing.assert_allclose(dg, dg1, rtol=0, atol=1e-12)
