@@ -218,9 +218,9 @@ struct ArgmaxEpiT {
   uint2* partial;     // [nparts][rows_pad][q] (|y| bits, index | sign << 31) of each slice
   int* counter;       // [slices][q] arrival counters, zero at rest (reset by the last arrival)
   int rows_pad;
-  // four independent running winners (column i goes to chain i % 4) keep the dependent
-  // compare/select chain short; merged by (larger |y|, then smaller index) at the end, which is
-  // exactly the first maximum of one ascending scan.
+  // running winner in chain 0 (chains 1-3 stay empty: the block-max scan below replaced the four
+  // interleaved chains); merged by (larger |y|, then smaller index), exactly the first maximum of
+  // one ascending scan.
   float cb[4];
   int ci[4];
   float best;
@@ -322,16 +322,30 @@ struct ArgmaxEpiT {
       if (r[0] == 0x7FC00001u && r[31] == 0x7FC00001u) cb[0] = 1.0f;   // keep the TMEM load live
       return;
     }
+    // Block maximum of |y| first (a 5-level fmax tree: |.| is a free operand modifier, max is exact
+    // and order-independent), then — only when the block beats the running winner (strictly, so an
+    // equal magnitude keeps the earlier column) — the first column attaining it and its sign.
+    float m16[16];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float v = __uint_as_float(r[i]);
-      const float a = fabsf(v);
-      const int k = i & 3;
-      if (a > cb[k]) {          // strict: equal magnitudes keep the smaller (earlier) index
-        cb[k] = a;
-        // index | sign bit; -0.0f is not < 0, so a zero winner is '+'
-        ci[k] = (col0 + i) | (v < 0.0f ? static_cast<int>(0x80000000u) : 0);
+    for (int i = 0; i < 16; ++i) m16[i] = fmaxf(fabsf(__uint_as_float(r[i])), fabsf(__uint_as_float(r[i + 16])));
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+      for (int i = 0; i < w; ++i) m16[i] = fmaxf(m16[i], m16[i + w]);
+    const float bm = m16[0];
+    if (bm > cb[0]) {
+      int idx = 0;
+      bool neg = false;
+#pragma unroll
+      for (int i = 31; i >= 0; --i) {   // descending: the last hit is the smallest column
+        const float v = __uint_as_float(r[i]);
+        if (fabsf(v) == bm) {
+          idx = i;
+          neg = v < 0.0f;                 // -0.0f is not < 0, so a zero winner is '+'
+        }
       }
+      cb[0] = bm;
+      ci[0] = (col0 + idx) | (neg ? static_cast<int>(0x80000000u) : 0);
     }
   }
   // half: which half of the unit's columns this thread scanned (8 epilogue warps) or 0.
