@@ -42,6 +42,12 @@ def parse():
                    help="hash family: cross-polytope (paper default, Eq. 3), spherical-plane (NEXT-3), or "
                         "cross-polytope on e4m3 operands (NEXT-2 fp8 option)")
     p.add_argument("--sp-bits", type=int, default=12, help="sign bits per SP hash function")
+    p.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                   help="a6/a8 at N>1: phase 1 (NCCL, one host count sync) or phase 2 (device-initiated stores "
+                        "into the peers' windows, no host sync, CUDA-graph captured)")
+    p.add_argument("--share-gpu", action="store_true",
+                   help="testing only: every rank on cuda:0 with a gloo group (p2p exchange); the line is "
+                        "marked and is not a measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-uncompressed", action="store_true")
     p.add_argument("--no-graph", action="store_true")
@@ -217,13 +223,24 @@ def main():
     import paper_2411_08446_b200 as L
     from lshmoe_inputs import make_experts, make_rank_inputs, rotation_seed
 
+    if args.share_gpu:
+        assert args.exchange == "p2p", "--share-gpu needs --exchange p2p (NCCL refuses two ranks on one GPU)"
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     assert cfg.E % world == 0, "experts must split evenly over ranks"
     E_local = cfg.E // world
-    comm = L.Comm.from_process_group() if world > 1 else None
+    p2p = args.exchange == "p2p"
+    if p2p:     # phase 2: a window per rank (receive + returned buffers), peers mapped over CUDA IPC
+        comm = L.Comm(world, rank, None).p2p_init(cfg.n * cfg.k * world, cfg.n * cfg.k, cfg.d, X_dtype(cfg), cfg.E,
+                                                  group=dist.group.WORLD if world > 1 else None)
+    else:
+        comm = L.Comm.from_process_group() if world > 1 else None
 
     # ---- inputs (seeded synthetic, per rank) and buffers ----
     X_cpu, zeta_cpu, _ = make_rank_inputs(cfg, args.seed, rank)
@@ -244,6 +261,8 @@ def main():
     hid = torch.empty((cap, cfg.d_ffn), dtype=X.dtype, device=dev)
     eo = torch.empty((cap, d), dtype=X.dtype, device=dev)
     ret = eo if world == 1 else torch.empty((nk, d), dtype=X.dtype, device=dev)
+    if p2p:     # the exchange lands in the window
+        recv, ret, rr = comm.p2p_buffers()
     y = torch.empty_like(X)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)     # 256 MiB > 126 MB L2
     stream = torch.cuda.Stream(device=dev)          # non-default stream (graph capture needs one)
@@ -254,7 +273,9 @@ def main():
     if world > 1:
         torch.cuda.synchronize()
         dist.barrier()
+    if comm is not None:
         comm.close()
+    if world > 1:
         dist.destroy_process_group()
 
 
@@ -264,6 +285,7 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     from lshmoe_inputs import make_experts, rotation_seed
     n, k, d = cfg.n, cfg.k, cfg.d
     nk = n * k
+    p2p = args.exchange == "p2p"
 
     Nrm = L.sp_normals(R, args.sp_bits) if args.hash == "sp" else None
     R8 = L.rotation_e4m3(cfg.d, cfg.q, rotation_seed(args.seed)).to(dev) if args.hash == "cp8" else None
@@ -281,9 +303,10 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
         return [
             h,
             lambda: L.compress(Xb, codes, zb, cfg.E, out=comp, workspace=ws),
-            lambda: L.dispatch(comm, comp.centroids, comp.expert_rows, cfg.E, recv, rr),
+            (lambda: L.dispatch_p2p(comm, comp.centroids, comp.expert_rows)) if p2p else
+            (lambda: L.dispatch(comm, comp.centroids, comp.expert_rows, cfg.E, recv, rr)),
             lambda: L.expert_ffn(recv, rr, W1, b1, W2, b2, out=eo, hidden=hid),
-            lambda: L.combine(comm, eo, comp.expert_rows, cfg.E, ret),
+            (lambda: L.combine_p2p(comm, eo)) if p2p else (lambda: L.combine(comm, eo, comp.expert_rows, cfg.E, ret)),
             lambda: L.restore(Xb, comp.centroids, ret, comp.bucket, y=yb),
         ]
 
@@ -304,7 +327,7 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if args.share_gpu else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -343,7 +366,7 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     compress_cta = L.compress_cta_times(ws)
 
     # ---- headline: whole step, CUDA graph replay at world 1 (no host sync inside the step) ----
-    use_graph = world == 1 and not args.no_graph
+    use_graph = (world == 1 or p2p) and not args.no_graph   # phase 1 at N>1 syncs the host: eager
     run = step
     if use_graph:
         g = torch.cuda.CUDAGraph()
@@ -448,11 +471,20 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
         uret = eo if world == 1 else torch.empty((nk, d), dtype=X.dtype, device=dev)
         yb = torch.empty_like(X)
 
+        if p2p:
+            urecv, uret, brr = recv, ret, rr
+
         def base_step():
             L.permute(X, zeta, cfg.E, send, slot, er, ws)
-            L.dispatch(comm, send, er, cfg.E, urecv, brr)
+            if p2p:
+                L.dispatch_p2p(comm, send, er)
+            else:
+                L.dispatch(comm, send, er, cfg.E, urecv, brr)
             L.expert_ffn(urecv, brr, W1, b1, W2, b2, out=eo, hidden=hid)
-            L.combine(comm, eo, er, cfg.E, uret)
+            if p2p:
+                L.combine_p2p(comm, eo)
+            else:
+                L.combine(comm, eo, er, cfg.E, uret)
             L.unpermute(uret, slot, yb)
 
         for _ in range(3):
@@ -579,6 +611,9 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 "compression_ratio": ratio, "centroids": m, "routed_copies": nk,
                 "gpu_launches": launches_per_step * args.steps, "gpu_launches_per_step": launches_per_step,
                 "cuda_graph": use_graph,
+                "exchange": ("phase 2: device-initiated stores into the peers' windows (CUDA IPC), no host sync"
+                             if p2p else "phase 1: NCCL all-gather of counts + grouped send/recv"
+                             if world > 1 else "world 1: aliased (no copy)"),
                 "stages_ms": stage_ms, "eager_ms_per_step": eager_ms,
                 "compress_kernels_us": compress_phases,
                 "compress_centroid_cta_us": compress_cta,
@@ -591,7 +626,14 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 "uncompressed_baseline": unc,
                 "backward_lsh": bwd,
                 "cpu_baseline": cpu}
+        if args.share_gpu:
+            line["share_gpu"] = "all ranks time-slice cuda:0: a correctness run of the N>1 path, not a measurement"
         print(json.dumps(line), flush=True)
+
+
+def X_dtype(cfg):
+    import torch
+    return torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
 
 
 if __name__ == "__main__":

@@ -46,6 +46,7 @@ extern "C" {
 
 #define LSHMOE_ABI_VERSION 1
 #define LSHMOE_UNIQUE_ID_BYTES 128
+#define LSHMOE_P2P_HANDLE_BYTES 64   /* cudaIpcMemHandle_t */
 #define LSHMOE_MAX_Q 16
 
 typedef enum {
@@ -180,7 +181,8 @@ lshmoe_status lshmoe_compress(const void* x, lshmoe_dtype dtype, int64_t n, int 
 
 /* ---- a6/a8 communicator ----------------------------------------------------------------------
    Expert placement: rank p owns experts [p*E/w, (p+1)*E/w).  NCCL over NVLink; the
-   bootstrap id travels over torch.distributed.  world == 1 needs no id (pass NULL). */
+   bootstrap id travels over torch.distributed.  world == 1 needs no id (pass NULL); id == NULL at
+   world > 1 makes a comm without NCCL, usable only by the phase-2 calls below. */
 lshmoe_status lshmoe_get_unique_id(uint8_t* id /* [host] LSHMOE_UNIQUE_ID_BYTES */);
 lshmoe_status lshmoe_comm_init(const uint8_t* id /* [host] */, int world, int rank,
                                lshmoe_comm** out /* [host] */);
@@ -226,6 +228,55 @@ lshmoe_status lshmoe_expert_ffn(const void* in, lshmoe_dtype dtype, int d, int d
 lshmoe_status lshmoe_combine(lshmoe_comm* comm, const void* expert_out, lshmoe_dtype dtype, int d,
                              const int32_t* expert_rows, int num_experts, void* returned,
                              int64_t returned_capacity, lshmoe_stream stream);
+
+/* ---- a6/a8 phase 2: device-initiated exchange over peer memory ------------------
+   The same all-to-all as lshmoe_dispatch / lshmoe_combine (identical layouts, reading R24) without a
+   host synchronisation and without NCCL on the data path: every rank owns a window holding its
+   receive and returned buffers, per-epoch count mailboxes and flags; dispatch writes its counts and
+   its centroid rows straight into the owners' windows (NVLink stores), combine writes the expert
+   outputs straight back into the sources' returned buffers, flag handshakes (system-scope
+   release/acquire) complete each call on the device.  All ranks must call dispatch_p2p /
+   combine_p2p in the same order; the kernels spin until every peer has arrived, so the kernels of
+   all ranks must be able to run concurrently.
+   lshmoe_comm_p2p_init: allocates the window (recv_capacity / ret_capacity rows of row_bytes =
+     d * sizeof(dtype), a multiple of 16; E % world == 0, world <= 8, E <= 256) and maps every
+     peer's window with CUDA IPC (handles all-gathered over the comm's NCCL; collective).
+   The same in three steps when the handles travel another way (e.g. torch.distributed, or a comm
+   made with id == NULL at world > 1, which has no NCCL and serves phase 2 only):
+   lshmoe_comm_p2p_alloc (same arguments; complete at world 1), lshmoe_comm_p2p_handle (this
+   window's CUDA IPC handle, LSHMOE_P2P_HANDLE_BYTES [host] out), lshmoe_comm_p2p_open (handles
+   [host] world * LSHMOE_P2P_HANDLE_BYTES, rank-major; maps every peer's window).
+   lshmoe_comm_local_group: `world` comms in this process sharing one device (virtual ranks, plain
+     pointers instead of IPC), for testing the protocol on one GPU; out [host] lshmoe_comm* [world],
+     each released with lshmoe_comm_destroy.  Their dispatch_p2p calls must run on distinct streams.
+   lshmoe_comm_p2p_buffers: the window's recv [recv_capacity, d], returned [ret_capacity, d] and the
+     device int32 recv_rows [E/w, w] written by dispatch_p2p (pointers owned by the comm).
+   lshmoe_dispatch_p2p: centroids [m, d] (send layout; may be NULL when m == 0) + expert_rows [E]
+     device -> every owner's recv / recv_rows.  Row capacities are the caller's contract (not checked on the device).
+   lshmoe_combine_p2p: expert_out [rows received, d] in recv layout (may be NULL when no rows were
+     received) -> the sources' returned
+     buffers (centroid layout), for the last dispatch_p2p.  grid: CTAs per call (<= 0: two per SM, divided by w in a local
+     group so that every virtual rank's kernel is resident at once).
+   Capacities must be equal on every rank.  Rows that would land past a receive / returned buffer
+   are dropped and flagged on the sending rank; lshmoe_comm_p2p_error synchronises `stream`, reads
+   and clears the flags (value bit 0: a receive buffer overflowed, bit 1: a returned buffer) and
+   returns LSHMOE_EDEVICE when any is set.  A peer that never joins a call makes the waiting kernel
+   trap after 10 s (sticky CUDA error) rather than hang the device. */
+lshmoe_status lshmoe_comm_p2p_init(lshmoe_comm* comm, int64_t recv_capacity, int64_t ret_capacity,
+                                   int row_bytes, int num_experts);
+lshmoe_status lshmoe_comm_p2p_alloc(lshmoe_comm* comm, int64_t recv_capacity, int64_t ret_capacity,
+                                    int row_bytes, int num_experts);
+lshmoe_status lshmoe_comm_p2p_handle(const lshmoe_comm* comm, uint8_t* handle /* [host] */);
+lshmoe_status lshmoe_comm_p2p_open(lshmoe_comm* comm, const uint8_t* handles /* [host] */);
+lshmoe_status lshmoe_comm_local_group(int world, int64_t recv_capacity, int64_t ret_capacity,
+                                      int row_bytes, int num_experts, lshmoe_comm** out);
+lshmoe_status lshmoe_comm_p2p_buffers(lshmoe_comm* comm, void** recv, void** returned,
+                                      int32_t** recv_rows);
+lshmoe_status lshmoe_comm_p2p_error(lshmoe_comm* comm, int32_t* value /* [host] */, lshmoe_stream stream);
+lshmoe_status lshmoe_dispatch_p2p(lshmoe_comm* comm, const void* centroids, const int32_t* expert_rows,
+                                  int grid, lshmoe_stream stream);
+lshmoe_status lshmoe_combine_p2p(lshmoe_comm* comm, const void* expert_out, int grid,
+                                 lshmoe_stream stream);
 
 /* ---- a9: residual-based error compensation, Eq. 4-5, Alg. 1 L17-19 -------------
    y_t = sum_s g_ts * (returned[b_ts] + (x_t - centroids[b_ts])), b = bucket [n, k], g = gate_weight

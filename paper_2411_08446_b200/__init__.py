@@ -28,6 +28,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 OK, EINVAL, EUNSUPPORTED, ECUDA, ENCCL, EDEVICE = range(6)
 F32, BF16 = 0, 1
 UNIQUE_ID_BYTES = 128
+P2P_HANDLE_BYTES = 64
 _STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSUPPORTED", 3: "ECUDA", 4: "ENCCL", 5: "EDEVICE"}
 
 _vp, _i64, _i32, _u64, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64, ctypes.c_size_t
@@ -64,6 +65,15 @@ _SIGS = {
     "lshmoe_dispatch": ([_vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp, ctypes.POINTER(_i64), _vp], _i32),
     "lshmoe_expert_ffn": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp], _i32),
     "lshmoe_combine": ([_vp, _vp, _i32, _i32, _vp, _i32, _vp, _i64, _vp], _i32),
+    "lshmoe_comm_p2p_init": ([_vp, _i64, _i64, _i32, _i32], _i32),
+    "lshmoe_comm_p2p_alloc": ([_vp, _i64, _i64, _i32, _i32], _i32),
+    "lshmoe_comm_p2p_handle": ([_vp, _vp], _i32),
+    "lshmoe_comm_p2p_open": ([_vp, _vp], _i32),
+    "lshmoe_comm_local_group": ([_i32, _i64, _i64, _i32, _i32, _vp], _i32),
+    "lshmoe_comm_p2p_buffers": ([_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)], _i32),
+    "lshmoe_comm_p2p_error": ([_vp, ctypes.POINTER(_i32), _vp], _i32),
+    "lshmoe_dispatch_p2p": ([_vp, _vp, _vp, _i32, _vp], _i32),
+    "lshmoe_combine_p2p": ([_vp, _vp, _i32, _vp], _i32),
     "lshmoe_restore": ([_vp, _vp, _vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _vp], _i32),
     "lshmoe_permute": ([_vp, _i32, _i64, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp], _i32),
     "lshmoe_unpermute": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _vp], _i32),
@@ -450,9 +460,9 @@ class Comm:
         self.world, self.rank = world, rank
         h = ctypes.c_void_p()
         idbuf = None
-        if world > 1:
-            if unique_id is None or len(unique_id) != UNIQUE_ID_BYTES:
-                raise ValueError("world > 1 needs the 128-byte unique id from rank 0")
+        if world > 1 and unique_id is not None:       # None: phase-2-only comm (no NCCL)
+            if len(unique_id) != UNIQUE_ID_BYTES:
+                raise ValueError("the NCCL unique id is 128 bytes")
             idbuf = (ctypes.c_uint8 * UNIQUE_ID_BYTES).from_buffer_copy(unique_id)
         _check(_lib.lshmoe_comm_init(idbuf, world, rank, ctypes.byref(h)), "lshmoe_comm_init")
         self._h = h
@@ -482,6 +492,59 @@ class Comm:
         _check(_lib.lshmoe_comm_last_counts(self._h, _ptr(out), num_experts), "lshmoe_comm_last_counts")
         return out
 
+    # phase 2: device-initiated exchange over peer memory
+    def p2p_init(self, recv_capacity: int, ret_capacity: int, d: int, dtype: torch.dtype, num_experts: int,
+                 group=None):
+        """Allocate this rank's exchange window and map every peer's (collective at world > 1).  The
+        CUDA IPC handles travel over the comm's NCCL, or over torch.distributed `group` if given."""
+        self._p2p = (recv_capacity, ret_capacity, d, dtype, num_experts)
+        rb = d * _esize(dtype)
+        if group is None:
+            _check(_lib.lshmoe_comm_p2p_init(self._h, recv_capacity, ret_capacity, rb, num_experts),
+                   "lshmoe_comm_p2p_init")
+            return self
+        import torch.distributed as dist
+        _check(_lib.lshmoe_comm_p2p_alloc(self._h, recv_capacity, ret_capacity, rb, num_experts),
+               "lshmoe_comm_p2p_alloc")
+        h = (ctypes.c_uint8 * P2P_HANDLE_BYTES)()
+        _check(_lib.lshmoe_comm_p2p_handle(self._h, h), "lshmoe_comm_p2p_handle")
+        allh = [None] * self.world
+        dist.all_gather_object(allh, bytes(h), group=group)
+        buf = (ctypes.c_uint8 * (P2P_HANDLE_BYTES * self.world)).from_buffer_copy(b"".join(allh))
+        _check(_lib.lshmoe_comm_p2p_open(self._h, buf), "lshmoe_comm_p2p_open")
+        return self
+
+    @classmethod
+    def local_group(cls, world: int, recv_capacity: int, ret_capacity: int, d: int, dtype: torch.dtype,
+                    num_experts: int) -> list:
+        """`world` virtual ranks in this process on the current device (testing the phase-2 protocol on
+        one GPU).  Their dispatch_p2p / combine_p2p calls must be issued on distinct streams."""
+        hs = (ctypes.c_void_p * world)()
+        _check(_lib.lshmoe_comm_local_group(world, recv_capacity, ret_capacity, d * _esize(dtype), num_experts, hs),
+               "lshmoe_comm_local_group")
+        out = []
+        for r in range(world):
+            c = cls.__new__(cls)
+            c.world, c.rank, c._h = world, r, ctypes.c_void_p(hs[r])
+            c._p2p = (recv_capacity, ret_capacity, d, dtype, num_experts)
+            out.append(c)
+        return out
+
+    def p2p_buffers(self):
+        """(recv [recv_capacity, d], returned [ret_capacity, d], recv_rows int32 [E/w, w]): views of the
+        window owned by this comm (valid until close())."""
+        rc, tc, d, dtype, E = self._p2p
+        pr, pt, pn = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _check(_lib.lshmoe_comm_p2p_buffers(self._h, ctypes.byref(pr), ctypes.byref(pt), ctypes.byref(pn)),
+               "lshmoe_comm_p2p_buffers")
+        return (_device_view(pr.value, (rc, d), dtype, self), _device_view(pt.value, (tc, d), dtype, self),
+                _device_view(pn.value, (E // self.world, self.world), torch.int32, self))
+
+    def p2p_check(self, stream=None):
+        """Raise if a phase-2 call on this rank dropped rows (a receive / returned buffer too small)."""
+        v = ctypes.c_int(0)
+        _check(_lib.lshmoe_comm_p2p_error(self._h, ctypes.byref(v), _stream(stream)), "lshmoe_comm_p2p_error")
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             _lib.lshmoe_comm_destroy(self._h)
@@ -492,6 +555,39 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+def _esize(dtype: torch.dtype) -> int:
+    return torch.empty((), dtype=dtype).element_size()
+
+
+class _DeviceBuf:
+    """__cuda_array_interface__ over library-owned device memory (keeps its owner alive)."""
+
+    def __init__(self, ptr: int, shape, typestr: str, owner):
+        self.owner = owner
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": tuple(shape), "typestr": typestr,
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def _device_view(ptr: int, shape, dtype: torch.dtype, owner) -> torch.Tensor:
+    code = {torch.float32: "<f4", torch.bfloat16: "<i2", torch.int32: "<i4"}[dtype]
+    t = torch.as_tensor(_DeviceBuf(ptr, shape, code, owner), device="cuda")
+    return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
+
+
+def dispatch_p2p(comm: Comm, centroids: torch.Tensor, expert_rows: torch.Tensor, grid: int = 0, stream=None):
+    """Phase-2 centroid all-to-all (Alg. 1 L14) over peer memory, no host synchronisation: rows land in
+    every owner's comm.p2p_buffers()[0], counts in [2]."""
+    _require_cuda(centroids, expert_rows)
+    _check(_lib.lshmoe_dispatch_p2p(comm.handle, _ptr(centroids), _ptr(expert_rows), grid, _stream(stream)),
+           "lshmoe_dispatch_p2p")
+
+
+def combine_p2p(comm: Comm, expert_out: torch.Tensor, grid: int = 0, stream=None):
+    """Phase-2 reverse all-to-all (Alg. 1 L16): rows land in every source's comm.p2p_buffers()[1]."""
+    _require_cuda(expert_out)
+    _check(_lib.lshmoe_combine_p2p(comm.handle, _ptr(expert_out), grid, _stream(stream)), "lshmoe_combine_p2p")
 
 
 def exchange_plan(world: int, rank: int, counts: torch.Tensor):

@@ -22,6 +22,17 @@ struct lshmoe_comm {
   int world = 1;
   int rank = 0;
   ncclComm_t nccl = nullptr;
+  // phase 2 (device-initiated exchange over peer memory)
+  uint8_t* window = nullptr;               // this rank's window (owned)
+  std::vector<uint8_t*> peers;             // every rank's window as mapped here (peers[rank] = window)
+  std::vector<bool> peer_ipc;              // opened with cudaIpcOpenMemHandle (close on destroy)
+  uint8_t** peers_dev = nullptr;           // device copy of `peers`
+  unsigned* done = nullptr;                // [0] CTA arrival counter (zero at rest), [1] error bits, [2] epoch
+  int32_t* recv_rows_dev = nullptr;        // [E/world][world] rows received per (local expert, source)
+  P2PLayout L{};
+  int p2p_E = 0;
+  int p2p_grid = 64;                       // default CTAs per phase-2 call
+  bool dispatched = false;                 // a dispatch_p2p was issued (combine needs one)
   int32_t* counts_dev = nullptr;     // [world * E_cap]
   int32_t* counts_host = nullptr;    // pinned [world * E_cap]
   int32_t* rr_host = nullptr;        // pinned [E_cap] recv_rows staging
@@ -87,11 +98,10 @@ lshmoe_status lshmoe_get_unique_id(uint8_t* id) {
 lshmoe_status lshmoe_comm_init(const uint8_t* id, int world, int rank, lshmoe_comm** out) {
   if (!out) return set_error(LSHMOE_EINVAL, "lshmoe_comm_init: out is NULL");
   if (world < 1 || rank < 0 || rank >= world) return set_error(LSHMOE_EINVAL, "lshmoe_comm_init: bad world/rank");
-  if (world > 1 && !id) return set_error(LSHMOE_EINVAL, "lshmoe_comm_init: id is NULL at world > 1");
   auto* c = new lshmoe_comm();
   c->world = world;
   c->rank = rank;
-  if (world > 1) {
+  if (world > 1 && id) {   // id == NULL at world > 1: a phase-2-only comm (no NCCL)
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof(u));
     lshmoe_status st = nccl_status(ncclCommInitRank(&c->nccl, world, u, rank), "ncclCommInitRank");
@@ -104,8 +114,205 @@ lshmoe_status lshmoe_comm_init(const uint8_t* id, int world, int rank, lshmoe_co
   return LSHMOE_OK;
 }
 
+static void p2p_release(lshmoe_comm* c) {
+  for (size_t p = 0; p < c->peers.size(); ++p)
+    if (c->peer_ipc.size() > p && c->peer_ipc[p] && c->peers[p]) cudaIpcCloseMemHandle(c->peers[p]);
+  c->peers.clear();
+  c->peer_ipc.clear();
+  if (c->window) cudaFree(c->window);
+  if (c->peers_dev) cudaFree(c->peers_dev);
+  if (c->done) cudaFree(c->done);
+  if (c->recv_rows_dev) cudaFree(c->recv_rows_dev);
+  c->window = nullptr;
+  c->peers_dev = nullptr;
+  c->done = nullptr;
+  c->recv_rows_dev = nullptr;
+  c->p2p_E = 0;
+}
+
+static P2PLayout p2p_layout(int world, int E, int64_t recv_cap, int64_t ret_cap, int row_bytes) {
+  P2PLayout L{};
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t o = off;
+    off += (bytes + 255) & ~int64_t(255);
+    return o;
+  };
+  L.data_flag = take(4 * world);
+  L.ret_flag = take(4 * world);
+  L.mailbox = take(8 * 2 * static_cast<int64_t>(world) * E);
+  L.recv = take(recv_cap * row_bytes);
+  L.returned = take(ret_cap * row_bytes);
+  L.recv_capacity = recv_cap;
+  L.ret_capacity = ret_cap;
+  L.row_bytes = row_bytes;
+  L.bytes = off;
+  return L;
+}
+
+// Allocates this rank's window (zeroed: flags and mailboxes at rest) and its device-side state.
+static lshmoe_status p2p_alloc(lshmoe_comm* c, int E, int64_t recv_cap, int64_t ret_cap, int row_bytes) {
+  p2p_release(c);
+  c->L = p2p_layout(c->world, E, recv_cap, ret_cap, row_bytes);
+  int err = cudaMalloc(&c->window, c->L.bytes);
+  if (!err) err = cudaMemset(c->window, 0, c->L.bytes);
+  if (!err) err = cudaMalloc(&c->peers_dev, sizeof(uint8_t*) * c->world);
+  if (!err) err = cudaMalloc(&c->done, 4 * sizeof(unsigned));
+  if (!err) err = cudaMemset(c->done, 0, 4 * sizeof(unsigned));
+  if (!err) err = cudaMalloc(&c->recv_rows_dev, sizeof(int32_t) * E);
+  if (err) return cuda_status(err, "lshmoe_comm_p2p_init: allocation");
+  c->peers.assign(c->world, nullptr);
+  c->peer_ipc.assign(c->world, false);
+  c->peers[c->rank] = c->window;
+  c->p2p_E = E;
+  c->dispatched = false;
+  int dev = 0, sms = 148;
+  if (!cudaGetDevice(&dev)) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  c->p2p_grid = 2 * sms;                   // two 256-thread CTAs per SM
+  return LSHMOE_OK;
+}
+
+static lshmoe_status p2p_publish_peers(lshmoe_comm* c) {
+  const int err = cudaMemcpy(c->peers_dev, c->peers.data(), sizeof(uint8_t*) * c->world, cudaMemcpyHostToDevice);
+  return cuda_status(err, "lshmoe_comm_p2p_init: peer table");
+}
+
+static lshmoe_status p2p_check(const lshmoe_comm* c, int64_t recv_capacity, int64_t ret_capacity, int row_bytes,
+                               int E, const char* fn) {
+  if (!c) return set_error(LSHMOE_EINVAL, std::string(fn) + ": comm is NULL");
+  if (recv_capacity < 0 || ret_capacity < 0 || row_bytes < 16 || row_bytes % 16 || E < 1 || E % c->world)
+    return set_error(LSHMOE_EINVAL, std::string(fn) + ": bad capacity / row_bytes (multiple of 16) / E");
+  if (c->world > 8 || E > 256) return set_error(LSHMOE_EUNSUPPORTED, std::string(fn) + ": world <= 8, E <= 256");
+  return LSHMOE_OK;
+}
+
+lshmoe_status lshmoe_comm_p2p_alloc(lshmoe_comm* c, int64_t recv_capacity, int64_t ret_capacity, int row_bytes,
+                                    int E) {
+  lshmoe_status st = p2p_check(c, recv_capacity, ret_capacity, row_bytes, E, "lshmoe_comm_p2p_alloc");
+  if (st) return st;
+  st = p2p_alloc(c, E, recv_capacity, ret_capacity, row_bytes);
+  if (st) return st;
+  return p2p_publish_peers(c);   // world 1 is complete; world > 1 needs lshmoe_comm_p2p_open
+}
+
+lshmoe_status lshmoe_comm_p2p_handle(const lshmoe_comm* c, uint8_t* handle) {
+  if (!c || !c->window || !handle) return set_error(LSHMOE_EINVAL, "lshmoe_comm_p2p_handle: no window / NULL");
+  cudaIpcMemHandle_t h;
+  const int err = cudaIpcGetMemHandle(&h, c->window);
+  if (err) return cuda_status(err, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == LSHMOE_P2P_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+  std::memcpy(handle, &h, sizeof(h));
+  return LSHMOE_OK;
+}
+
+lshmoe_status lshmoe_comm_p2p_open(lshmoe_comm* c, const uint8_t* handles) {
+  if (!c || !c->window || !handles) return set_error(LSHMOE_EINVAL, "lshmoe_comm_p2p_open: no window / NULL");
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank || c->peer_ipc[p]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + static_cast<size_t>(p) * sizeof(h), sizeof(h));
+    void* ptr = nullptr;
+    const int err = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (err) return cuda_status(err, "cudaIpcOpenMemHandle (peer window)");
+    c->peers[p] = static_cast<uint8_t*>(ptr);
+    c->peer_ipc[p] = true;
+  }
+  return p2p_publish_peers(c);
+}
+
+lshmoe_status lshmoe_comm_p2p_init(lshmoe_comm* c, int64_t recv_capacity, int64_t ret_capacity, int row_bytes,
+                                   int E) {
+  lshmoe_status st = lshmoe_comm_p2p_alloc(c, recv_capacity, ret_capacity, row_bytes, E);
+  if (st || c->world == 1) return st;
+  if (!c->nccl) return set_error(LSHMOE_EINVAL, "lshmoe_comm_p2p_init: no NCCL to exchange handles (use _open)");
+  constexpr size_t kH = LSHMOE_P2P_HANDLE_BYTES;
+  uint8_t* dev = nullptr;
+  int err = cudaMalloc(&dev, kH * c->world);
+  if (err) return cuda_status(err, "lshmoe_comm_p2p_init: handle buffer");
+  std::vector<uint8_t> all(kH * c->world);
+  st = lshmoe_comm_p2p_handle(c, all.data() + kH * c->rank);
+  if (!st) err = cudaMemcpy(dev + kH * c->rank, all.data() + kH * c->rank, kH, cudaMemcpyHostToDevice);
+  if (!st && !err) {
+    st = nccl_status(ncclAllGather(dev + kH * c->rank, dev, kH, ncclUint8, c->nccl, nullptr),
+                     "ncclAllGather(ipc handles)");
+    if (!st) err = cudaMemcpy(all.data(), dev, kH * c->world, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(dev);
+  if (st) return st;
+  if (err) return cuda_status(err, "lshmoe_comm_p2p_init: handle exchange");
+  return lshmoe_comm_p2p_open(c, all.data());
+}
+
+lshmoe_status lshmoe_comm_local_group(int world, int64_t recv_capacity, int64_t ret_capacity, int row_bytes, int E,
+                                      lshmoe_comm** out) {
+  if (!out || world < 1 || world > 8) return set_error(LSHMOE_EINVAL, "lshmoe_comm_local_group: bad world / out");
+  if (recv_capacity < 0 || ret_capacity < 0 || row_bytes < 16 || row_bytes % 16 || E < 1 || E % world || E > 256)
+    return set_error(LSHMOE_EINVAL, "lshmoe_comm_local_group: bad sizes");
+  std::vector<lshmoe_comm*> cs(world);
+  for (int r = 0; r < world; ++r) {
+    cs[r] = new lshmoe_comm();
+    cs[r]->world = world;
+    cs[r]->rank = r;
+    lshmoe_status st = p2p_alloc(cs[r], E, recv_capacity, ret_capacity, row_bytes);
+    if (st) {
+      for (int q = 0; q <= r; ++q) lshmoe_comm_destroy(cs[q]);
+      return st;
+    }
+  }
+  for (int r = 0; r < world; ++r) {
+    for (int p = 0; p < world; ++p) cs[r]->peers[p] = cs[p]->window;   // same process: plain pointers
+    cs[r]->p2p_grid = cs[r]->p2p_grid / world > 0 ? cs[r]->p2p_grid / world : 1;   // all ranks co-resident
+    lshmoe_status st = p2p_publish_peers(cs[r]);
+    if (st) return st;
+    out[r] = cs[r];
+  }
+  return LSHMOE_OK;
+}
+
+lshmoe_status lshmoe_comm_p2p_buffers(lshmoe_comm* c, void** recv, void** returned, int32_t** recv_rows) {
+  if (!c || !c->window) return set_error(LSHMOE_EINVAL, "lshmoe_comm_p2p_buffers: no phase-2 window");
+  if (recv) *recv = c->window + c->L.recv;
+  if (returned) *returned = c->window + c->L.returned;
+  if (recv_rows) *recv_rows = c->recv_rows_dev;
+  return LSHMOE_OK;
+}
+
+lshmoe_status lshmoe_comm_p2p_error(lshmoe_comm* c, int32_t* value, lshmoe_stream stream) {
+  if (!c || !c->window || !value) return set_error(LSHMOE_EINVAL, "lshmoe_comm_p2p_error: no window / NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned v = 0;
+  int err = cudaMemcpyAsync(&v, c->done + 1, sizeof(v), cudaMemcpyDeviceToHost, s);
+  if (!err) err = cudaStreamSynchronize(s);
+  if (!err && v) err = cudaMemsetAsync(c->done + 1, 0, sizeof(unsigned), s);
+  if (err) return cuda_status(err, "lshmoe_comm_p2p_error");
+  *value = static_cast<int32_t>(v);
+  if (v) return set_error(LSHMOE_EDEVICE, v & 1 ? "phase-2 dispatch: a receive buffer was too small (rows dropped)"
+                                                 : "phase-2 combine: a returned buffer was too small (rows dropped)");
+  return LSHMOE_OK;
+}
+
+lshmoe_status lshmoe_dispatch_p2p(lshmoe_comm* c, const void* centroids, const int32_t* expert_rows, int grid,
+                                  lshmoe_stream stream) {
+  if (!c || !c->window) return set_error(LSHMOE_EINVAL, "lshmoe_dispatch_p2p: no phase-2 window");
+  if (!expert_rows) return set_error(LSHMOE_EINVAL, "lshmoe_dispatch_p2p: expert_rows is NULL");
+  c->dispatched = true;
+  const int g = grid > 0 ? grid : c->p2p_grid;
+  return cuda_status(launch_p2p(0, c->peers_dev, c->L, c->world, c->rank, c->p2p_E, centroids, expert_rows,
+                                c->recv_rows_dev, c->done, g, stream),
+                     "lshmoe_dispatch_p2p");
+}
+
+lshmoe_status lshmoe_combine_p2p(lshmoe_comm* c, const void* expert_out, int grid, lshmoe_stream stream) {
+  if (!c || !c->window || !c->dispatched) return set_error(LSHMOE_EINVAL, "lshmoe_combine_p2p: no matching dispatch");
+  const int g = grid > 0 ? grid : c->p2p_grid;
+  return cuda_status(launch_p2p(1, c->peers_dev, c->L, c->world, c->rank, c->p2p_E, expert_out, nullptr, nullptr,
+                                c->done, g, stream),
+                     "lshmoe_combine_p2p");
+}
+
 lshmoe_status lshmoe_comm_destroy(lshmoe_comm* c) {
   if (!c) return LSHMOE_OK;
+  p2p_release(c);
   if (c->nccl) ncclCommDestroy(c->nccl);
   if (c->counts_dev) cudaFree(c->counts_dev);
   if (c->counts_host) cudaFreeHost(c->counts_host);
@@ -136,6 +343,7 @@ lshmoe_status lshmoe_dispatch(lshmoe_comm* c, const void* centroids, lshmoe_dtyp
                                     recv_rows == expert_rows ? nullptr : recv_rows, stream);
     return cuda_status(err, "lshmoe_dispatch (local)");
   }
+  if (!c->nccl) return set_error(LSHMOE_EINVAL, "lshmoe_dispatch: comm has no NCCL (created without an id)");
   lshmoe_status st = ensure_capacity(c, E);
   if (st) return st;
   const int epr = E / world;
@@ -208,6 +416,7 @@ lshmoe_status lshmoe_combine(lshmoe_comm* c, const void* expert_out, lshmoe_dtyp
                                     static_cast<int>(row_bytes), expert_rows, E, nullptr, stream);
     return cuda_status(err, "lshmoe_combine (local)");
   }
+  if (!c->nccl) return set_error(LSHMOE_EINVAL, "lshmoe_combine: comm has no NCCL (created without an id)");
   if (c->last_E != E) return set_error(LSHMOE_EINVAL, "lshmoe_combine: no matching dispatch plan on this comm");
   const int epr = E / world;
   const int me = c->rank;

@@ -87,6 +87,18 @@ int launch_expert_ffn_backward(const void* grad_out, lshmoe_dtype dtype, int d, 
                                int E_local, int world, const void* W2T, const void* W1T, const void* hidden,
                                void* dhidden, int64_t capacity, void* grad_in, void* stream);
 
+// Phase-2 exchange window (p2p.cu / comm.cpp): byte offsets inside every rank's window.
+struct P2PLayout {
+  int64_t data_flag, ret_flag;             // uint32 [world] epoch flags
+  int64_t mailbox;                         // uint64 [2][world][E] (epoch << 32 | count), by epoch parity
+  int64_t recv, returned;                  // row buffers (row_bytes each)
+  int64_t recv_capacity, ret_capacity;     // rows
+  int row_bytes;
+  int64_t bytes;                           // window size
+};
+int launch_p2p(int which, uint8_t* const* peers_dev, const P2PLayout& L, int world, int me, int E, const void* src,
+               const int32_t* expert_rows, int32_t* recv_rows, unsigned* done, int grid, void* stream);
+
 int read_and_clear_device_error(int* value, void* stream);
 void set_compress_diag(int on);   // per-CTA globaltimer stamps in the compress workspace header
 void count_launches(int n);   // kernels launched by this library (lshmoe_kernel_launches)

@@ -97,7 +97,16 @@ def test_validation_errors(L):
     assert lib.lshmoe_restore(ctypes.c_void_p(18), v, v, 1, 4, 64, v, 1, None, v, None) == L.EINVAL
     # E % world: world-1 comm with NULL handle accepts any E; bad dtype
     assert lib.lshmoe_dispatch(None, v, 7, 64, v, 4, v, 10, v, None, None) == L.EINVAL
-    assert lib.lshmoe_comm_init(None, 2, 0, ctypes.byref(ctypes.c_void_p())) == L.EINVAL   # world 2 needs an id
+    # world 2 without an id: a phase-2-only comm; the NCCL calls refuse it, phase-2 calls check sizes
+    h2 = ctypes.c_void_p()
+    assert lib.lshmoe_comm_init(None, 2, 0, ctypes.byref(h2)) == L.OK and h2.value
+    assert lib.lshmoe_dispatch(h2, v, 1, 64, v, 4, v, 10, v, None, None) == L.EINVAL
+    assert lib.lshmoe_comm_p2p_alloc(h2, 10, 10, 24, 4) == L.EINVAL        # row_bytes % 16
+    assert lib.lshmoe_comm_p2p_alloc(h2, 10, 10, 32, 3) == L.EINVAL        # E % world
+    assert lib.lshmoe_comm_p2p_alloc(h2, 10, 10, 32, 512) == L.EUNSUPPORTED
+    assert lib.lshmoe_dispatch_p2p(h2, v, v, 0, None) == L.EINVAL          # no window yet
+    assert lib.lshmoe_combine_p2p(h2, v, 0, None) == L.EINVAL
+    assert lib.lshmoe_comm_destroy(h2) == L.OK
     h = ctypes.c_void_p()
     assert lib.lshmoe_comm_init(None, 1, 0, ctypes.byref(h)) == L.OK and h.value
     assert lib.lshmoe_comm_destroy(h) == L.OK
