@@ -21,6 +21,11 @@ done
 for c in C3 C4 C5; do
   timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_${TAG}_$c.json 2> gpurun_out/bench_${TAG}_$c.err; echo "bench $c rc=$?"
 done
+# the N=2 path through the phase-2 exchange, both ranks on this one GPU (correctness run, not a measurement)
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 \
+   bench.py --gpus 2 --steps 3 --warmup 3 --exchange p2p --share-gpu --no-backward \
+   > gpurun_out/bench_${TAG}_p2p_n2share.json 2> gpurun_out/bench_${TAG}_p2p_n2share.err; echo "bench p2p n2 share rc=$?"
+timeout 300 python scripts/p2p_bench.py 0 16 > gpurun_out/p2p_micro_${TAG}.log 2>&1; echo "p2p micro rc=$?"
 for q in 1 2 3 4 5 6 7 8; do
   timeout 600 python bench.py --config C5 --q $q --no-cpu-baseline --no-backward --steps 10 > gpurun_out/qsweep_${TAG}_q$q.json 2> gpurun_out/qsweep_${TAG}_q$q.err; echo "q=$q rc=$?"
 done

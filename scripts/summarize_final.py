@@ -24,7 +24,8 @@ def main():
     lines = {}
     for nm, f in [("default", f"bench_{tag}.json"), ("reference", f"bench_ref_{tag}.json"),
                   ("sp", f"bench_{tag}_sp.json"), ("cp8", f"bench_{tag}_cp8.json"),
-                  ("C3", f"bench_{tag}_C3.json"), ("C4", f"bench_{tag}_C4.json"), ("C5", f"bench_{tag}_C5.json")]:
+                  ("C3", f"bench_{tag}_C3.json"), ("C4", f"bench_{tag}_C4.json"), ("C5", f"bench_{tag}_C5.json"),
+                  ("p2p_n2_share_gpu", f"bench_{tag}_p2p_n2share.json")]:
         d = load(os.path.join(SRC, f))
         if d:
             lines[nm] = d
@@ -48,7 +49,8 @@ def main():
     launches = os.path.join(SRC, f"launches_{tag}.csv")
     if reps and os.path.exists(launches):
         subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), tag, launches, *reps], check=False)
-    for nm, f in [("clocks", f"clocks_{tag}.csv"), ("tests", f"tests_{tag}.log"), ("smoke", f"smoke_{tag}.log")]:
+    for nm, f in [("clocks", f"clocks_{tag}.csv"), ("tests", f"tests_{tag}.log"), ("smoke", f"smoke_{tag}.log"),
+                  ("p2p_micro", f"p2p_micro_{tag}.log")]:
         p = os.path.join(SRC, f)
         if os.path.exists(p):
             with open(p) as a, open(os.path.join(OUT, f"{nm}_{tag}" + os.path.splitext(f)[1]), "w") as b:
