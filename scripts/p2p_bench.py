@@ -27,9 +27,10 @@ def timed(fn, reps=20, flush=True):
             with torch.cuda.stream(s):
                 FLUSH.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(s)
-        g.replay()
-        b.record(s)
+        with torch.cuda.stream(s):              # replay on the stream the events are recorded on
+            a.record(s)
+            g.replay()
+            b.record(s)
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e3)
     return statistics.median(ts)
