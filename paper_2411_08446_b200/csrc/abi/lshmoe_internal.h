@@ -100,6 +100,8 @@ int launch_p2p(int which, uint8_t* const* peers_dev, const P2PLayout& L, int wor
                const int32_t* expert_rows, int32_t* recv_rows, unsigned* done, int grid, void* stream);
 
 int read_and_clear_device_error(int* value, void* stream);
+// Programmatic dependent launch for the GEMM and restore kernels (LSHMOE_PDL=0 turns it off, A/B).
+bool pdl_enabled();
 void set_compress_diag(int on);   // per-CTA globaltimer stamps in the compress workspace header
 void count_launches(int n);   // kernels launched by this library (lshmoe_kernel_launches)
 int device_sm_count();

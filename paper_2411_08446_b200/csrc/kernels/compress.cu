@@ -134,6 +134,9 @@ __device__ __forceinline__ void dstamp(const Params& P, int kern, int j) {
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Lets the next PDL-launched kernel's CTAs be scheduled (onto SMs this grid leaves free) and run
+// their prologue; they still block in their own pdl_wait until this grid has completed.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 // Exclusive scan of one int per thread over a CTA of NW warps; *total = the sum.  s = [NW + 1].
 template <int NW>
@@ -216,6 +219,7 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(Params P) {
   const int E1 = P.E + 1;
   const int t = blockIdx.x;
   pdl_wait();                                // the hash kernel's codes (and every earlier write) are visible
+  pdl_trigger();
   dstamp(P, 0, 0);
   const int c = t * kTile + tid;
   const bool ok = c < P.nk;
@@ -353,6 +357,7 @@ __global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
   const int e = blockIdx.x / CS, r = blockIdx.x - e * CS;   // cluster (CS, 1, 1): rank = blockIdx.x % CS
   const int E1 = P.E + 1;
   pdl_wait();                               // K1's tiles and table are complete and visible
+  pdl_trigger();
   dstamp(P, 1, 0);
   // group size and offset: one column of the tile offsets
   int n_e, goff;
@@ -1014,6 +1019,7 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   __shared__ int s_job[8];
   const int tid = threadIdx.x;
   pdl_wait();                                // K2's perm, rows and counts are complete
+  pdl_trigger();
   dstamp(P, 2, 0);
   if (!P.permute)                             // K2 was the table's last reader: leave it at rest (-1)
     for (int64_t i = blockIdx.x * int64_t(kThreads) + tid; i <= P.mask; i += int64_t(gridDim.x) * kThreads)

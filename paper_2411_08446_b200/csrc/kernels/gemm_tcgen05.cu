@@ -605,6 +605,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (kCta == 2) tmem_alloc_2cta<C::kTmemCols>(tmem_slot);
     else tmem_alloc<C::kTmemCols>(tmem_slot);
   }
+  // PDL: everything above (barriers, TMEM, descriptor prefetch) overlaps the previous kernel's
+  // tail; nothing a predecessor writes is read before this wait.  Then let the next kernel launch.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   sched.init(sched_tables);   // contains __syncthreads
   tc_fence_before();
   if (kCta == 2) cluster_sync();   // peer barriers initialised before any remote arrive / TMA
@@ -803,13 +807,15 @@ int launch_tc(const CUtensorMap& a, const CUtensorMap& b, int K, const Sched& s,
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Cfg<BN, kCta, EpiScratch<Epi>::value>::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kCta;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see the kernel's wait)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   int err = cudaLaunchKernelEx(&cfg, kern, a, b, K, s, e);
   count_launches(1);
   return err ? err : cudaGetLastError();

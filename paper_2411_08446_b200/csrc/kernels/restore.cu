@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "../abi/lshmoe_internal.h"
 #include "common.cuh"
@@ -25,6 +26,8 @@ __global__ void __launch_bounds__(256) restore_kernel(const T* x /* y may alias 
   constexpr int VN = Vec<T>::N;
   const int cpr = d / VN;
   const int64_t total = n * cpr;
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: the combined rows are complete
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t t = i / cpr;
     const int ch = static_cast<int>(i - t * cpr);
@@ -187,22 +190,37 @@ int grid_for(int64_t work) {
 
 }  // namespace
 
+template <typename T>
+int launch_restore_pdl(const void* x, const void* ct, const void* ret, int64_t n, int d, const int32_t* bucket, int k,
+                       const float* g, void* y, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid_for(n * (d / Vec<T>::N)));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, restore_kernel<T>, static_cast<const T*>(x), static_cast<const T*>(ct),
+                            static_cast<const T*>(ret), n, d, bucket, k, g, static_cast<T*>(y));
+}
+
 int launch_restore(const void* x, const void* ct, const void* ret, lshmoe_dtype dtype, int64_t n, int d,
                    const int32_t* bucket, int k, const float* g, void* y, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (dtype == LSHMOE_BF16) {
-    using T = __nv_bfloat16;
-    restore_kernel<T><<<grid_for(n * (d / 8)), 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(ct),
-                                                             static_cast<const T*>(ret), n, d, bucket, k, g,
-                                                             static_cast<T*>(y));
-  } else {
-    restore_kernel<float><<<grid_for(n * (d / 4)), 256, 0, st>>>(static_cast<const float*>(x),
-                                                                 static_cast<const float*>(ct),
-                                                                 static_cast<const float*>(ret), n, d, bucket, k, g,
-                                                                 static_cast<float*>(y));
-  }
+  const int err = dtype == LSHMOE_BF16 ? launch_restore_pdl<__nv_bfloat16>(x, ct, ret, n, d, bucket, k, g, y, st)
+                                       : launch_restore_pdl<float>(x, ct, ret, n, d, bucket, k, g, y, st);
   count_launches(1);
-  return cudaGetLastError();
+  return err ? err : cudaGetLastError();
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* env = getenv("LSHMOE_PDL");
+    return !(env && env[0] == '0');
+  }();
+  return on;
 }
 
 int launch_grad_restore(const void* dy, const void* x, const void* ct, const void* ret, const void* G, const void* H,
