@@ -58,11 +58,12 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
     nccl_inc, nccl_lib = _nccl_dirs()
     cu, cpp = sources()
     objs, cmds = [], []
+    extra = os.environ.get("LSHMOE_NVCC_EXTRA", "").split()   # experiments only, e.g. -DLSHMOE_MERGE_BATCH=8
     for src in cu:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         objs.append(obj)
         cmds.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                     "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj])
+                     "--expt-relaxed-constexpr", *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj])
     for src in cpp:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         objs.append(obj)

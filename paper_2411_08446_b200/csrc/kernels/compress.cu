@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(Params P) {
   const int E1 = P.E + 1;
   const int t = blockIdx.x;
   pdl_wait();                                // the hash kernel's codes (and every earlier write) are visible
-  pdl_trigger();
+  // (no early trigger here: bucket CTAs placed beside a small tile grid delayed K2 by ~6 us on C2)
   dstamp(P, 0, 0);
   const int c = t * kTile + tid;
   const bool ok = c < P.nk;
@@ -683,9 +683,16 @@ __device__ __forceinline__ void store_chunk8(const Params& P, int row, int ch, c
   }
 }
 
-__device__ __forceinline__ int range_begin(int b, int nk, int G) { return static_cast<int>(static_cast<int64_t>(b) * nk / G); }
+// 32-bit divisions whenever the product fits (a 64-bit division is ~4x the instructions)
+__device__ __forceinline__ int range_begin(int b, int nk, int G) {
+  const uint64_t prod = static_cast<uint64_t>(b) * static_cast<uint32_t>(nk);
+  return prod >> 32 ? static_cast<int>(prod / static_cast<uint32_t>(G))
+                    : static_cast<int>(static_cast<uint32_t>(prod) / static_cast<uint32_t>(G));
+}
 __device__ __forceinline__ int range_cta(int p, int nk, int G) {   // CTA whose range holds p
-  return static_cast<int>((static_cast<int64_t>(p + 1) * G - 1) / nk);
+  const uint64_t prod = static_cast<uint64_t>(p + 1) * static_cast<uint32_t>(G) - 1;
+  return prod >> 32 ? static_cast<int>(prod / static_cast<uint32_t>(nk))
+                    : static_cast<int>(static_cast<uint32_t>(prod) / static_cast<uint32_t>(nk));
 }
 
 // Dynamic shared memory of compress_kernel, named at file scope so that the centroid phase's
@@ -928,6 +935,11 @@ __device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_
 // Rows cut by CTA ranges: each CTA holding a piece publishes its fp32 partial (centroid_block),
 // then arrives on the counter of the CTA where the row starts; the last arriver adds the
 // partials in CTA order (the same order whichever CTA arrives last) and stores the centroid.
+#ifndef LSHMOE_MERGE_BATCH
+#define LSHMOE_MERGE_BATCH 8
+#endif
+constexpr int kMergeBatch = LSHMOE_MERGE_BATCH;   // partials of a cut row loaded before any is added
+
 template <typename T>
 __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int* s_goff, const int* s_mrow,
                                const int* s_cut, int* s_job) {
@@ -947,8 +959,11 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
     if (cand) {
       const int rs = X.cut_rs, re = X.cut_re;
       const int b0 = range_cta(rs, P.nk, G), b1 = range_cta(re - 1, P.nk, G);
-      int expected = 0;
-      for (int bb = b0; bb <= b1; ++bb) expected += range_begin(bb + 1, P.nk, G) > range_begin(bb, P.nk, G);
+      int expected = b1 - b0 + 1;             // every range is non-empty when nk >= G
+      if (P.nk < G) {
+        expected = 0;
+        for (int bb = b0; bb <= b1; ++bb) expected += range_begin(bb + 1, P.nk, G) > range_begin(bb, P.nk, G);
+      }
       const int old = atomicAdd(reinterpret_cast<int*>(P.bar) + kArrive + b0, 1);   // counters start at -1
       if (old + 2 == expected) {
         __threadfence();                      // acquire the other CTAs' partials
@@ -967,18 +982,20 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
     const int rs = s_job[4 * j + 1], re = s_job[4 * j + 2];
     const int b0 = s_job[4 * j + 3] & 0xFFFF, b1 = s_job[4 * j + 3] >> 16;
     const int nc8 = P.row_bytes / 8;
+    const int slot0 = rs == range_begin(b0, P.nk, G) ? 0 : 1;
+    const bool all_nonempty = P.nk >= G;
     for (int ch = tid; ch < nc8; ch += kThreads) {
       float acc[VC];
-      const float* src = P.partial + (static_cast<int64_t>(b0) * 2 + (rs == range_begin(b0, P.nk, G) ? 0 : 1)) * P.d + ch * VC;
+      const float* src = P.partial + (static_cast<int64_t>(b0) * 2 + slot0) * P.d + ch * VC;
 #pragma unroll
       for (int e = 0; e < VC; ++e) acc[e] = __ldcg(src + e);
-      for (int bb0 = b0 + 1; bb0 <= b1; bb0 += 8) {   // 8 partials in flight, added in CTA order
-        float tmp[8][VC];
-        bool used[8];
+      for (int bb0 = b0 + 1; bb0 <= b1; bb0 += kMergeBatch) {   // kMergeBatch partials in flight, added in CTA order
+        float tmp[kMergeBatch][VC];
+        bool used[kMergeBatch];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kMergeBatch; ++u) {
           const int bb = bb0 + u;
-          const bool use = bb <= b1 && range_begin(bb + 1, P.nk, G) > range_begin(bb, P.nk, G);   // skip empty ranges
+          const bool use = bb <= b1 && (all_nonempty || range_begin(bb + 1, P.nk, G) > range_begin(bb, P.nk, G));   // skip empty ranges
           const float* s2 = P.partial + (static_cast<int64_t>(bb) * 2) * P.d + ch * VC;
 #pragma unroll
           used[u] = use;
@@ -986,7 +1003,7 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
           for (int e = 0; e < VC; ++e) tmp[u][e] = use ? __ldcg(s2 + e) : 0.0f;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < kMergeBatch; ++u)
           if (used[u])
 #pragma unroll
             for (int e = 0; e < VC; ++e) acc[e] += tmp[u][e];
