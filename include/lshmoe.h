@@ -249,6 +249,8 @@ lshmoe_status lshmoe_combine(lshmoe_comm* comm, const void* expert_out, lshmoe_d
    lshmoe_comm_local_group: `world` comms in this process sharing one device (virtual ranks, plain
      pointers instead of IPC), for testing the protocol on one GPU; out [host] lshmoe_comm* [world],
      each released with lshmoe_comm_destroy.  Their dispatch_p2p calls must run on distinct streams.
+   lshmoe_comm_destroy releases the window and unmaps the peers': every rank must be done with the
+     phase-2 calls (e.g. a barrier) before any rank destroys its comm.
    lshmoe_comm_p2p_buffers: the window's recv [recv_capacity, d], returned [ret_capacity, d] and the
      device int32 recv_rows [E/w, w] written by dispatch_p2p (pointers owned by the comm).
    lshmoe_dispatch_p2p: centroids [m, d] (send layout; may be NULL when m == 0) + expert_rows [E]

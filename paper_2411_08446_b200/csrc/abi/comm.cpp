@@ -263,9 +263,12 @@ lshmoe_status lshmoe_comm_local_group(int world, int64_t recv_capacity, int64_t 
     for (int p = 0; p < world; ++p) cs[r]->peers[p] = cs[p]->window;   // same process: plain pointers
     cs[r]->p2p_grid = cs[r]->p2p_grid / world > 0 ? cs[r]->p2p_grid / world : 1;   // all ranks co-resident
     lshmoe_status st = p2p_publish_peers(cs[r]);
-    if (st) return st;
-    out[r] = cs[r];
+    if (st) {
+      for (int q = 0; q < world; ++q) lshmoe_comm_destroy(cs[q]);
+      return st;
+    }
   }
+  for (int r = 0; r < world; ++r) out[r] = cs[r];
   return LSHMOE_OK;
 }
 
