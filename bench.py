@@ -42,9 +42,10 @@ def parse():
                    help="hash family: cross-polytope (paper default, Eq. 3), spherical-plane (NEXT-3), or "
                         "cross-polytope on e4m3 operands (NEXT-2 fp8 option)")
     p.add_argument("--sp-bits", type=int, default=12, help="sign bits per SP hash function")
-    p.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
-                   help="a6/a8 at N>1: phase 1 (NCCL, one host count sync) or phase 2 (device-initiated stores "
-                        "into the peers' windows, no host sync, CUDA-graph captured)")
+    p.add_argument("--exchange", default="nccl", choices=["nccl", "p2p", "p2p-fused"],
+                   help="a6/a8 at N>1: phase 1 (NCCL, one host count sync), phase 2 (device-initiated stores "
+                        "into the peers' windows, no host sync, CUDA-graph captured), or phase 2 with the dispatch "
+                        "fused into the centroid kernel (lshmoe_compress_p2p)")
     p.add_argument("--share-gpu", action="store_true",
                    help="testing only: every rank on cuda:0 with a gloo group (p2p exchange); the line is "
                         "marked and is not a measurement")
@@ -224,7 +225,7 @@ def main():
     from lshmoe_inputs import make_experts, make_rank_inputs, rotation_seed
 
     if args.share_gpu:
-        assert args.exchange == "p2p", "--share-gpu needs --exchange p2p (NCCL refuses two ranks on one GPU)"
+        assert args.exchange != "nccl", "--share-gpu needs a phase-2 exchange (NCCL refuses two ranks on one GPU)"
         local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -235,7 +236,7 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
     assert cfg.E % world == 0, "experts must split evenly over ranks"
     E_local = cfg.E // world
-    p2p = args.exchange == "p2p"
+    p2p = args.exchange in ("p2p", "p2p-fused")
     if p2p:     # phase 2: a window per rank (receive + returned buffers), peers mapped over CUDA IPC
         comm = L.Comm(world, rank, None).p2p_init(cfg.n * cfg.k * world, cfg.n * cfg.k, cfg.d, X_dtype(cfg), cfg.E,
                                                   group=dist.group.WORLD if world > 1 else None)
@@ -285,7 +286,8 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     from lshmoe_inputs import make_experts, rotation_seed
     n, k, d = cfg.n, cfg.k, cfg.d
     nk = n * k
-    p2p = args.exchange == "p2p"
+    p2p = args.exchange in ("p2p", "p2p-fused")
+    fused = args.exchange == "p2p-fused"
 
     Nrm = L.sp_normals(R, args.sp_bits) if args.hash == "sp" else None
     R8 = L.rotation_e4m3(cfg.d, cfg.q, rotation_seed(args.seed)).to(dev) if args.hash == "cp8" else None
@@ -302,7 +304,9 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
             h = lambda: L.hash(Xb, R, codes)   # noqa: E731
         return [
             h,
-            lambda: L.compress(Xb, codes, zb, cfg.E, out=comp, workspace=ws),
+            (lambda: L.compress_p2p(comm, Xb, codes, zb, cfg.E, out=comp, workspace=ws)) if fused else
+            (lambda: L.compress(Xb, codes, zb, cfg.E, out=comp, workspace=ws)),
+            (lambda: None) if fused else
             (lambda: L.dispatch_p2p(comm, comp.centroids, comp.expert_rows)) if p2p else
             (lambda: L.dispatch(comm, comp.centroids, comp.expert_rows, cfg.E, recv, rr)),
             lambda: L.expert_ffn(recv, rr, W1, b1, W2, b2, out=eo, hidden=hid),
@@ -611,7 +615,9 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 "compression_ratio": ratio, "centroids": m, "routed_copies": nk,
                 "gpu_launches": launches_per_step * args.steps, "gpu_launches_per_step": launches_per_step,
                 "cuda_graph": use_graph,
-                "exchange": ("phase 2: device-initiated stores into the peers' windows (CUDA IPC), no host sync"
+                "exchange": ("phase 2 fused: the centroid kernel stores every centroid row into its owner's "
+                             "window (CUDA IPC), no host sync" if fused else
+                             "phase 2: device-initiated stores into the peers' windows (CUDA IPC), no host sync"
                              if p2p else "phase 1: NCCL all-gather of counts + grouped send/recv"
                              if world > 1 else "world 1: aliased (no copy)"),
                 "stages_ms": stage_ms, "eager_ms_per_step": eager_ms,

@@ -274,6 +274,18 @@ lshmoe_status lshmoe_comm_local_group(int world, int64_t recv_capacity, int64_t 
                                       int row_bytes, int num_experts, lshmoe_comm** out);
 lshmoe_status lshmoe_comm_p2p_buffers(lshmoe_comm* comm, void** recv, void** returned,
                                       int32_t** recv_rows);
+/* a3-a6 fused: lshmoe_compress whose centroid kernel also performs the phase-2 dispatch (Alg. 1 L8
+   and L14, SURVEY §8(e) "stores from the centroid kernel"): it posts this rank's per-expert counts,
+   reads every source's, and stores each centroid row into its owner's receive buffer as well as into
+   `centroids` (restore needs them); its last CTA completes the same flag handshake as
+   lshmoe_dispatch_p2p, so the receive buffer and recv_rows of comm's window are complete when it
+   ends and lshmoe_combine_p2p follows as usual.  Arguments as lshmoe_compress (no fp32 copy);
+   comm must have a phase-2 window for num_experts and rows of d elements. */
+lshmoe_status lshmoe_compress_p2p(lshmoe_comm* comm, const void* x, lshmoe_dtype dtype, int64_t n, int d,
+                                  const int16_t* codes, int q, const int32_t* experts, int k,
+                                  int num_experts, int32_t* bucket, int32_t* perm, int32_t* row_start,
+                                  int32_t* expert_rows, int32_t* num_rows, void* centroids,
+                                  void* workspace, size_t workspace_bytes, lshmoe_stream stream);
 lshmoe_status lshmoe_comm_p2p_error(lshmoe_comm* comm, int32_t* value /* [host] */, lshmoe_stream stream);
 lshmoe_status lshmoe_dispatch_p2p(lshmoe_comm* comm, const void* centroids, const int32_t* expert_rows,
                                   int grid, lshmoe_stream stream);

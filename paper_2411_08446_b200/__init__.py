@@ -71,6 +71,8 @@ _SIGS = {
     "lshmoe_comm_p2p_open": ([_vp, _vp], _i32),
     "lshmoe_comm_local_group": ([_i32, _i64, _i64, _i32, _i32, _vp], _i32),
     "lshmoe_comm_p2p_buffers": ([_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)], _i32),
+    "lshmoe_compress_p2p": ([_vp, _vp, _i32, _i64, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
+                             _vp, _sz, _vp], _i32),
     "lshmoe_comm_p2p_error": ([_vp, ctypes.POINTER(_i32), _vp], _i32),
     "lshmoe_dispatch_p2p": ([_vp, _vp, _vp, _i32, _vp], _i32),
     "lshmoe_combine_p2p": ([_vp, _vp, _i32, _vp], _i32),
@@ -388,6 +390,26 @@ def compress(x: torch.Tensor, codes: torch.Tensor, experts: torch.Tensor, num_ex
                                 _ptr(out.bucket), _ptr(out.perm), _ptr(out.row_start), _ptr(out.expert_rows),
                                 _ptr(out.num_rows), _ptr(out.centroids), _ptr(out.centroids_f32),
                                 _ptr(workspace), workspace.numel(), _stream(stream)), "lshmoe_compress")
+    return out
+
+
+def compress_p2p(comm: "Comm", x: torch.Tensor, codes: torch.Tensor, experts: torch.Tensor, num_experts: int,
+                 out: Optional[Compressed] = None, workspace: Optional[torch.Tensor] = None, stream=None) -> Compressed:
+    """compress fused with the phase-2 dispatch: the centroid kernel also stores every centroid row
+    into its owner's receive buffer (comm.p2p_buffers()[0]; counts in [2])."""
+    _require_cuda(x, codes, experts)
+    n, d = x.shape
+    k = experts.shape[1]
+    q = codes.shape[1]
+    if out is None:
+        out = alloc_compressed(n, k, num_experts, d, x.dtype, x.device)
+    wsb = compress_workspace_bytes(n, k, num_experts, q, d, x.dtype)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = compress_workspace(n, k, num_experts, q, d, x.dtype, x.device)
+    _check(_lib.lshmoe_compress_p2p(comm.handle, _ptr(x), _dt(x), n, d, _ptr(codes), q, _ptr(experts), k, num_experts,
+                                    _ptr(out.bucket), _ptr(out.perm), _ptr(out.row_start), _ptr(out.expert_rows),
+                                    _ptr(out.num_rows), _ptr(out.centroids), _ptr(workspace), workspace.numel(),
+                                    _stream(stream)), "lshmoe_compress_p2p")
     return out
 
 

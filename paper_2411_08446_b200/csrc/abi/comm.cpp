@@ -272,6 +272,7 @@ lshmoe_status lshmoe_comm_local_group(int world, int64_t recv_capacity, int64_t 
   return LSHMOE_OK;
 }
 
+
 lshmoe_status lshmoe_comm_p2p_buffers(lshmoe_comm* c, void** recv, void** returned, int32_t** recv_rows) {
   if (!c || !c->window) return set_error(LSHMOE_EINVAL, "lshmoe_comm_p2p_buffers: no phase-2 window");
   if (recv) *recv = c->window + c->L.recv;
@@ -466,3 +467,19 @@ lshmoe_status lshmoe_combine(lshmoe_comm* c, const void* expert_out, lshmoe_dtyp
 }
 
 }  // extern "C"
+
+namespace lshmoe {
+// Phase-2 window of `c` for the fused compress + dispatch (lshmoe_compress_p2p in lshmoe.cpp).
+int comm_p2p_fuse(lshmoe_comm* c, int E, P2PFuse* out) {
+  if (!c || !c->window || !c->peers_dev) return LSHMOE_EINVAL;
+  if (E != c->p2p_E) return LSHMOE_EINVAL;
+  out->peers = c->peers_dev;
+  out->L = c->L;
+  out->world = c->world;
+  out->me = c->rank;
+  out->done = c->done;
+  out->recv_rows = c->recv_rows_dev;
+  c->dispatched = true;
+  return LSHMOE_OK;
+}
+}  // namespace lshmoe

@@ -209,6 +209,36 @@ lshmoe_status lshmoe_compress(const void* x, lshmoe_dtype dtype, int64_t n, int 
   return cuda_status(err, "lshmoe_compress");
 }
 
+lshmoe_status lshmoe_compress_p2p(lshmoe_comm* comm, const void* x, lshmoe_dtype dtype, int64_t n, int d,
+                                  const int16_t* codes, int q, const int32_t* experts, int k, int E, int32_t* bucket,
+                                  int32_t* perm, int32_t* row_start, int32_t* expert_rows, int32_t* num_rows,
+                                  void* centroids, void* workspace, size_t workspace_bytes, lshmoe_stream stream) {
+  P2PFuse fuse;
+  REQUIRE(comm_p2p_fuse(comm, E, &fuse) == LSHMOE_OK, LSHMOE_EINVAL,
+          "comm has no phase-2 window for this number of experts (lshmoe_comm_p2p_init)");
+  REQUIRE(d * (dtype == LSHMOE_F32 ? 4 : 2) == fuse.L.row_bytes, LSHMOE_EINVAL, "row bytes differ from the window's");
+  lshmoe_status st = check_token_shape(__func__, dtype, n, d);
+  if (st) return st;
+  REQUIRE(q >= 1, LSHMOE_EINVAL, "q < 1");
+  REQUIRE(q <= LSHMOE_MAX_Q, LSHMOE_EUNSUPPORTED, "q > LSHMOE_MAX_Q");
+  REQUIRE(k >= 1 && E >= 1, LSHMOE_EINVAL, "k < 1 or E < 1");
+  REQUIRE(k <= E, LSHMOE_EINVAL, "k > E (S:L228)");
+  REQUIRE(n * k < (int64_t(1) << 31), LSHMOE_EUNSUPPORTED, "n * k >= 2^31");
+  REQUIRE(row_start && expert_rows && num_rows, LSHMOE_EINVAL, "NULL output pointer");
+  if (n > 0) {
+    REQUIRE(x && codes && experts && bucket && perm && centroids, LSHMOE_EINVAL, "NULL pointer");
+    REQUIRE(aligned16(x) && aligned16(centroids), LSHMOE_EINVAL, "x / centroids must be 16-byte aligned");
+  }
+  size_t need = compress_workspace_layout(n, k, E, d, nullptr, nullptr);
+  REQUIRE(workspace_bytes >= need, LSHMOE_EINVAL, "workspace too small (see lshmoe_compress_workspace)");
+  REQUIRE(need == 0 || (workspace && aligned16(workspace)), LSHMOE_EINVAL, "workspace NULL or misaligned");
+  CompressWs ws;
+  compress_workspace_layout(n, k, E, d, workspace, &ws);
+  int err = launch_compress(x, dtype, n, d, codes, q, experts, k, E, bucket, perm, row_start, expert_rows, num_rows,
+                            centroids, nullptr, ws, stream, &fuse);
+  return cuda_status(err, "lshmoe_compress_p2p");
+}
+
 lshmoe_status lshmoe_expert_ffn_backward(const void* grad_out, lshmoe_dtype dtype, int d, int d_ffn,
                                          const int32_t* recv_rows, int experts_local, int world, const void* W2T,
                                          const void* W1T, const void* hidden, void* dhidden, int64_t capacity,

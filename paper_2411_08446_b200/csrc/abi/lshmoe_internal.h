@@ -51,7 +51,8 @@ size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, Com
 int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int16_t* codes, int q,
                     const int32_t* experts, int k, int E, int32_t* bucket, int32_t* perm,
                     int32_t* row_start, int32_t* expert_rows, int32_t* num_rows, void* centroids,
-                    float* centroids_f32, const CompressWs& ws, void* stream);
+                    float* centroids_f32, const CompressWs& ws, void* stream,
+                    const struct P2PFuse* fuse = nullptr);
 
 int launch_permute(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int32_t* experts, int k,
                    int E, int32_t* slot, int32_t* expert_rows, void* send, const CompressWs& ws, void* stream);
@@ -96,6 +97,17 @@ struct P2PLayout {
   int row_bytes;
   int64_t bytes;                           // window size
 };
+// Phase-2 dispatch fused into the centroid kernel (lshmoe_compress_p2p): the kernel posts the counts,
+// reads every source's, and stores each centroid row straight into its owner's receive buffer too.
+struct P2PFuse {
+  uint8_t* const* peers;     // device [world] window bases
+  P2PLayout L;
+  int world, me;
+  unsigned* done;            // [0] arrivals, [1] errors, [2] epoch
+  int32_t* recv_rows;        // device [E/world][world] out
+};
+int comm_p2p_fuse(::lshmoe_comm* c, int E, P2PFuse* out);   // comm.cpp: LSHMOE_OK or EINVAL
+
 int launch_p2p(int which, uint8_t* const* peers_dev, const P2PLayout& L, int world, int me, int E, const void* src,
                const int32_t* expert_rows, int32_t* recv_rows, unsigned* done, int grid, void* stream);
 

@@ -120,7 +120,19 @@ struct Params {
   int grad;                        // 1: NEXT-1 grad_compress: weighted per-row SUMS (no 1/count)
   const float* gw;                 // grad: gate weights [nk] or nullptr (weight 1)
   int diag;                        // 1: record per-CTA globaltimer stamps (diagnostics)
+  // phase-2 dispatch fused into K3 (lshmoe_compress_p2p); p2p_peers == nullptr: off
+  uint8_t* const* p2p_peers;
+  int64_t p2p_mailbox, p2p_recv, p2p_data_flag, p2p_recv_cap;
+  int p2p_world, p2p_me;
+  unsigned* p2p_done;
+  int32_t* p2p_recv_rows;
 };
+
+// K3's fused-dispatch tables (shared, set once per CTA): first global row of each expert and the
+// destination row, in its owner's receive buffer, of this rank's first row of each expert.
+__shared__ int g_f_roff[257];
+__shared__ long long g_f_dst[256];
+
 
 __device__ __forceinline__ unsigned globaltimer_lo() {
   unsigned t;
@@ -1026,6 +1038,134 @@ __device__ void gather_rows(const Params& P) {   // baseline: send[p] = x[token 
   }
 }
 
+// ---- fused phase-2 dispatch (lshmoe_compress_p2p; the protocol of p2p.cu's dispatch_p2p_kernel) ----
+__device__ __forceinline__ void st_rel_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acq_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_rlx_sys64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint64_t* f_slot(const Params& P, int rank, uint32_t ep, int src, int e) {
+  return reinterpret_cast<uint64_t*>(P.p2p_peers[rank] + P.p2p_mailbox) +
+         (static_cast<int64_t>(ep & 1) * P.p2p_world + src) * P.E + e;
+}
+constexpr uint64_t kFuseSpinNs = 10ull * 1000 * 1000 * 1000;   // a peer that never arrives traps
+
+// CTA 0 posts this rank's counts (epoch-tagged words) into every peer's mailbox; every CTA reads all
+// sources' counts, then the destination base of each of its experts' rows in the owner's receive
+// layout (local expert, source, bucket; reading R24).  CTA 0 also writes recv_rows.
+__device__ void fused_prologue(const Params& P, const int* s_roff, const int* s_mrow, uint32_t* epoch_out) {
+  int* s_fc = reinterpret_cast<int*>(g_dsmem);   // [w][E] counts: the ring is not in use yet
+  const int tid = threadIdx.x, E = P.E, w = P.p2p_world, epr = E / w;
+  const uint32_t ep = *reinterpret_cast<volatile unsigned*>(P.p2p_done + 2) + 1u;
+  *epoch_out = ep;
+  if (blockIdx.x == 0)
+    for (int i = tid; i < w * E; i += kThreads) {
+      const int p = i / E, e = i - p * E;
+      const uint64_t v = (static_cast<uint64_t>(ep) << 32) | static_cast<uint32_t>(s_mrow[e]);
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(f_slot(P, p, ep, P.p2p_me, e)), "l"(v) : "memory");
+    }
+  const uint64_t t0 = gtimer();
+  for (int i = tid; i < w * E; i += kThreads) {
+    const int src = i / E, e = i - src * E;
+    uint64_t v = ld_rlx_sys64(f_slot(P, P.p2p_me, ep, src, e));
+    while (static_cast<uint32_t>(v >> 32) != ep) {
+      __nanosleep(32);
+      if (gtimer() - t0 > kFuseSpinNs) __trap();
+      v = ld_rlx_sys64(f_slot(P, P.p2p_me, ep, src, e));
+    }
+    s_fc[i] = static_cast<int>(v & 0xffffffffu);
+  }
+  __syncthreads();
+  for (int e = tid; e <= E; e += kThreads) g_f_roff[e] = s_roff[e];
+  for (int e = tid; e < E; e += kThreads) {
+    const int p = e / epr, el = e - p * epr;
+    long long b = 0;
+    for (int e2 = 0; e2 < el; ++e2)
+      for (int s2 = 0; s2 < w; ++s2) b += s_fc[s2 * E + p * epr + e2];
+    for (int s2 = 0; s2 < P.p2p_me; ++s2) b += s_fc[s2 * E + p * epr + el];
+    g_f_dst[e] = b;
+  }
+  if (blockIdx.x == 0 && P.p2p_recv_rows)
+    for (int i = tid; i < epr * w; i += kThreads) {
+      const int el = i / w, s2 = i - el * w;
+      P.p2p_recv_rows[i] = s_fc[s2 * E + P.p2p_me * epr + el];
+    }
+  __syncthreads();
+}
+
+// After every CTA's stores (the kernel's final barrier): arrive on the local counter (gpu-scope
+// acq_rel); the last CTA issues one system-scope fence, records the epoch, raises data_flag[me] on
+// every peer and waits until every source raised this rank's: the receive buffer is complete.
+// After the centroid phase and the cut-row merges (kernel barrier): this CTA copies the centroid
+// rows it finalised — rows lying wholly in its perm range, and the cut rows it merged as the last
+// arriver (s_job) — from `centroids` to their owners' receive buffers, 16-byte chunks over all
+// threads.  Kept out of the reduction loop so the unfused kernel's hot path is unchanged.
+__device__ __forceinline__ void fused_copy_rows(const Params& P, const CentroidCtx& X, const int* s_job) {
+  int* s_n = reinterpret_cast<int*>(g_dsmem);          // [0] count, then row ids (the ring is free)
+  int* s_rows = s_n + 1;
+  if (threadIdx.x == 0) *s_n = 0;
+  __syncthreads();
+  if (X.range > 0)
+    for (int p = X.p_begin + threadIdx.x; p < X.p_end; p += kThreads) {
+      const uint32_t r = X.row_at(p);
+      if (X.row_at(p - 1) != r && X.row_at(X.p_end) != r) s_rows[atomicAdd(s_n, 1)] = static_cast<int>(r);
+    }
+  if (threadIdx.x == 0 && X.range > 0)      // (s_job is only written for a non-empty range)
+    for (int j = 0; j < 2; ++j)
+      if (s_job[4 * j] >= 0) s_rows[atomicAdd(s_n, 1)] = s_job[4 * j];
+  __syncthreads();
+  const int nr = *s_n, nch = P.row_bytes / 16;
+  for (int i = threadIdx.x; i < nr * nch; i += kThreads) {
+    const int k = i / nch, ch = i - k * nch;
+    const int row = s_rows[k];
+    int lo = 0, hi = P.E - 1;               // expert of global row `row`
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (g_f_roff[mid] <= row) lo = mid; else hi = mid - 1;
+    }
+    const int64_t drow = g_f_dst[lo] + (row - g_f_roff[lo]);
+    if (drow >= P.p2p_recv_cap) {           // the owner's receive buffer is too small: drop, flag
+      atomicOr(P.p2p_done + 1, 1u);
+      continue;
+    }
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(P.cent + static_cast<int64_t>(row) * P.row_bytes) + ch);
+    reinterpret_cast<uint4*>(P.p2p_peers[lo / (P.E / P.p2p_world)] + P.p2p_recv + drow * P.row_bytes)[ch] = v;
+  }
+  __syncthreads();
+}
+
+__device__ void fused_close(const Params& P, uint32_t ep) {
+  if (threadIdx.x != 0) return;
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(P.p2p_done) : "memory");
+  if (old != gridDim.x - 1) return;
+  __threadfence_system();
+  *P.p2p_done = 0;
+  P.p2p_done[2] = ep;
+  for (int p = 0; p < P.p2p_world; ++p)
+    st_rel_sys(reinterpret_cast<uint32_t*>(P.p2p_peers[p] + P.p2p_data_flag) + P.p2p_me, ep);
+  const uint32_t* fl = reinterpret_cast<const uint32_t*>(P.p2p_peers[P.p2p_me] + P.p2p_data_flag);
+  const uint64_t t0 = gtimer();
+  for (int s2 = 0; s2 < P.p2p_world; ++s2)
+    while (static_cast<int32_t>(ld_acq_sys(fl + s2) - ep) < 0) {
+      __nanosleep(64);
+      if (gtimer() - t0 > kFuseSpinNs) __trap();
+    }
+}
+
 // ---- K3 ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   __shared__ int s_goff[kRadix + 1];         // perm offset of each expert group
@@ -1067,6 +1207,8 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   }
   for (int e = blockIdx.x; e < P.E; e += gridDim.x)   // row_start of every global row
     for (int r = tid; r < s_mrow[e]; r += kThreads) P.row_start[s_roff[e] + r] = ldcg(P.rsl + s_goff[e] + r);
+  uint32_t f_epoch = 0;
+  if (P.p2p_peers) fused_prologue(P, s_roff, s_mrow, &f_epoch);
   // per-CTA centroid-phase start / end stamps (diagnostics, bar[64 + 2 * cta])
   if (P.diag && tid == 0 && blockIdx.x < 1024) P.bar[64 + 2 * blockIdx.x] = globaltimer_lo();
   CentroidCtx X;
@@ -1080,6 +1222,10 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
     merge_cut_rows<float>(P, X, s_goff, s_mrow, s_cut, s_job);
   }
   __syncthreads();
+  if (P.p2p_peers) {
+    fused_copy_rows(P, X, s_job);
+    fused_close(P, f_epoch);
+  }
   dstamp(P, 2, 3);
   if (P.diag && tid == 0 && blockIdx.x < 1024) P.bar[65 + 2 * blockIdx.x] = globaltimer_lo();
 }
@@ -1337,7 +1483,7 @@ static Params base_params(const void* x, lshmoe_dtype dtype, int64_t n, int d, c
 int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int16_t* codes, int q,
                     const int32_t* experts, int k, int E, int32_t* bucket, int32_t* perm, int32_t* row_start,
                     int32_t* expert_rows, int32_t* num_rows, void* centroids, float* centroids_f32,
-                    const CompressWs& ws, void* stream) {
+                    const CompressWs& ws, void* stream, const P2PFuse* fuse) {
   if (E > kMaxE || q > kMaxQ) return cudaErrorInvalidValue;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nk = static_cast<int>(n * k);
@@ -1345,7 +1491,11 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
   if (nk == 0) {
     if ((err = cudaMemsetAsync(expert_rows, 0, sizeof(int32_t) * E, st))) return err;
     if ((err = cudaMemsetAsync(num_rows, 0, sizeof(int32_t), st))) return err;
-    return cudaMemsetAsync(row_start, 0, sizeof(int32_t), st);
+    if ((err = cudaMemsetAsync(row_start, 0, sizeof(int32_t), st))) return err;
+    if (fuse)   // no rows: the standalone dispatch kernel still posts the zero counts and handshakes
+      return launch_p2p(0, fuse->peers, fuse->L, fuse->world, fuse->me, E, nullptr, expert_rows, fuse->recv_rows,
+                        fuse->done, 2 * device_sm_count(), stream);
+    return 0;
   }
   // The workspace is at rest between calls (hash table slots and arrival counters -1: K3 resets
   // the table, the last arriver its counter); the diagnostics stamps are cleared only when on.
@@ -1360,6 +1510,17 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
   P.num_rows = num_rows;
   P.cent = static_cast<uint8_t*>(centroids);
   P.cent32 = centroids_f32;
+  if (fuse) {
+    P.p2p_peers = fuse->peers;
+    P.p2p_mailbox = fuse->L.mailbox;
+    P.p2p_recv = fuse->L.recv;
+    P.p2p_data_flag = fuse->L.data_flag;
+    P.p2p_recv_cap = fuse->L.recv_capacity;
+    P.p2p_world = fuse->world;
+    P.p2p_me = fuse->me;
+    P.p2p_done = fuse->done;
+    P.p2p_recv_rows = fuse->recv_rows;
+  }
   return launch_chain(P, st);
 }
 

@@ -41,7 +41,7 @@ def _inputs(cfg, world):
     return R64, Xs, zs, make_experts(cfg, 0)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, fused=False):
     try:
         sys.path.insert(0, ROOT)
         import torch.distributed as dist
@@ -64,8 +64,11 @@ def _worker(rank, world, port, q):
         comm = L.Comm(world, rank, None).p2p_init(world * nk, nk, cfg.d, X.dtype, cfg.E, group=dist.group.WORLD)
         for it in range(2):                                   # twice: the second call reuses the windows
             codes = L.hash(X, R)
-            out = L.compress(X, codes, zeta, cfg.E)
-            L.dispatch_p2p(comm, out.centroids, out.expert_rows)
+            if fused:                                         # the centroid kernel stores to the owners
+                out = L.compress_p2p(comm, X, codes, zeta, cfg.E)
+            else:
+                out = L.compress(X, codes, zeta, cfg.E)
+                L.dispatch_p2p(comm, out.centroids, out.expert_rows)
             recv, ret, rr = comm.p2p_buffers()
             eo = L.expert_ffn(recv, rr, *W)
             L.combine_p2p(comm, eo)
@@ -87,11 +90,12 @@ def _worker(rank, world, port, q):
         q.put((rank, repr(exc)))
 
 
-def test_layer_two_ranks_p2p_matches_oracle():
+@pytest.mark.parametrize("fused", [False, True], ids=["dispatch_p2p", "compress_p2p"])
+def test_layer_two_ranks_p2p_matches_oracle(fused):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, fused)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=280) for _ in procs)
