@@ -133,6 +133,21 @@ struct Params {
 __shared__ int g_f_roff[257];
 __shared__ long long g_f_dst[256];
 
+// Destination of centroid row `row` in its owner's receive buffer (nullptr: over capacity, flagged).
+__device__ __forceinline__ uint8_t* fused_row_dst(const Params& P, int row) {
+  int lo = 0, hi = P.E - 1;                 // expert of global row `row`: last e with roff[e] <= row
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (g_f_roff[mid] <= row) lo = mid; else hi = mid - 1;
+  }
+  const int64_t drow = g_f_dst[lo] + (row - g_f_roff[lo]);
+  if (drow >= P.p2p_recv_cap) {             // the owner's receive buffer is too small: drop, flag
+    atomicOr(P.p2p_done + 1, 1u);
+    return nullptr;
+  }
+  return P.p2p_peers[lo / (P.E / P.p2p_world)] + P.p2p_recv + drow * P.row_bytes;
+}
+
 
 __device__ __forceinline__ unsigned globaltimer_lo() {
   unsigned t;
@@ -636,7 +651,7 @@ __device__ __noinline__ void store_f32_copy(float* dst, const float* v) {   // t
 }
 
 // centroid = acc * rc, rc = RN(1/count) (reading R10), RNE to the wire dtype; fp32 copy if requested.
-template <typename T>
+template <typename T, bool kF = false>
 __device__ __forceinline__ void store_chunk16(const Params& P, int row, int c16, const float* acc, float rc) {
   constexpr int VC = 16 / sizeof(T);
   float v[VC];
@@ -655,6 +670,10 @@ __device__ __forceinline__ void store_chunk16(const Params& P, int row, int c16,
     out = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
   }
   *reinterpret_cast<uint4*>(P.cent + static_cast<int64_t>(row) * P.row_bytes + 16 * c16) = out;
+  if constexpr (kF) {                        // fused dispatch: the row also goes to its owner
+    uint8_t* dst = fused_row_dst(P, row);
+    if (dst) *reinterpret_cast<uint4*>(dst + 16 * c16) = out;
+  }
   if (P.cent32) store_f32_copy<VC>(P.cent32 + static_cast<int64_t>(row) * P.d + c16 * VC, v);
 }
 
@@ -672,7 +691,7 @@ __device__ __forceinline__ void add_chunk8(float* acc, uint2 raw) {
 }
 
 // centroid = acc * RN(1/count) (reading R10), RNE to the wire dtype; fp32 copy if requested.
-template <typename T>
+template <typename T, bool kF = false>
 __device__ __forceinline__ void store_chunk8(const Params& P, int row, int ch, const float* acc, float cnt) {
   constexpr int VC = sizeof(T) == 2 ? 4 : 2;
   const float rc = P.grad ? 1.0f : __frcp_rn(cnt);
@@ -688,6 +707,10 @@ __device__ __forceinline__ void store_chunk8(const Params& P, int row, int ch, c
     out = make_uint2(__float_as_uint(v[0]), __float_as_uint(v[1]));
   }
   *reinterpret_cast<uint2*>(P.cent + static_cast<int64_t>(row) * P.row_bytes + 8 * ch) = out;
+  if constexpr (kF) {
+    uint8_t* dst = fused_row_dst(P, row);
+    if (dst) *reinterpret_cast<uint2*>(dst + 8 * ch) = out;
+  }
   if (P.cent32) {
     float* dst = P.cent32 + static_cast<int64_t>(row) * P.d + ch * VC;
 #pragma unroll
@@ -731,7 +754,7 @@ struct CentroidCtx {                     // one CTA's view of its perm range (ce
 
 // One column block (chunks [c0, c0 + ncb), CPL = ceil(ncb / 32) chunks per lane) of the centroid
 // phase: stream the warp's rows through its ring, reduce segments, then combine cut rows.
-template <typename T, int CPL, int QD = kQ>
+template <typename T, int CPL, int QD = kQ, bool kF = false>
 __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, int c0, int ncb) {
   const int slotB = 16 * CPL * 32;           // packed ring slot (this block's row bytes, rounded to a lane round)
   constexpr int VC = 16 / sizeof(T);
@@ -782,7 +805,7 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
 #pragma unroll
       for (int t = 0; t < CPL; ++t) {
         const int c = lane + 32 * t;
-        if (full || c < ncb) store_chunk16<T>(P, static_cast<int>(row), c0 + c, acc[t], rc);
+        if (full || c < ncb) store_chunk16<T, kF>(P, static_cast<int>(row), c0 + c, acc[t], rc);
       }
     } else if (p + 1 == w_end) {
       break;                                  // the last segment stays in acc (partial, see below)
@@ -852,7 +875,7 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
 #pragma unroll
         for (int e = 0; e < VC; ++e) dst[e] = v[e];
       } else {
-        store_chunk16<T>(P, static_cast<int>(r), c0 + c, v, rc);
+        store_chunk16<T, kF>(P, static_cast<int>(r), c0 + c, v, rc);
       }
     }
   };
@@ -897,7 +920,7 @@ __device__ __forceinline__ void prefetch_cut_extent(const Params& P, CentroidCtx
 // Phase B of one CTA: its perm range's rows (global ids = row offset of the expert + local row),
 // token ids and bucket outputs, then the centroid reduction.  s_cut[0..1] receive the (expert,
 // local row) of the range's first and last entries for the cut-row merge.
-template <typename T>
+template <typename T, bool kF = false>
 __device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_roff, const int* s_mrow, int* s_cut,
                                CentroidCtx& X) {
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
@@ -936,10 +959,10 @@ __device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_
   for (int c0 = 0, cb = 0; c0 < P.nch; c0 += kBlkChunks, ++cb) {
     const int ncb = min(kBlkChunks, P.nch - c0);
     switch ((ncb + 31) / 32) {
-      case 1: centroid_block<T, 1, 16>(P, X, cb, c0, ncb); break;
-      case 2: centroid_block<T, 2, 16>(P, X, cb, c0, ncb); break;
-      case 3: centroid_block<T, 3, 13>(P, X, cb, c0, ncb); break;
-      default: centroid_block<T, 4>(P, X, cb, c0, ncb); break;
+      case 1: centroid_block<T, 1, 16, kF>(P, X, cb, c0, ncb); break;
+      case 2: centroid_block<T, 2, 16, kF>(P, X, cb, c0, ncb); break;
+      case 3: centroid_block<T, 3, 13, kF>(P, X, cb, c0, ncb); break;
+      default: centroid_block<T, 4, kQ, kF>(P, X, cb, c0, ncb); break;
     }
   }
 }
@@ -952,7 +975,7 @@ __device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_
 #endif
 constexpr int kMergeBatch = LSHMOE_MERGE_BATCH;   // partials of a cut row loaded before any is added
 
-template <typename T>
+template <typename T, bool kF = false>
 __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int* s_goff, const int* s_mrow,
                                const int* s_cut, int* s_job) {
   constexpr int VC = sizeof(T) == 2 ? 4 : 2;
@@ -1020,7 +1043,7 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
 #pragma unroll
             for (int e = 0; e < VC; ++e) acc[e] += tmp[u][e];
       }
-      store_chunk8<T>(P, row, ch, acc, static_cast<float>(re - rs));
+      store_chunk8<T, kF>(P, row, ch, acc, static_cast<float>(re - rs));
     }
   }
 }
@@ -1109,44 +1132,6 @@ __device__ void fused_prologue(const Params& P, const int* s_roff, const int* s_
 // After every CTA's stores (the kernel's final barrier): arrive on the local counter (gpu-scope
 // acq_rel); the last CTA issues one system-scope fence, records the epoch, raises data_flag[me] on
 // every peer and waits until every source raised this rank's: the receive buffer is complete.
-// After the centroid phase and the cut-row merges (kernel barrier): this CTA copies the centroid
-// rows it finalised — rows lying wholly in its perm range, and the cut rows it merged as the last
-// arriver (s_job) — from `centroids` to their owners' receive buffers, 16-byte chunks over all
-// threads.  Kept out of the reduction loop so the unfused kernel's hot path is unchanged.
-__device__ __forceinline__ void fused_copy_rows(const Params& P, const CentroidCtx& X, const int* s_job) {
-  int* s_n = reinterpret_cast<int*>(g_dsmem);          // [0] count, then row ids (the ring is free)
-  int* s_rows = s_n + 1;
-  if (threadIdx.x == 0) *s_n = 0;
-  __syncthreads();
-  if (X.range > 0)
-    for (int p = X.p_begin + threadIdx.x; p < X.p_end; p += kThreads) {
-      const uint32_t r = X.row_at(p);
-      if (X.row_at(p - 1) != r && X.row_at(X.p_end) != r) s_rows[atomicAdd(s_n, 1)] = static_cast<int>(r);
-    }
-  if (threadIdx.x == 0 && X.range > 0)      // (s_job is only written for a non-empty range)
-    for (int j = 0; j < 2; ++j)
-      if (s_job[4 * j] >= 0) s_rows[atomicAdd(s_n, 1)] = s_job[4 * j];
-  __syncthreads();
-  const int nr = *s_n, nch = P.row_bytes / 16;
-  for (int i = threadIdx.x; i < nr * nch; i += kThreads) {
-    const int k = i / nch, ch = i - k * nch;
-    const int row = s_rows[k];
-    int lo = 0, hi = P.E - 1;               // expert of global row `row`
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (g_f_roff[mid] <= row) lo = mid; else hi = mid - 1;
-    }
-    const int64_t drow = g_f_dst[lo] + (row - g_f_roff[lo]);
-    if (drow >= P.p2p_recv_cap) {           // the owner's receive buffer is too small: drop, flag
-      atomicOr(P.p2p_done + 1, 1u);
-      continue;
-    }
-    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(P.cent + static_cast<int64_t>(row) * P.row_bytes) + ch);
-    reinterpret_cast<uint4*>(P.p2p_peers[lo / (P.E / P.p2p_world)] + P.p2p_recv + drow * P.row_bytes)[ch] = v;
-  }
-  __syncthreads();
-}
-
 __device__ void fused_close(const Params& P, uint32_t ep) {
   if (threadIdx.x != 0) return;
   unsigned old;
@@ -1167,6 +1152,9 @@ __device__ void fused_close(const Params& P, uint32_t ep) {
 }
 
 // ---- K3 ------------------------------------------------------------------------------------
+// kF: the fused dispatch (lshmoe_compress_p2p) — compiled separately, so the plain kernel's
+// reduction loop carries no remote-store code.
+template <bool kF>
 __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   __shared__ int s_goff[kRadix + 1];         // perm offset of each expert group
   __shared__ int s_roff[kRadix + 1];         // first global row of each expert
@@ -1208,24 +1196,21 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   for (int e = blockIdx.x; e < P.E; e += gridDim.x)   // row_start of every global row
     for (int r = tid; r < s_mrow[e]; r += kThreads) P.row_start[s_roff[e] + r] = ldcg(P.rsl + s_goff[e] + r);
   uint32_t f_epoch = 0;
-  if (P.p2p_peers) fused_prologue(P, s_roff, s_mrow, &f_epoch);
+  if constexpr (kF) fused_prologue(P, s_roff, s_mrow, &f_epoch);
   // per-CTA centroid-phase start / end stamps (diagnostics, bar[64 + 2 * cta])
   if (P.diag && tid == 0 && blockIdx.x < 1024) P.bar[64 + 2 * blockIdx.x] = globaltimer_lo();
   CentroidCtx X;
   if (P.is_bf16) {
-    centroid_phase<__nv_bfloat16>(P, s_goff, s_roff, s_mrow, s_cut, X);
+    centroid_phase<__nv_bfloat16, kF>(P, s_goff, s_roff, s_mrow, s_cut, X);
     dstamp(P, 2, 2);
-    merge_cut_rows<__nv_bfloat16>(P, X, s_goff, s_mrow, s_cut, s_job);
+    merge_cut_rows<__nv_bfloat16, kF>(P, X, s_goff, s_mrow, s_cut, s_job);
   } else {
-    centroid_phase<float>(P, s_goff, s_roff, s_mrow, s_cut, X);
+    centroid_phase<float, kF>(P, s_goff, s_roff, s_mrow, s_cut, X);
     dstamp(P, 2, 2);
-    merge_cut_rows<float>(P, X, s_goff, s_mrow, s_cut, s_job);
+    merge_cut_rows<float, kF>(P, X, s_goff, s_mrow, s_cut, s_job);
   }
   __syncthreads();
-  if (P.p2p_peers) {
-    fused_copy_rows(P, X, s_job);
-    fused_close(P, f_epoch);
-  }
+  if constexpr (kF) fused_close(P, f_epoch);   // every row was stored to its owner in the loop
   dstamp(P, 2, 3);
   if (P.diag && tid == 0 && blockIdx.x < 1024) P.bar[65 + 2 * blockIdx.x] = globaltimer_lo();
 }
@@ -1343,7 +1328,8 @@ int launch_chain(const Params& P, cudaStream_t st) {
   const int csmem = centroid_smem(max_range);
   if (!P.permute && csmem > kCentroidSmemMax) return cudaErrorInvalidValue;   // range too long
   if (!configured) {
-    int err = cudaFuncSetAttribute(centroid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCentroidSmemMax);
+    int err = cudaFuncSetAttribute(centroid_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCentroidSmemMax);
+    if (!err) err = cudaFuncSetAttribute(centroid_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCentroidSmemMax);
     if (!err) err = cudaFuncSetAttribute(bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBucketSmem);
     if (err) return err;
     configured = true;
@@ -1355,7 +1341,8 @@ int launch_chain(const Params& P, cudaStream_t st) {
   p.cs = bucket_cluster_size(P.E);
   int err = launch_pdl(tile_kernel, P.ntiles, kThreads, 0, st, p, true);
   if (!err) err = launch_pdl(bucket_kernel, P.E * p.cs, kBThreads, kBucketSmem, st, p, true, p.cs);
-  if (!err) err = launch_pdl(centroid_kernel, centroid_grid(), kThreads, P.permute ? 0 : csmem, st, p, true);
+  if (!err) err = p.p2p_peers ? launch_pdl(centroid_kernel<true>, centroid_grid(), kThreads, csmem, st, p, true)
+                              : launch_pdl(centroid_kernel<false>, centroid_grid(), kThreads, P.permute ? 0 : csmem, st, p, true);
   return err;
 }
 
