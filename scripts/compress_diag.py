@@ -10,6 +10,7 @@ import paper_2411_08446_b200 as L  # noqa: E402
 from lshmoe_inputs import CONFIGS, make_gate, make_tokens, rotation_seed  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
+fused = len(sys.argv) > 2 and sys.argv[2] == "fused"   # lshmoe_compress_p2p at world 1
 cfg = CONFIGS[name]
 X = make_tokens(cfg, 0)
 zeta, _ = make_gate(cfg, 0, X)
@@ -21,18 +22,21 @@ ws = torch.full((L.compress_workspace_bytes(cfg.n, cfg.k, cfg.E, cfg.q, cfg.d, X
 out = L.alloc_compressed(cfg.n, cfg.k, cfg.E, cfg.d, X.dtype, "cuda")
 G = torch.cuda.get_device_properties(0).multi_processor_count
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+comm = L.Comm(1, 0).p2p_init(nk, nk, cfg.d, X.dtype, cfg.E) if fused else None
+run = (lambda: L.compress_p2p(comm, Xd, codes, zd, cfg.E, out=out, workspace=ws)) if fused else \
+    (lambda: L.compress(Xd, codes, zd, cfg.E, out=out, workspace=ws))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 times = []
 for it in range(20):
     flush.zero_()
     ev[0].record()
-    L.compress(Xd, codes, zd, cfg.E, out=out, workspace=ws)
+    run()
     ev[1].record()
     torch.cuda.synchronize()
     times.append(ev[0].elapsed_time(ev[1]) * 1e3)
 print(f"{name}: compress event time us: median {np.median(times[5:]):.1f} min {min(times[5:]):.1f}")
 L.set_diagnostics(True)
-L.compress(Xd, codes, zd, cfg.E, out=out, workspace=ws)
+run()
 torch.cuda.synchronize()
 L.set_diagnostics(False)
 print("kernel spans", L.compress_phase_times(ws))
