@@ -51,3 +51,8 @@ for kern, st in L.compress_diag(ws).items():
         print(f"  {k:12s} max {np.nanmax(v):7.2f}  med {np.nanmedian(v):7.2f}  min {np.nanmin(v):7.2f}  argmax {int(np.nanargmax(v))}")
     crit = int(np.nanargmax(D["end"]))
     print("  critical CTA", crit, {k: round(float(D[k][crit]), 2) for k in D})
+if fused:
+    comm.p2p_check()                          # raises if any row was dropped (capacity)
+    recv, _, rr = comm.p2p_buffers()
+    m = int(out.num_rows.item())
+    print("fused: rows delivered match the centroids:", bool(torch.equal(recv[:m], out.centroids[:m])))
