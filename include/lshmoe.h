@@ -59,7 +59,8 @@ typedef enum {
                               n * k >= 2^31 */
   LSHMOE_ECUDA = 3,        /* CUDA runtime / launch error */
   LSHMOE_ENCCL = 4,        /* NCCL error, including ncclCommGetAsyncError */
-  LSHMOE_EDEVICE = 5       /* device-side validation failed (expert id outside [0, E));
+  LSHMOE_EDEVICE = 5       /* device-side validation failed (expert id outside [0, E), S:L312;
+                              an expert repeated among a token's k slots, "distinct");
                               latched in a device error word, reported by the next call that
                               synchronises (lshmoe_dispatch at world > 1, lshmoe_check_device_error) */
 } lshmoe_status;
@@ -89,7 +90,7 @@ lshmoe_status lshmoe_check_device_error(lshmoe_stream stream);
    rotation_seed ^ (0x9E3779B97F4A7C15 * (j+1)), Irwin-Hall(12) approximately-Gaussian G_j,
    modified Gram-Schmidt over the columns of G_j in fp64 with left-to-right sums and no FMA,
    R_j = Q_j^T, rounded fp64 -> fp32 (RNE) -> bf16 (RNE) for bf16.  Pure host function,
-   deterministic, bit-identical to the independent oracle (tests/test_abi_rotation.py). */
+   deterministic, bit-identical to the independent oracle (tests/test_abi.py, T0). */
 lshmoe_status lshmoe_rotation(int d, int q, uint64_t rotation_seed, lshmoe_dtype dtype, void* out);
 
 /* ---- a2: cross-polytope hash, Eq. 3 --------------------------------------------
@@ -262,8 +263,10 @@ lshmoe_status lshmoe_combine(lshmoe_comm* comm, const void* expert_out, lshmoe_d
    Capacities must be equal on every rank.  Rows that would land past a receive / returned buffer
    are dropped and flagged on the sending rank; lshmoe_comm_p2p_error synchronises `stream`, reads
    and clears the flags (value bit 0: a receive buffer overflowed, bit 1: a returned buffer) and
-   returns LSHMOE_EDEVICE when any is set.  A peer that never joins a call makes the waiting kernel
-   trap after 10 s (sticky CUDA error) rather than hang the device. */
+   returns LSHMOE_EDEVICE when any is set.  A peer that never joins a call (or falls further behind
+   than the spin limit, LSHMOE_P2P_TIMEOUT_S seconds, default 300) does not hang the device: the
+   waiting kernel gives up, sets value bit 2 and finishes; that call's results are invalid and
+   lshmoe_comm_p2p_error returns LSHMOE_EDEVICE (no trap, so the CUDA context survives). */
 lshmoe_status lshmoe_comm_p2p_init(lshmoe_comm* comm, int64_t recv_capacity, int64_t ret_capacity,
                                    int row_bytes, int num_experts);
 lshmoe_status lshmoe_comm_p2p_alloc(lshmoe_comm* comm, int64_t recv_capacity, int64_t ret_capacity,
@@ -280,13 +283,20 @@ lshmoe_status lshmoe_comm_p2p_buffers(lshmoe_comm* comm, void** recv, void** ret
    `centroids` (restore needs them); its last CTA completes the same flag handshake as
    lshmoe_dispatch_p2p, so the receive buffer and recv_rows of comm's window are complete when it
    ends and lshmoe_combine_p2p follows as usual.  Arguments as lshmoe_compress (no fp32 copy);
-   comm must have a phase-2 window for num_experts and rows of d elements. */
+   comm must have a phase-2 window for num_experts and rows of d elements.  The kernel occupies every
+   SM (one CTA each) and spins on its peers, so every rank needs its own GPU: a local group at
+   world > 1 (or ranks sharing a GPU under MPS) returns LSHMOE_EUNSUPPORTED — use lshmoe_compress +
+   lshmoe_dispatch_p2p there.  Arguments are validated before anything is launched; only a launched
+   call licenses the following lshmoe_combine_p2p. */
 lshmoe_status lshmoe_compress_p2p(lshmoe_comm* comm, const void* x, lshmoe_dtype dtype, int64_t n, int d,
                                   const int16_t* codes, int q, const int32_t* experts, int k,
                                   int num_experts, int32_t* bucket, int32_t* perm, int32_t* row_start,
                                   int32_t* expert_rows, int32_t* num_rows, void* centroids,
                                   void* workspace, size_t workspace_bytes, lshmoe_stream stream);
 lshmoe_status lshmoe_comm_p2p_error(lshmoe_comm* comm, int32_t* value /* [host] */, lshmoe_stream stream);
+/* Peer-wait limit of this comm's phase-2 kernels, in seconds (> 0; default LSHMOE_P2P_TIMEOUT_S or
+   300).  Applies to calls issued afterwards (a captured graph keeps the value it was captured with). */
+lshmoe_status lshmoe_comm_p2p_set_timeout(lshmoe_comm* comm, double seconds);
 lshmoe_status lshmoe_dispatch_p2p(lshmoe_comm* comm, const void* centroids, const int32_t* expert_rows,
                                   int grid, lshmoe_stream stream);
 lshmoe_status lshmoe_combine_p2p(lshmoe_comm* comm, const void* expert_out, int grid,

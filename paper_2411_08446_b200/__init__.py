@@ -74,6 +74,7 @@ _SIGS = {
     "lshmoe_compress_p2p": ([_vp, _vp, _i32, _i64, _i32, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
                              _vp, _sz, _vp], _i32),
     "lshmoe_comm_p2p_error": ([_vp, ctypes.POINTER(_i32), _vp], _i32),
+    "lshmoe_comm_p2p_set_timeout": ([_vp, ctypes.c_double], _i32),
     "lshmoe_dispatch_p2p": ([_vp, _vp, _vp, _i32, _vp], _i32),
     "lshmoe_combine_p2p": ([_vp, _vp, _i32, _vp], _i32),
     "lshmoe_restore": ([_vp, _vp, _vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _vp], _i32),
@@ -561,6 +562,11 @@ class Comm:
                "lshmoe_comm_p2p_buffers")
         return (_device_view(pr.value, (rc, d), dtype, self), _device_view(pt.value, (tc, d), dtype, self),
                 _device_view(pn.value, (E // self.world, self.world), torch.int32, self))
+
+    def p2p_set_timeout(self, seconds: float):
+        """Peer-wait limit of this comm's phase-2 kernels (then error bit 2, reported by p2p_check)."""
+        _check(_lib.lshmoe_comm_p2p_set_timeout(self._h, float(seconds)), "lshmoe_comm_p2p_set_timeout")
+        return self
 
     def p2p_check(self, stream=None):
         """Raise if a phase-2 call on this rank dropped rows (a receive / returned buffer too small)."""

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -33,6 +34,8 @@ struct lshmoe_comm {
   int p2p_E = 0;
   int p2p_grid = 64;                       // default CTAs per phase-2 call
   bool dispatched = false;                 // a dispatch_p2p was issued (combine needs one)
+  bool local_group = false;                // virtual ranks of one process on one GPU (lshmoe_comm_local_group)
+  unsigned long long spin_ns = 0;          // peer-wait limit of the phase-2 kernels (0: p2p_spin_limit_ns())
   int32_t* counts_dev = nullptr;     // [world * E_cap]
   int32_t* counts_host = nullptr;    // pinned [world * E_cap]
   int32_t* rr_host = nullptr;        // pinned [E_cap] recv_rows staging
@@ -40,6 +43,8 @@ struct lshmoe_comm {
   int last_E = 0;                    // E of the last dispatch (plan valid iff > 0)
   std::vector<int32_t> counts;       // host copy of the last plan [world * E]
 };
+
+static unsigned long long comm_spin_ns(const lshmoe_comm* c) { return c->spin_ns ? c->spin_ns : p2p_spin_limit_ns(); }
 
 static lshmoe_status nccl_status(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return LSHMOE_OK;
@@ -253,6 +258,7 @@ lshmoe_status lshmoe_comm_local_group(int world, int64_t recv_capacity, int64_t 
     cs[r] = new lshmoe_comm();
     cs[r]->world = world;
     cs[r]->rank = r;
+    cs[r]->local_group = true;
     lshmoe_status st = p2p_alloc(cs[r], E, recv_capacity, ret_capacity, row_bytes);
     if (st) {
       for (int q = 0; q <= r; ++q) lshmoe_comm_destroy(cs[q]);
@@ -273,6 +279,12 @@ lshmoe_status lshmoe_comm_local_group(int world, int64_t recv_capacity, int64_t 
 }
 
 
+lshmoe_status lshmoe_comm_p2p_set_timeout(lshmoe_comm* c, double seconds) {
+  if (!c || !(seconds > 0) || seconds > 1e6) return set_error(LSHMOE_EINVAL, "lshmoe_comm_p2p_set_timeout: bad comm / seconds");
+  c->spin_ns = static_cast<unsigned long long>(seconds * 1e9);
+  return LSHMOE_OK;
+}
+
 lshmoe_status lshmoe_comm_p2p_buffers(lshmoe_comm* c, void** recv, void** returned, int32_t** recv_rows) {
   if (!c || !c->window) return set_error(LSHMOE_EINVAL, "lshmoe_comm_p2p_buffers: no phase-2 window");
   if (recv) *recv = c->window + c->L.recv;
@@ -290,6 +302,9 @@ lshmoe_status lshmoe_comm_p2p_error(lshmoe_comm* c, int32_t* value, lshmoe_strea
   if (!err && v) err = cudaMemsetAsync(c->done + 1, 0, sizeof(unsigned), s);
   if (err) return cuda_status(err, "lshmoe_comm_p2p_error");
   *value = static_cast<int32_t>(v);
+  if (v & kP2PErrTimeout)
+    return set_error(LSHMOE_EDEVICE, "phase-2 exchange: a peer did not arrive within the spin limit "
+                                     "(LSHMOE_P2P_TIMEOUT_S); the call's results are invalid");
   if (v) return set_error(LSHMOE_EDEVICE, v & 1 ? "phase-2 dispatch: a receive buffer was too small (rows dropped)"
                                                  : "phase-2 combine: a returned buffer was too small (rows dropped)");
   return LSHMOE_OK;
@@ -299,18 +314,20 @@ lshmoe_status lshmoe_dispatch_p2p(lshmoe_comm* c, const void* centroids, const i
                                   lshmoe_stream stream) {
   if (!c || !c->window) return set_error(LSHMOE_EINVAL, "lshmoe_dispatch_p2p: no phase-2 window");
   if (!expert_rows) return set_error(LSHMOE_EINVAL, "lshmoe_dispatch_p2p: expert_rows is NULL");
-  c->dispatched = true;
   const int g = grid > 0 ? grid : c->p2p_grid;
-  return cuda_status(launch_p2p(0, c->peers_dev, c->L, c->world, c->rank, c->p2p_E, centroids, expert_rows,
-                                c->recv_rows_dev, c->done, g, stream),
-                     "lshmoe_dispatch_p2p");
+  const lshmoe_status st = cuda_status(launch_p2p(0, c->peers_dev, c->L, c->world, c->rank, c->p2p_E, centroids,
+                                                  expert_rows, c->recv_rows_dev, c->done, g, comm_spin_ns(c),
+                                                  stream),
+                                       "lshmoe_dispatch_p2p");
+  if (!st) c->dispatched = true;
+  return st;
 }
 
 lshmoe_status lshmoe_combine_p2p(lshmoe_comm* c, const void* expert_out, int grid, lshmoe_stream stream) {
   if (!c || !c->window || !c->dispatched) return set_error(LSHMOE_EINVAL, "lshmoe_combine_p2p: no matching dispatch");
   const int g = grid > 0 ? grid : c->p2p_grid;
   return cuda_status(launch_p2p(1, c->peers_dev, c->L, c->world, c->rank, c->p2p_E, expert_out, nullptr, nullptr,
-                                c->done, g, stream),
+                                c->done, g, comm_spin_ns(c), stream),
                      "lshmoe_combine_p2p");
 }
 
@@ -473,13 +490,28 @@ namespace lshmoe {
 int comm_p2p_fuse(lshmoe_comm* c, int E, P2PFuse* out) {
   if (!c || !c->window || !c->peers_dev) return LSHMOE_EINVAL;
   if (E != c->p2p_E) return LSHMOE_EINVAL;
+  if (c->local_group && c->world > 1) return LSHMOE_EUNSUPPORTED;
   out->peers = c->peers_dev;
   out->L = c->L;
   out->world = c->world;
   out->me = c->rank;
   out->done = c->done;
   out->recv_rows = c->recv_rows_dev;
-  c->dispatched = true;
+  out->grid = c->p2p_grid;
+  out->spin_ns = comm_spin_ns(c);
   return LSHMOE_OK;
+}
+void comm_p2p_mark_dispatched(lshmoe_comm* c) { c->dispatched = true; }
+
+unsigned long long p2p_spin_limit_ns() {
+  static unsigned long long v = [] {
+    double s = 300.0;
+    if (const char* e = getenv("LSHMOE_P2P_TIMEOUT_S")) {
+      const double x = atof(e);
+      if (x > 0) s = x;
+    }
+    return static_cast<unsigned long long>(s * 1e9);
+  }();
+  return v;
 }
 }  // namespace lshmoe

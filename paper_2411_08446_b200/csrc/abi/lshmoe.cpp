@@ -63,7 +63,9 @@ lshmoe_status lshmoe_check_device_error(lshmoe_stream stream) {
   int v = 0;
   int err = read_and_clear_device_error(&v, stream);
   if (err) return cuda_status(err, "lshmoe_check_device_error");
-  if (v) return set_error(LSHMOE_EDEVICE, "device error word set: expert id outside [0, E) (S:L312)");
+  if (v & 1) return set_error(LSHMOE_EDEVICE, "device error word set: expert id outside [0, E) (S:L312)");
+  if (v) return set_error(LSHMOE_EDEVICE, "device error word set: an expert appears twice among a token's k slots "
+                                          "(the k experts must be distinct, S:L227)");
   return LSHMOE_OK;
 }
 
@@ -214,7 +216,11 @@ lshmoe_status lshmoe_compress_p2p(lshmoe_comm* comm, const void* x, lshmoe_dtype
                                   int32_t* perm, int32_t* row_start, int32_t* expert_rows, int32_t* num_rows,
                                   void* centroids, void* workspace, size_t workspace_bytes, lshmoe_stream stream) {
   P2PFuse fuse;
-  REQUIRE(comm_p2p_fuse(comm, E, &fuse) == LSHMOE_OK, LSHMOE_EINVAL,
+  const int fst = comm_p2p_fuse(comm, E, &fuse);
+  REQUIRE(fst != LSHMOE_EUNSUPPORTED, LSHMOE_EUNSUPPORTED,
+          "a local group at world > 1 cannot run the fused kernel (its CTAs occupy every SM, so the virtual "
+          "ranks' kernels could not be co-resident): use lshmoe_compress + lshmoe_dispatch_p2p");
+  REQUIRE(fst == LSHMOE_OK, LSHMOE_EINVAL,
           "comm has no phase-2 window for this number of experts (lshmoe_comm_p2p_init)");
   REQUIRE(d * (dtype == LSHMOE_F32 ? 4 : 2) == fuse.L.row_bytes, LSHMOE_EINVAL, "row bytes differ from the window's");
   lshmoe_status st = check_token_shape(__func__, dtype, n, d);
@@ -236,7 +242,9 @@ lshmoe_status lshmoe_compress_p2p(lshmoe_comm* comm, const void* x, lshmoe_dtype
   compress_workspace_layout(n, k, E, d, workspace, &ws);
   int err = launch_compress(x, dtype, n, d, codes, q, experts, k, E, bucket, perm, row_start, expert_rows, num_rows,
                             centroids, nullptr, ws, stream, &fuse);
-  return cuda_status(err, "lshmoe_compress_p2p");
+  st = cuda_status(err, "lshmoe_compress_p2p");
+  if (!st) comm_p2p_mark_dispatched(comm);   // only a launched dispatch licenses a combine
+  return st;
 }
 
 lshmoe_status lshmoe_expert_ffn_backward(const void* grad_out, lshmoe_dtype dtype, int d, int d_ffn,

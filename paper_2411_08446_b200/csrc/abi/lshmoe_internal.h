@@ -105,11 +105,23 @@ struct P2PFuse {
   int world, me;
   unsigned* done;            // [0] arrivals, [1] errors, [2] epoch
   int32_t* recv_rows;        // device [E/world][world] out
+  int grid;                  // the comm's phase-2 grid (the nk == 0 fallback launch)
+  unsigned long long spin_ns;   // peer-wait limit (then error bit 4, no trap)
 };
-int comm_p2p_fuse(::lshmoe_comm* c, int E, P2PFuse* out);   // comm.cpp: LSHMOE_OK or EINVAL
+// comm.cpp: LSHMOE_OK, EINVAL (no window for E) or EUNSUPPORTED (a local group at world > 1: the
+// fused kernel needs one CTA per SM, so the virtual ranks could not be co-resident).  Does not mark
+// the comm as dispatched: call comm_p2p_mark_dispatched after the launch succeeded.
+int comm_p2p_fuse(::lshmoe_comm* c, int E, P2PFuse* out);
+void comm_p2p_mark_dispatched(::lshmoe_comm* c);
+// Error bits of done[1]: 1 = a receive buffer too small (dispatch), 2 = a returned buffer too small
+// (combine), 4 = a peer did not arrive within the spin limit (the call's results are invalid).
+constexpr unsigned kP2PErrTimeout = 4u;
 
 int launch_p2p(int which, uint8_t* const* peers_dev, const P2PLayout& L, int world, int me, int E, const void* src,
-               const int32_t* expert_rows, int32_t* recv_rows, unsigned* done, int grid, void* stream);
+               const int32_t* expert_rows, int32_t* recv_rows, unsigned* done, int grid, unsigned long long spin_ns,
+               void* stream);
+// Peer-wait limit of the phase-2 kernels in ns: LSHMOE_P2P_TIMEOUT_S (seconds), default 300 s.
+unsigned long long p2p_spin_limit_ns();
 
 int read_and_clear_device_error(int* value, void* stream);
 // Programmatic dependent launch for the GEMM and restore kernels (LSHMOE_PDL=0 turns it off, A/B).

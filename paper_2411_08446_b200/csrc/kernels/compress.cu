@@ -55,7 +55,8 @@ constexpr int kDiag = kArrive + kMaxGrid;
 constexpr int kHdr = kDiag + 16 * kMaxGrid;
 
 // Device error word (read by lshmoe_check_device_error).  Bit 0: expert id outside [0, E)
-// (S:L312).  Only this translation unit validates expert ids.
+// (S:L312); bit 1: an expert repeated among a token's k slots ("distinct").  Only this
+// translation unit validates expert ids.
 __device__ int g_device_error = 0;
 
 __device__ __forceinline__ int load_expert(const int32_t* experts, int c, int E) {
@@ -124,6 +125,7 @@ struct Params {
   uint8_t* const* p2p_peers;
   int64_t p2p_mailbox, p2p_recv, p2p_data_flag, p2p_recv_cap;
   int p2p_world, p2p_me;
+  unsigned long long p2p_spin_ns;   // peer-wait limit (then error bit 4 in p2p_done[1], no trap)
   unsigned* p2p_done;
   int32_t* p2p_recv_rows;
 };
@@ -251,6 +253,11 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(Params P) {
   const int c = t * kTile + tid;
   const bool ok = c < P.nk;
   const int e = ok ? load_expert(P.experts, c, P.E) : P.E;   // digit E = past the end
+  if (ok && P.k > 1) {                       // the token's k experts must be distinct
+    const int s = c % P.k;
+    for (int s2 = 0; s2 < s; ++s2)
+      if (P.experts[c - s + s2] == P.experts[c]) atomicOr(&g_device_error, 2);
+  }
   int16_t key[kMaxQ];
   if (ok && !P.permute) {
     const int16_t* mc = P.codes + static_cast<int64_t>(c / P.k) * P.q;
@@ -652,7 +659,8 @@ __device__ __noinline__ void store_f32_copy(float* dst, const float* v) {   // t
 
 // centroid = acc * rc, rc = RN(1/count) (reading R10), RNE to the wire dtype; fp32 copy if requested.
 template <typename T, bool kF = false>
-__device__ __forceinline__ void store_chunk16(const Params& P, int row, int c16, const float* acc, float rc) {
+__device__ __forceinline__ void store_chunk16(const Params& P, int row, int c16, const float* acc, float rc,
+                                              uint8_t* fdst = nullptr) {
   constexpr int VC = 16 / sizeof(T);
   float v[VC];
 #pragma unroll
@@ -671,8 +679,7 @@ __device__ __forceinline__ void store_chunk16(const Params& P, int row, int c16,
   }
   *reinterpret_cast<uint4*>(P.cent + static_cast<int64_t>(row) * P.row_bytes + 16 * c16) = out;
   if constexpr (kF) {                        // fused dispatch: the row also goes to its owner
-    uint8_t* dst = fused_row_dst(P, row);
-    if (dst) *reinterpret_cast<uint4*>(dst + 16 * c16) = out;
+    if (fdst) *reinterpret_cast<uint4*>(fdst + 16 * c16) = out;
   }
   if (P.cent32) store_f32_copy<VC>(P.cent32 + static_cast<int64_t>(row) * P.d + c16 * VC, v);
 }
@@ -692,7 +699,8 @@ __device__ __forceinline__ void add_chunk8(float* acc, uint2 raw) {
 
 // centroid = acc * RN(1/count) (reading R10), RNE to the wire dtype; fp32 copy if requested.
 template <typename T, bool kF = false>
-__device__ __forceinline__ void store_chunk8(const Params& P, int row, int ch, const float* acc, float cnt) {
+__device__ __forceinline__ void store_chunk8(const Params& P, int row, int ch, const float* acc, float cnt,
+                                             uint8_t* fdst = nullptr) {
   constexpr int VC = sizeof(T) == 2 ? 4 : 2;
   const float rc = P.grad ? 1.0f : __frcp_rn(cnt);
   float v[VC];
@@ -708,8 +716,7 @@ __device__ __forceinline__ void store_chunk8(const Params& P, int row, int ch, c
   }
   *reinterpret_cast<uint2*>(P.cent + static_cast<int64_t>(row) * P.row_bytes + 8 * ch) = out;
   if constexpr (kF) {
-    uint8_t* dst = fused_row_dst(P, row);
-    if (dst) *reinterpret_cast<uint2*>(dst + 8 * ch) = out;
+    if (fdst) *reinterpret_cast<uint2*>(fdst + 8 * ch) = out;
   }
   if (P.cent32) {
     float* dst = P.cent32 + static_cast<int64_t>(row) * P.d + ch * VC;
@@ -802,10 +809,12 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
     const bool head = seg_start > w_begin || X.prev_row != row;   // the row starts in this warp
     if (head && next != row) {                // the whole row lies in this warp's sub-range
       const float rc = P.grad ? 1.0f : __frcp_rn(static_cast<float>(p + 1 - seg_start));
+      uint8_t* fdst = nullptr;
+      if constexpr (kF) fdst = fused_row_dst(P, static_cast<int>(row));   // owner row, once per row
 #pragma unroll
       for (int t = 0; t < CPL; ++t) {
         const int c = lane + 32 * t;
-        if (full || c < ncb) store_chunk16<T, kF>(P, static_cast<int>(row), c0 + c, acc[t], rc);
+        if (full || c < ncb) store_chunk16<T, kF>(P, static_cast<int>(row), c0 + c, acc[t], rc, fdst);
       }
     } else if (p + 1 == w_end) {
       break;                                  // the last segment stays in acc (partial, see below)
@@ -856,6 +865,9 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
     const bool before = lo == X.p_begin && X.row_at(X.p_begin - 1) == r;
     const bool after = hi == X.p_end && X.row_at(X.p_end) == r;
     const float rc = P.grad ? 1.0f : __frcp_rn(static_cast<float>(hi - lo));
+    uint8_t* fdst = nullptr;
+    if constexpr (kF)
+      if (!(before || after)) fdst = fused_row_dst(P, static_cast<int>(r));   // owner row, once per row
 #pragma unroll
     for (int t = 0; t < CPL; ++t) {
       const int c = lane + 32 * t;
@@ -875,7 +887,7 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
 #pragma unroll
         for (int e = 0; e < VC; ++e) dst[e] = v[e];
       } else {
-        store_chunk16<T, kF>(P, static_cast<int>(r), c0 + c, v, rc);
+        store_chunk16<T, kF>(P, static_cast<int>(r), c0 + c, v, rc, fdst);
       }
     }
   };
@@ -1019,6 +1031,8 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
     const int nc8 = P.row_bytes / 8;
     const int slot0 = rs == range_begin(b0, P.nk, G) ? 0 : 1;
     const bool all_nonempty = P.nk >= G;
+    uint8_t* fdst = nullptr;
+    if constexpr (kF) fdst = fused_row_dst(P, row);   // owner row, once per merged row
     for (int ch = tid; ch < nc8; ch += kThreads) {
       float acc[VC];
       const float* src = P.partial + (static_cast<int64_t>(b0) * 2 + slot0) * P.d + ch * VC;
@@ -1043,7 +1057,7 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
 #pragma unroll
             for (int e = 0; e < VC; ++e) acc[e] += tmp[u][e];
       }
-      store_chunk8<T, kF>(P, row, ch, acc, static_cast<float>(re - rs));
+      store_chunk8<T, kF>(P, row, ch, acc, static_cast<float>(re - rs), fdst);
     }
   }
 }
@@ -1084,7 +1098,6 @@ __device__ __forceinline__ uint64_t* f_slot(const Params& P, int rank, uint32_t 
   return reinterpret_cast<uint64_t*>(P.p2p_peers[rank] + P.p2p_mailbox) +
          (static_cast<int64_t>(ep & 1) * P.p2p_world + src) * P.E + e;
 }
-constexpr uint64_t kFuseSpinNs = 10ull * 1000 * 1000 * 1000;   // a peer that never arrives traps
 
 // CTA 0 posts this rank's counts (epoch-tagged words) into every peer's mailbox; every CTA reads all
 // sources' counts, then the destination base of each of its experts' rows in the owner's receive
@@ -1106,7 +1119,11 @@ __device__ void fused_prologue(const Params& P, const int* s_roff, const int* s_
     uint64_t v = ld_rlx_sys64(f_slot(P, P.p2p_me, ep, src, e));
     while (static_cast<uint32_t>(v >> 32) != ep) {
       __nanosleep(32);
-      if (gtimer() - t0 > kFuseSpinNs) __trap();
+      if (gtimer() - t0 > P.p2p_spin_ns) {     // a peer never posted: count 0, flagged (no trap)
+        atomicOr(P.p2p_done + 1, kP2PErrTimeout);
+        v = static_cast<uint64_t>(ep) << 32;
+        break;
+      }
       v = ld_rlx_sys64(f_slot(P, P.p2p_me, ep, src, e));
     }
     s_fc[i] = static_cast<int>(v & 0xffffffffu);
@@ -1147,7 +1164,10 @@ __device__ void fused_close(const Params& P, uint32_t ep) {
   for (int s2 = 0; s2 < P.p2p_world; ++s2)
     while (static_cast<int32_t>(ld_acq_sys(fl + s2) - ep) < 0) {
       __nanosleep(64);
-      if (gtimer() - t0 > kFuseSpinNs) __trap();
+      if (gtimer() - t0 > P.p2p_spin_ns) {     // a peer never arrived: flagged, no trap
+        atomicOr(P.p2p_done + 1, kP2PErrTimeout);
+        return;
+      }
     }
 }
 
@@ -1481,7 +1501,7 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
     if ((err = cudaMemsetAsync(row_start, 0, sizeof(int32_t), st))) return err;
     if (fuse)   // no rows: the standalone dispatch kernel still posts the zero counts and handshakes
       return launch_p2p(0, fuse->peers, fuse->L, fuse->world, fuse->me, E, nullptr, expert_rows, fuse->recv_rows,
-                        fuse->done, 2 * device_sm_count(), stream);
+                        fuse->done, fuse->grid, fuse->spin_ns, stream);
     return 0;
   }
   // The workspace is at rest between calls (hash table slots and arrival counters -1: K3 resets
@@ -1506,6 +1526,7 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
     P.p2p_world = fuse->world;
     P.p2p_me = fuse->me;
     P.p2p_done = fuse->done;
+    P.p2p_spin_ns = fuse->spin_ns;
     P.p2p_recv_rows = fuse->recv_rows;
   }
   return launch_chain(P, st);

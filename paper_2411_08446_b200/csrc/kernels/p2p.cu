@@ -55,15 +55,19 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 // Spin until every source's flag reached `epoch`.  A peer that never arrives (a rank that skipped
-// the call, kernels of a local group that cannot be co-resident) traps after 10 s instead of
-// hanging the device: the launch fails with a sticky error the host sees at its next sync.
-constexpr uint64_t kSpinLimitNs = 10ull * 1000 * 1000 * 1000;
-__device__ __forceinline__ void wait_flags(const uint32_t* flags, int world, uint32_t epoch) {
+// the call, a straggler beyond the limit, kernels that cannot be co-resident) does not hang the
+// device or trap (a trap would kill the whole context): after `spin_ns` the wait gives up, sets
+// error bit 4 in done[1] (lshmoe_comm_p2p_error reports it) and the kernel finishes.
+__device__ __forceinline__ void wait_flags(const uint32_t* flags, int world, uint32_t epoch, uint64_t spin_ns,
+                                           unsigned* err) {
   const uint64_t t0 = global_ns();
   for (int s = 0; s < world; ++s)
     while (static_cast<int32_t>(ld_acquire_sys(flags + s) - epoch) < 0) {
       if (!(g_p2p_exp & 2)) __nanosleep(64);
-      if (global_ns() - t0 > kSpinLimitNs) __trap();
+      if (global_ns() - t0 > spin_ns) {
+        atomicOr(err, kP2PErrTimeout);
+        return;
+      }
     }
 }
 
@@ -76,6 +80,7 @@ struct P2PArgs {
   const int32_t* expert_rows;   // dispatch: this rank's m_e [E]
   int32_t* recv_rows;      // dispatch: out [E/world][world] (may be null)
   unsigned* done;          // [0] CTA arrival counter (zero at rest); [1] error bits; [2] last epoch
+  unsigned long long spin_ns;   // peer-wait limit
 };
 
 // Count mailbox slot (source `src`, expert e) of epoch `ep` in rank `rank`'s window: one 64-bit word
@@ -110,7 +115,11 @@ __device__ void read_counts(const P2PArgs& a, int32_t* s_cnt) {
     uint64_t v = ld_relaxed_sys_u64(slot);
     while (static_cast<uint32_t>(v >> 32) != a.epoch) {
       if (!(g_p2p_exp & 2)) __nanosleep(32);
-      if (global_ns() - t0 > kSpinLimitNs) __trap();
+      if (global_ns() - t0 > a.spin_ns) {     // a peer never posted: count 0, flagged (no trap)
+        atomicOr(a.done + 1, kP2PErrTimeout);
+        v = static_cast<uint64_t>(a.epoch) << 32;
+        break;
+      }
       v = ld_relaxed_sys_u64(slot);
     }
     s_cnt[i] = static_cast<int32_t>(v & 0xffffffffu);
@@ -134,7 +143,8 @@ __device__ void close_call(const P2PArgs& a, int64_t flag_off, bool dispatch, bo
     if (!(g_p2p_exp & 8)) {
       for (int p = 0; p < a.world; ++p)
         st_release_sys(reinterpret_cast<uint32_t*>(a.peers[p] + flag_off) + a.me, a.epoch);
-      wait_flags(reinterpret_cast<const uint32_t*>(a.peers[a.me] + flag_off), a.world, a.epoch);
+      wait_flags(reinterpret_cast<const uint32_t*>(a.peers[a.me] + flag_off), a.world, a.epoch, a.spin_ns,
+                 a.done + 1);
     }
   }
   if (stamp) g_p2p_stamp[blockIdx.x * 4 + 3] = global_ns();
@@ -285,8 +295,9 @@ __global__ void __launch_bounds__(kP2PThreads) combine_p2p_kernel(P2PArgs a) {
 }  // namespace
 
 int launch_p2p(int which, uint8_t* const* peers_dev, const P2PLayout& L, int world, int me, int E, const void* src,
-               const int32_t* expert_rows, int32_t* recv_rows, unsigned* done, int grid, void* stream) {
-  P2PArgs a{peers_dev, L, world, me, E, 0u, static_cast<const uint8_t*>(src), expert_rows, recv_rows, done};
+               const int32_t* expert_rows, int32_t* recv_rows, unsigned* done, int grid, unsigned long long spin_ns,
+               void* stream) {
+  P2PArgs a{peers_dev, L, world, me, E, 0u, static_cast<const uint8_t*>(src), expert_rows, recv_rows, done, spin_ns};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   static int exp_set = -1;
   const int exp = p2p_experiment();

@@ -137,8 +137,12 @@ def run_layer(L, case, ex_stacked, E):
     return codes, out, y
 
 
-@pytest.mark.parametrize("cfgname,tol", [("C1", 1e-5), ("C2", 2e-2)])
+@pytest.mark.parametrize("cfgname,tol", [("C1", 1e-5), ("C2", 2e-2), ("C3", 2e-2), ("C4", 2e-2), ("C5", 2e-2)])
 def test_layer_end_to_end(L, cfgname, tol):
+    """The whole layer at every BASELINE.json config's full per-rank size, through the bench's
+    calls: real oracle hashes (fp64 Eq. 3 on the stored x and R_j; near-tie tokens sanitised),
+    bucket ids bit-exact, y within the tier.  C3 / C4 hash at d = 1024 over 32K / 64K tokens and run
+    the expert FFN at d_ffn = 4096 / 16384; C3 is top-2.  (The oracle costs ~1 min per config.)"""
     cfg = CONFIGS[cfgname]
     case = make_case(L, cfg, seed=0, sanitize=True)
     ex = experts_for(cfg, 0)
@@ -148,6 +152,9 @@ def test_layer_end_to_end(L, cfgname, tol):
     b = res.buckets[0]
     assert int(out.num_rows.item()) == b.m
     assert np.array_equal(out.bucket.cpu().numpy(), b.bucket)
+    assert np.array_equal(out.perm.cpu().numpy(), b.perm)
+    assert np.array_equal(out.row_start.cpu().numpy()[:b.m + 1], b.row_start)
+    assert np.array_equal(out.expert_rows.cpu().numpy(), b.expert_rows)
     err = row_rel_err(f64(y), res.y[0])
     print(f"[layer {cfgname}] replaced near-tie tokens={case.replaced} ratio={res.ratio:.4f} y row-rel err={err:.3e}")
     assert err <= tol

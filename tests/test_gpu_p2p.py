@@ -181,3 +181,61 @@ def test_p2p_graph_replay():
         torch.cuda.synchronize()
         for c in comms:
             c.close()
+
+
+def test_p2p_peer_timeout_is_flagged_not_trapped():
+    """A peer that never joins (rank 1 of a local group skips the call): rank 0's dispatch gives up
+    after the comm's spin limit, flags error bit 2 and returns — no trap, so the CUDA context
+    survives and the next calls on a fresh group work (a straggler must not kill the job)."""
+    import paper_2411_08446_b200 as L
+    E, d = 4, 64
+    comms = L.Comm.local_group(2, 100, 100, d, torch.bfloat16, E)
+    try:
+        comms[0].p2p_set_timeout(0.05)
+        er = torch.tensor([3, 3, 3, 3], dtype=torch.int32, device="cuda")
+        C = torch.ones((12, d), dtype=torch.bfloat16, device="cuda")
+        L.dispatch_p2p(comms[0], C, er)
+        torch.cuda.synchronize()                             # completes (no hang, no sticky error)
+        with pytest.raises(L.LshmoeError, match="spin limit"):
+            comms[0].p2p_check()
+        comms[0].p2p_check()                                  # the flag was read and cleared
+    finally:
+        torch.cuda.synchronize()
+        for c in comms:
+            c.close()
+    _run_group(2, 8, 128, torch.bfloat16, rounds=1, grid=8, seed=5)   # the context is healthy
+
+
+def test_compress_p2p_refuses_local_group():
+    """The fused compress + dispatch needs every rank on its own GPU: a local group at world > 1 is
+    refused before any launch, and the comm is not marked as dispatched."""
+    import paper_2411_08446_b200 as L
+    E, d, n = 4, 64, 256
+    comms = L.Comm.local_group(2, 2 * n, n, d, torch.bfloat16, E)
+    try:
+        x = torch.ones((n, d), dtype=torch.bfloat16, device="cuda")
+        codes = torch.ones((n, 2), dtype=torch.int16, device="cuda")
+        zeta = (torch.arange(n, dtype=torch.int32, device="cuda") % E).view(n, 1)
+        with pytest.raises(L.LshmoeError, match="EUNSUPPORTED"):
+            L.compress_p2p(comms[0], x, codes, zeta, E)
+        with pytest.raises(L.LshmoeError, match="no matching dispatch"):
+            L.combine_p2p(comms[0], x)
+    finally:
+        torch.cuda.synchronize()
+        for c in comms:
+            c.close()
+
+
+def test_duplicate_expert_in_row_is_flagged():
+    """The k experts of a token must be distinct: a repeated id sets the device error word
+    and lshmoe_check_device_error returns LSHMOE_EDEVICE."""
+    import paper_2411_08446_b200 as L
+    n, d, E = 300, 64, 4
+    x = torch.randn((n, d), device="cuda").to(torch.bfloat16)
+    codes = torch.ones((n, 1), dtype=torch.int16, device="cuda")
+    zeta = torch.stack([torch.arange(n) % E, (torch.arange(n) + 1) % E], 1).to(torch.int32)
+    zeta[17, 1] = zeta[17, 0]
+    L.compress(x, codes, zeta.cuda(), E)
+    with pytest.raises(L.LshmoeError, match="twice"):
+        L.check_device_error()
+    L.check_device_error()                                    # cleared

@@ -32,3 +32,23 @@ def test_gate_k_equals_E():
     zeta, g, margin = O.gate_topk(rng.standard_normal((10, 4)), rng.standard_normal((5, 4)), 5)
     assert np.array_equal(zeta, np.tile(np.arange(5), (10, 1))) and np.allclose(g.sum(1), 1)
     assert np.all(margin == 1)
+
+
+def test_gate_margin_brute_force():
+    """margin (R29) = (k-th largest score - (k+1)-th largest) / max |s|, for every k < E, by fsum
+    loops and an explicit selection sort; a planted exact tie at the k/k+1 boundary gives 0."""
+    rng = np.random.default_rng(2)
+    X, Wg = rng.standard_normal((40, 6)), rng.standard_normal((7, 6))
+    Wg[5] = Wg[2]                                       # experts 2 and 5 always tie
+    for k in range(1, 7):
+        _, _, margin = O.gate_topk(X, Wg, k)
+        for t in range(40):
+            s = [math.fsum(X[t, i] * Wg[e, i] for i in range(6)) for e in range(7)]
+            rest, srt = list(s), []
+            while rest:                                 # selection sort, descending
+                j = max(range(len(rest)), key=lambda i: rest[i])
+                srt.append(rest.pop(j))
+            want = (srt[k - 1] - srt[k]) / max(abs(v) for v in s)
+            assert abs(margin[t] - want) <= 1e-12 * max(1.0, abs(want))
+            if s[2] == srt[k - 1] and s[5] == srt[k]:
+                assert margin[t] == 0.0
