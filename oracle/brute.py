@@ -69,3 +69,17 @@ def ffn_loops(x, W1, b1, W2, b2):
     """E(x) = W2 relu(W1 x + b1) + b2 with explicit loops and fsum."""
     h = [max(0.0, math.fsum(W1[i][j] * x[j] for j in range(len(x))) + b1[i]) for i in range(len(W1))]
     return [math.fsum(W2[o][i] * h[i] for i in range(len(h))) + b2[o] for o in range(len(W2))]
+
+
+def fwht_loops(v: Sequence[float]) -> List[float]:
+    """Unnormalised fast Walsh-Hadamard transform by the textbook in-place butterfly loops
+    (len(v) a power of two): for h = 1, 2, 4, ...: (a, b) <- (a + b, a - b) on pairs h apart.
+    Equals H v with the Sylvester H (an independent route to the dense matrix of O2*)."""
+    a = list(v)
+    h = 1
+    while h < len(a):
+        for i in range(0, len(a), 2 * h):
+            for j in range(i, i + h):
+                a[j], a[j + h] = a[j] + a[j + h], a[j] - a[j + h]
+        h *= 2
+    return a

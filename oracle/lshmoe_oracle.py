@@ -18,6 +18,10 @@ The functions follow Algorithm 1 (App. A "Framework of LSH-MoE") ste
                                       e4m3-rounded, power-of-two-scaled x and R_j (reading R28) [pinned]
   O0  gate_topk(X, Wg, k)             the gate of Eq. 1-2 as a linear scorer + top-k
                                       + softmax; NEXT-2 fuses it into the hash pass     [pinned]
+  O2* hd3_rotation(d, q, seed)        NEXT-4 structured pseudo-random rotation of Eq. 3's R
+                                      (P:L228): R_j = H D3 H D2 H D1 on x zero-padded to
+                                      d' = 1024 (reading R30), materialised dense; cp_hash then
+                                      takes its argmax over the d' outputs                [pinned]
   O2' sp_hash(X, N, q, b)             §4.5 spherical-plane hashing (P:L474-479), SPEC's
                                       sign-bit construction (reading R26)   [pinned]
   O3  group_by_expert(zeta, E)        Alg. 1 L3 "Dispatch X into {X_i}"        [pinned]
@@ -51,7 +55,7 @@ import numpy as np
 __all__ = [
     "GAMMA", "splitmix64_stream", "irwin_hall_gaussian", "rotation_fp64", "rotation",
     "round_to_dtype", "f32_to_bf16_bits", "bf16_bits_to_f64", "to_stored",
-    "cp_hash", "sp_hash", "sp_normals", "gate_topk", "e4m3_values", "round_e4m3", "pow2_scale_e4m3",
+    "cp_hash", "sp_hash", "sp_normals", "gate_topk", "HD3_DIM", "HD3_GAMMA", "hadamard", "hd3_signs", "hd3_rotation", "e4m3_values", "round_e4m3", "pow2_scale_e4m3",
     "quantize_tokens_e4m3", "quantize_rotation_e4m3", "group_by_expert", "bucketize", "Buckets", "centroids", "expert_ffn",
     "dispatch_sim", "combine_sim", "restore", "moe_dense", "lsh_layer", "lsh_layer_ranks",
     "LayerResult", "ulp_bf16", "grad_compress", "expert_ffn_vjp", "grad_restore", "lsh_layer_backward",
@@ -178,16 +182,17 @@ def round_to_dtype(x: np.ndarray, dtype: str) -> np.ndarray:
 # function and the q codes are combined into the bucket key (reading R4).
 # ---------------------------------------------------------------------------------------------
 def cp_hash(X: np.ndarray, R: np.ndarray):
-    """X [n, d] (stored values as fp64), R [q, d, d] (stored values as fp64).
+    """X [n, d] (stored values as fp64), R [q, d_out, d] (stored values as fp64; d_out = d for the
+    dense rotations of O1, d_out = 1024 for NEXT-4's padded structured rotations, reading R30).
 
-    Returns codes int16 [n, q] in {+-1..+-d} and margins fp64 [n, q]:
-    margin = (max|y| - second max|y|) / max|y| (0 if max|y| = 0; 1 if d = 1).
+    Returns codes int16 [n, q] in {+-1..+-d_out} and margins fp64 [n, q]:
+    margin = (max|y| - second max|y|) / max|y| (0 if max|y| = 0; 1 if d_out = 1).
     y = R_j x is evaluated in fp64: bf16/fp32 products are exact in fp64 and the sum's rounding
     (~1e-16 relative) is far below the 1e-5 near-tie band of BASELINE.json tier 1."""
     X = np.asarray(X, dtype=np.float64)
     R = np.asarray(R, dtype=np.float64)
-    n, d = X.shape
-    q = R.shape[0]
+    n = X.shape[0]
+    q, dout = R.shape[0], R.shape[1]
     codes = np.empty((n, q), dtype=np.int16)
     margins = np.empty((n, q), dtype=np.float64)
     rows = np.arange(n)
@@ -198,13 +203,63 @@ def cp_hash(X: np.ndarray, R: np.ndarray):
         amax = A[rows, istar]
         neg = Y[rows, istar] < 0             # zero winner (+0 or -0) counts as positive
         codes[:, j] = np.where(neg, -(istar + 1), istar + 1).astype(np.int16)
-        if d == 1:
+        if dout == 1:
             margins[:, j] = 1.0
         else:
-            second = np.partition(A, d - 2, axis=1)[:, d - 2]
+            second = np.partition(A, dout - 2, axis=1)[:, dout - 2]
             with np.errstate(invalid="ignore", divide="ignore"):
                 margins[:, j] = np.where(amax > 0, (amax - second) / np.where(amax > 0, amax, 1.0), 0.0)
     return codes, margins
+
+
+# ---------------------------------------------------------------------------------------------
+# O2*. NEXT-4: a structured pseudo-random rotation in place of Eq. 3's dense random
+# rotation R ("R is a random rotation matrix"; the paper fixes no construction), "three
+# rounds of Hadamard x random +-1 diagonal".  Reading R30: x is zero-padded to d' = 1024 (d <= 1024;
+# d = 768 is not a power of two), R_j = H D3_j H D2_j H D1_j with H the unnormalised Sylvester
+# Hadamard matrix of order d' (H[a, b] = (-1)^popcount(a & b)) and D_r,j diagonal +-1: entry i is
+# -1 iff bit 63 of SplitMix64 output number r*d' + i + 1 of the stream seeded with
+# rotation_seed ^ (0xD1B54A32D192ED03 * (j + 1) mod 2^64) is set.  R_j (d' x d after the padding
+# columns are dropped) has exact integer entries (|R| <= d'^2) and orthogonal columns of norm
+# d'^(3/2); Eq. 3's argmax is scale invariant, so no normalisation.  Codes index the d' outputs:
+# code = sign(y_i*) (i* + 1), i* in [0, d').  The oracle materialises R_j densely and reuses
+# cp_hash (the GPU applies it as three fast Walsh-Hadamard transforms).
+# ---------------------------------------------------------------------------------------------
+HD3_DIM = 1024
+HD3_GAMMA = 0xD1B54A32D192ED03
+
+
+def hadamard(order: int) -> np.ndarray:
+    """Unnormalised Sylvester Hadamard matrix by the doubling recursion H_2m = [[H, H], [H, -H]]."""
+    if order < 1 or order & (order - 1):
+        raise ValueError("order must be a power of two")
+    H = np.ones((1, 1))
+    while H.shape[0] < order:
+        H = np.block([[H, H], [H, -H]])
+    return H
+
+
+def hd3_signs(q: int, rotation_seed: int) -> np.ndarray:
+    """D [q, 3, d'] in {+1, -1} (reading R30)."""
+    out = np.empty((q, 3, HD3_DIM))
+    for j in range(q):
+        state = (rotation_seed ^ ((HD3_GAMMA * (j + 1)) & _MASK64)) & _MASK64
+        z = splitmix64_stream(state, 3 * HD3_DIM).reshape(3, HD3_DIM)
+        out[j] = np.where((z >> np.uint64(63)) == 1, -1.0, 1.0)
+    return out
+
+
+def hd3_rotation(d: int, q: int, rotation_seed: int) -> np.ndarray:
+    """Dense R [q, d', d] = (H D3 H D2 H D1)[:, :d] per hash (reading R30), exact in fp64."""
+    if not 1 <= d <= HD3_DIM:
+        raise ValueError("NEXT-4 structured rotation needs 1 <= d <= 1024")
+    H = hadamard(HD3_DIM)
+    D = hd3_signs(q, rotation_seed)
+    out = np.empty((q, HD3_DIM, d))
+    for j in range(q):
+        M = H @ np.diag(D[j, 2]) @ H @ np.diag(D[j, 1]) @ H @ np.diag(D[j, 0])
+        out[j] = M[:, :d]
+    return out
 
 
 # ---------------------------------------------------------------------------------------------
