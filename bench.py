@@ -42,10 +42,11 @@ def parse():
                    help="hash family: cross-polytope (paper default, Eq. 3), spherical-plane (NEXT-3), or "
                         "cross-polytope on e4m3 operands (NEXT-2 fp8 option)")
     p.add_argument("--sp-bits", type=int, default=12, help="sign bits per SP hash function")
-    p.add_argument("--exchange", default="nccl", choices=["nccl", "p2p", "p2p-fused"],
+    p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p", "p2p-fused"],
                    help="a6/a8 at N>1: phase 1 (NCCL, one host count sync), phase 2 (device-initiated stores "
                         "into the peers' windows, no host sync, CUDA-graph captured), or phase 2 with the dispatch "
-                        "fused into the centroid kernel (lshmoe_compress_p2p)")
+                        "fused into the centroid kernel (lshmoe_compress_p2p).  auto = p2p (the parity-tested "
+                        "exchange; phase 1 has not run on several GPUs)")
     p.add_argument("--share-gpu", action="store_true",
                    help="testing only: every rank on cuda:0 with a gloo group (p2p exchange); the line is "
                         "marked and is not a measurement")
@@ -55,6 +56,19 @@ def parse():
     p.add_argument("--no-backward", action="store_true", help="skip the NEXT-1 backward timing")
     p.add_argument("--profile", action="store_true", help="minimal run for ncu: warmup + steps eager, no extras")
     return p.parse_args()
+
+
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1, exactly as the driver would, and return their exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def peaks():
@@ -163,7 +177,8 @@ def run_reference(args, cfg):
             "config": workload_config(cfg, args.gpus),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"Alg. 1 on the first {sample} of rank 0's {cfg.n} tokens per step (fp64 NumPy oracle, "
-                                       f"rotation generation excluded)"},
+                                       f"rotation generation excluded); one process on rank 0's host whatever "
+                                       f"n_gpus is (the other ranks exit without work)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -180,26 +195,42 @@ def workload_config(cfg, world, args=None):
             "parallelism": f"ep{world}", "l2": "flushed between timed steps (256 MiB write, outside the events)"}
 
 
-def cpu_baseline(cfg, seed, X, zeta, ex):
+def cpu_baseline(cfg, seed, X, zeta, ex, codes_gpu=None):
+    """The oracle (Alg. 1 in fp64 NumPy) timed on this host's cores on full steps of rank 0, and, from
+    the same oracle run, the in-run parity record of the bench's own inputs: BASELINE.json tier 1's
+    near-ties (oracle top-two margin < 1e-5 relative) for the hash and for the gate (reading R29),
+    and how many GPU codes differ from the oracle's (outside near-ties this must be 0)."""
     import numpy as np
     import torch
 
     import oracle as O
-    from lshmoe_inputs import rotation_seed
+    from lshmoe_inputs import gate_matrix, rotation_seed
     R64 = O.to_stored(O.rotation(cfg.d, cfg.q, rotation_seed(seed), cfg.dtype), cfg.dtype)
     oex = {e: tuple(t.to(torch.float64).numpy() for t in v) for e, v in ex.items()}
     X64 = X.to(torch.float64).numpy()
     z = zeta.numpy()
     reps, t0 = 0, time.perf_counter()
     while True:
-        O.lsh_layer(X64, z, R64, oex, cfg.E, cfg.dtype)
+        res = O.lsh_layer(X64, z, R64, oex, cfg.E, cfg.dtype)
         reps += 1
         if time.perf_counter() - t0 > 10.0 or reps >= 5:
             break
     dt = (time.perf_counter() - t0) / reps
-    return {"value": cfg.n / dt, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-            "sample": f"{reps} full step(s) of rank 0 (all {cfg.n} tokens, Alg. 1 incl. expert FFN) in fp64 NumPy; "
-                      f"rotation generation excluded"}
+    cpu = {"value": cfg.n / dt, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+           "sample": f"{reps} full step(s) of rank 0 (all {cfg.n} tokens, Alg. 1 incl. expert FFN) in fp64 NumPy; "
+                     f"rotation generation excluded"}
+    margins = res.margins[0]
+    near = margins < 1e-5
+    _, _, gmargin = O.gate_topk(X64, gate_matrix(cfg, seed), cfg.k)
+    parity = {"hash_near_ties": int(near.sum()), "hash_codes": int(near.size),
+              "gate_near_ties": int((gmargin < 1e-5).sum()),
+              "near_tie_band": "oracle top-two margin < 1e-5 relative (BASELINE.json tier 1; gate: reading R29)"}
+    if codes_gpu is not None:
+        diff = codes_gpu != res.codes[0]
+        parity["hash_code_mismatches"] = int(diff.sum())
+        parity["hash_code_mismatches_outside_near_ties"] = int((diff & ~near).sum())
+        parity["compression_ratio_oracle"] = res.ratio
+    return cpu, parity
 
 
 # ---------------------------------------------------------------------------------------------
@@ -209,13 +240,24 @@ def main():
     cfg = CONFIGS[args.config]
     if args.q:
         cfg = cfg.with_(q=args.q)
+    launched = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
+    if args.impl == "reference":       # the oracle runs once, on rank 0's host cores, whatever N is
         if rank == 0:
             run_reference(args, cfg)
         return
+    if args.gpus > 1 and not launched:
+        sys.exit(spawn_ranks(args))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
+    if args.exchange == "auto":        # world 1: the exchange is an alias (no copy, no kernel)
+        args.exchange = "p2p" if world > 1 else "nccl"
+    if world > 1:      # NCCL's init lines (rank / nranks per communicator) on stderr, for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
     import numpy as np
     import torch
@@ -399,8 +441,6 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
         launches_per_step = L.kernel_launches() - l1
     else:
         launches_per_step = launches // args.steps
-    m = int(comp.num_rows.item())
-    ratio = m / nk
 
     # ---- e2e: every step copies its inputs host->device (pinned) and its output device->host, all
     # inside the timed region.  The copies run on their own streams, double-buffered, so step i's
@@ -464,56 +504,167 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     h2d = X_h.numel() * X_h.element_size() + z_h.numel() * z_h.element_size()
     d2h = y_hs[0].numel() * y_hs[0].element_size()
 
+    # ---- generic device timing of a list of calls: CUDA graph (when the exchange allows it) or eager,
+    # L2 flushed before each replay (outside the events), events on `stream`; median us, max over ranks ----
+    def graph_time(fns, graph=None):
+        graph = use_graph if graph is None else graph
+        for fn in fns:
+            fn()
+        run_ = lambda: [fn() for fn in fns]   # noqa: E731
+        if graph:
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, stream=stream):
+                for fn in fns:
+                    fn()
+            run_ = gph.replay
+            run_()
+        tt = []
+        barrier()
+        for _ in range(args.steps):
+            flush.zero_()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            run_()
+            b_.record(stream)
+            barrier()
+            tt.append(a_.elapsed_time(b_))
+        return max_over_ranks(statistics.median(tt) * 1e3)
+
+    sb = 2 if X.dtype == torch.bfloat16 else 4
+    row_bytes = d * sb
+    m = int(comp.num_rows.item())
+    ratio = m / nk
+    lo_e, hi_e = rank * E_local, (rank + 1) * E_local
+
+    def off_gpu_rows(counts):            # rows this rank sends to experts owned by other ranks
+        c = counts.cpu().to(torch.int64)
+        return int(c.sum()) - int(c[lo_e:hi_e].sum())
+
     # ---- context: uncompressed expert-parallel baseline on the same machinery ----
     unc = None
+    send = torch.empty((nk, d), dtype=X.dtype, device=dev)
+    slot = torch.empty((n, k), dtype=torch.int32, device=dev)
+    er = torch.empty(cfg.E, dtype=torch.int32, device=dev)
+    brr = er.view(cfg.E, 1) if world == 1 else torch.empty((E_local, world), dtype=torch.int32, device=dev)
+    urecv = send if world == 1 else torch.empty((cap, d), dtype=X.dtype, device=dev)
+    uret = eo if world == 1 else torch.empty((nk, d), dtype=X.dtype, device=dev)
+    yb = torch.empty_like(X)
+    if p2p:
+        urecv, uret, brr = recv, ret, rr
+    base_parts = {
+        "permute": lambda: L.permute(X, zeta, cfg.E, send, slot, er, ws),
+        "dispatch": (lambda: L.dispatch_p2p(comm, send, er)) if p2p else
+                    (lambda: L.dispatch(comm, send, er, cfg.E, urecv, brr)),
+        "expert_ffn": lambda: L.expert_ffn(urecv, brr, W1, b1, W2, b2, out=eo, hidden=hid),
+        "combine": (lambda: L.combine_p2p(comm, eo)) if p2p else (lambda: L.combine(comm, eo, er, cfg.E, uret)),
+        "unpermute": lambda: L.unpermute(uret, slot, yb),
+    }
     if not args.no_uncompressed:
-        send = torch.empty((nk, d), dtype=X.dtype, device=dev)
-        slot = torch.empty((n, k), dtype=torch.int32, device=dev)
-        er = torch.empty(cfg.E, dtype=torch.int32, device=dev)
-        brr = er.view(cfg.E, 1) if world == 1 else torch.empty((E_local, world), dtype=torch.int32, device=dev)
-        urecv = send if world == 1 else torch.empty((cap, d), dtype=X.dtype, device=dev)
-        uret = eo if world == 1 else torch.empty((nk, d), dtype=X.dtype, device=dev)
-        yb = torch.empty_like(X)
-
-        if p2p:
-            urecv, uret, brr = recv, ret, rr
-
-        def base_step():
-            L.permute(X, zeta, cfg.E, send, slot, er, ws)
-            if p2p:
-                L.dispatch_p2p(comm, send, er)
-            else:
-                L.dispatch(comm, send, er, cfg.E, urecv, brr)
-            L.expert_ffn(urecv, brr, W1, b1, W2, b2, out=eo, hidden=hid)
-            if p2p:
-                L.combine_p2p(comm, eo)
-            else:
-                L.combine(comm, eo, er, cfg.E, uret)
-            L.unpermute(uret, slot, yb)
-
-        for _ in range(3):
-            base_step()
-        brun = base_step
-        if use_graph:
-            g3 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g3, stream=stream):
-                base_step()
-            brun = g3.replay
-        bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        barrier()
-        for s in range(args.steps):
-            flush.zero_()
-            bev[s][0].record(stream)
-            brun()
-            bev[s][1].record(stream)
-        barrier()
-        bms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in bev))
-        unc = {"ms_per_step": bms, "tokens_per_s": world * n / (bms / 1e3),
+        bus = graph_time(list(base_parts.values()))
+        unc = {"ms_per_step": bus / 1e3, "tokens_per_s": world * n / (bus / 1e6),
                "what": "permute -> all-to-all of every routed token -> expert FFN on n*k rows -> all-to-all -> unpermute",
-               "speedup_of_lsh": bms / ms}
+               "speedup_of_lsh": (bus / 1e3) / ms}
+
+    # ---- T_dc: hash + compress + dispatch + combine + restore, the expert FFN excluded;
+    # the same for both uncompressed baselines (this library's exchange; torch.distributed's NCCL
+    # all_to_all_single on the permuted tokens) ----
+    lsh_dc_fns = [stages[i] for i in (0, 1, 2, 4, 5)]
+    t_dc = graph_time(lsh_dc_fns)
+    t_base_dc = graph_time([base_parts[k_] for k_ in ("permute", "dispatch", "combine", "unpermute")])
+    t_exch = graph_time([stages[2], stages[4]]) if world > 1 else 0.0
+    off_rows = off_gpu_rows(comp.expert_rows)
+    base_off_rows = off_gpu_rows(er)
+    nccl_base = None
+    if world > 1 and not args.share_gpu:
+        nrecv = torch.empty((cap, d), dtype=X.dtype, device=dev)
+        nret = torch.empty((nk, d), dtype=X.dtype, device=dev)
+        rcnt = torch.empty(world, dtype=torch.int64, device=dev)
+
+        def nccl_step():
+            L.permute(X, zeta, cfg.E, send, slot, er, ws)           # rows grouped by destination rank
+            cnt = er.view(world, E_local).sum(1).to(torch.int64)
+            dist.all_to_all_single(rcnt, cnt)
+            ins, outs = cnt.tolist(), rcnt.tolist()                   # one host sync, like phase 1
+            dist.all_to_all_single(nrecv[:sum(outs)], send[:nk], outs, ins)
+            dist.all_to_all_single(nret, nrecv[:sum(outs)], ins, outs)   # the reverse (FFN excluded)
+            L.unpermute(nret, slot, yb)
+        t_nccl = graph_time([nccl_step], graph=False)
+        # the in-run NCCL all-to-all peak: 256 MiB per rank, equal splits
+        big = torch.empty(128 << 20, dtype=torch.bfloat16, device=dev)
+        bigo = torch.empty_like(big)
+        t_peak = graph_time([lambda: dist.all_to_all_single(bigo, big)], graph=False)
+        peak_gbs = big.numel() * 2 * (world - 1) / world / (t_peak / 1e6) / 1e9
+        del big, bigo
+        nccl_base = {"t_dc_us": t_nccl, "tokens_per_s": world * n / (t_nccl / 1e6),
+                     "what": "permute -> torch.distributed.all_to_all_single (NCCL) of every routed token -> "
+                             "the reverse -> unpermute (FFN excluded; splits learned by one count all-to-all + "
+                             "host sync)",
+                     "nccl_alltoall_peak_gbs": peak_gbs,
+                     "nccl_alltoall_peak_how": "all_to_all_single of 256 MiB per rank, off-GPU bytes per direction / time"}
+    pk = peaks()
+    nvlink_gbs = 770.0                       # B200_PROFILING.md: measured peer copy per direction
+    t_dc_block = {
+        "definition": "SURVEY §8d.2: wall time from x, zeta in HBM to y in HBM for hash + compress + dispatch + "
+                      "combine + restore, expert FFN excluded; median of the steps, max over ranks, L2 flushed",
+        "lsh_us": t_dc, "lsh_tokens_per_s": world * n / (t_dc / 1e6),
+        "uncompressed_same_exchange_us": t_base_dc,
+        "uncompressed_same_exchange_tokens_per_s": world * n / (t_base_dc / 1e6),
+        "speedup_vs_same_exchange": t_base_dc / t_dc,
+        "uncompressed_nccl_all_to_all_single": nccl_base,
+        "speedup_vs_nccl": (nccl_base["t_dc_us"] / t_dc) if nccl_base else None,
+        "exchange_pair_us": t_exch if world > 1 else None,
+        "off_gpu_bytes_per_direction": off_rows * row_bytes,
+        "uncompressed_off_gpu_bytes_per_direction": base_off_rows * row_bytes,
+        "nvlink_gbs_achieved": (2 * off_rows * row_bytes / (t_exch / 1e6) / 1e9) if world > 1 and t_exch else None,
+        "nvlink_peak_gbs": nvlink_gbs,
+        "nvlink_peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
+    }
+
+    # ---- per-kernel roofline fractions: each stage alone, graph-timed, L2 flushed before it ----
+    hbm = pk["hbm_gbs"]
+    tc_peak = pk["bf16_tflops"] * (1 if cfg.dtype == "bf16" else 0.5)   # f32 SIMT path: no tensor peak, context only
+    q_ = cfg.q
+    hash_bytes = n * d * sb + q_ * d * d * sb + 2 * n * q_
+    hash_flops = 2.0 * n * q_ * d * d
+    comp_bytes = nk * row_bytes + m * row_bytes + 4 * nk + 2 * n * q_ + 4 * nk + 4 * nk + 4 * (m + 1)
+    cent_bytes = nk * row_bytes + m * row_bytes + 4 * nk + 4 * nk
+    rest_bytes = 2 * n * row_bytes + 4 * nk + 2 * m * row_bytes
+    ffn_flops = 4.0 * m * d * cfg.d_ffn
+    t_comp = graph_time([stages[1]])
+    t_ffn = graph_time([stages[3]])
+    t_rest = graph_time([stages[5]])
+    t_hash = graph_time([stages[0]])
+    span = {k_: v for k_, v in (compress_phases or {}).items() if not k_.startswith("gap")}
+
+    def kern(name, bound, work, us):
+        if bound == "tensor":
+            ach = work / (us / 1e6) / 1e12
+            return {"kernel": name, "bound": bound, "flops": work, "us": us, "achieved": ach, "unit": "TFLOP/s",
+                    "peak": tc_peak, "frac": ach / tc_peak}
+        ach = work / (us / 1e6) / 1e9
+        return {"kernel": name, "bound": bound, "bytes": work, "us": us, "achieved": ach, "unit": "GB/s",
+                "peak": hbm, "frac": ach / hbm}
+    kernels = [kern("hash: tc_gemm_kernel<ArgmaxEpi>", "tensor", hash_flops, t_hash)]
+    kernels.append(kern("compress: tile + bucket + centroid (3 launches)", "hbm", comp_bytes, t_comp))
+    if span.get("centroid"):
+        kernels.append(kern("centroid_kernel (span, diagnostics stamps)", "hbm", cent_bytes, span["centroid"]))
+    for nm_ in ("tiles", "bucket"):
+        if span.get(nm_):
+            kk = kern(f"{nm_} kernel (span, diagnostics stamps)", "hbm", 4 * nk * (3 if nm_ == "tiles" else 4), span[nm_])
+            kk["bound"] = "latency"
+            kk["note"] = "integer index work of < 1 MB: dependent global round trips and barriers, not bytes"
+            kernels.append(kk)
+    kernels.append(kern("expert FFN: tc_gemm_kernel<BiasActEpi> x2 (on the m centroid rows)", "tensor", ffn_flops, t_ffn))
+    kernels.append(kern("restore_kernel", "hbm", rest_bytes, t_rest))
+    t_lower = max(hash_flops / (tc_peak * 1e12), hash_bytes / (hbm * 1e9)) * 1e6 + comp_bytes / (hbm * 1e9) * 1e6 \
+        + rest_bytes / (hbm * 1e9) * 1e6 + 2 * off_rows * row_bytes / (nvlink_gbs * 1e9) * 1e6
+    layer_roofline = {"t_lower_us": t_lower, "t_dc_us": t_dc, "frac": t_lower / t_dc,
+                      "how": "T_lower = sum over the T_dc steps of max(flops / bf16 peak, algorithmic bytes / HBM, "
+                             "off-GPU bytes / 770 GB/s); frac = T_lower / T_dc (SURVEY §8d.2)"}
 
     # ---- NEXT-1 backward (reading R27): grad_compress -> dispatch(G) -> expert backward (dX path)
-    # -> combine(H) -> grad_restore, graph-timed as one chain and per part, L2 flushed before each ----
+    # -> combine(H) -> grad_restore, graph-timed as one chain and per part, L2 flushed before each.
+    # At world 1 the exchanges are aliases (no kernel) and are left out. ----
     bwd = None
     if not args.no_backward and world == 1:
         gen = torch.Generator(device=dev).manual_seed(11)
@@ -526,39 +677,17 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
         W2T = W2.transpose(1, 2).contiguous()
         W1T = W1.transpose(1, 2).contiguous()
         parts = {"grad_compress": lambda: L.grad_compress(dY, comp, out=Gb, workspace=gws),
-                 "dispatch": lambda: L.dispatch(comm, Gb, comp.expert_rows, cfg.E, Gb, rr),
                  "expert_backward": lambda: L.expert_ffn_backward(Gb, rr, W2T, W1T, hid, out=Hb, dhidden=dhid),
-                 "combine": lambda: L.combine(comm, Hb, comp.expert_rows, cfg.E, Hb),
                  "grad_restore": lambda: L.grad_restore(dY, X, comp.centroids, ret, Gb, Hb, comp, dx=dxb)}
-
-        def graph_time(fns):
-            for fn in fns:
-                fn()
-            gph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gph, stream=stream):
-                for fn in fns:
-                    fn()
-            tt = []
-            for _ in range(args.steps):
-                flush.zero_()
-                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a_.record(stream)
-                gph.replay()
-                b_.record(stream)
-                torch.cuda.synchronize()
-                tt.append(a_.elapsed_time(b_))
-            return statistics.median(tt) * 1e3
-
         bwd = {nm + "_us": graph_time([fn]) for nm, fn in parts.items()}
         bwd["chain_us"] = graph_time(list(parts.values()))
         bwd["tokens_per_s"] = n / (bwd["chain_us"] / 1e6)
-        sb = 2 if X.dtype == torch.bfloat16 else 4
         bwd["grad_compress_hbm_bytes"] = (nk + m) * d * sb
         bwd["grad_compress_gbs"] = bwd["grad_compress_hbm_bytes"] / bwd["grad_compress_us"] / 1e3
-        bwd["what"] = ("NEXT-1 (reading R27) dX path: G = per-bucket sums of dY -> exchange -> H = J_E(c~)^T G "
-                       "(expert backward, transposed weights, relu' from the forward's hidden) -> exchange -> "
-                       "dX = sum_s g dY + (H - G)/n_b; weight gradients not computed; each a CUDA-graph replay "
-                       "with L2 flushed")
+        bwd["what"] = ("NEXT-1 (reading R27) dX path: G = per-bucket sums of dY -> H = J_E(c~)^T G "
+                       "(expert backward, transposed weights, relu' from the forward's hidden) -> "
+                       "dX = sum_s g dY + (H - G)/n_b; world 1: the two exchanges are aliases (no kernel); "
+                       "weight gradients not computed; each a CUDA-graph replay with L2 flushed")
 
     L.check_device_error()
     # ---- the dominant kernel alone (the hash launch), CUDA-graph replay on `stream`, L2 flushed
@@ -574,7 +703,6 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
         hev[s][1].record(stream)
     torch.cuda.synchronize()
     hash_dev_ms = statistics.median(a.elapsed_time(b) for a, b in hev)
-    pk = peaks()
     if args.hash == "cp8":
         flops = 2.0 * n * cfg.q * d * d
         achieved = flops / (hash_dev_ms / 1e3) / 1e12
@@ -603,8 +731,10 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 "frac_of_sustained": achieved / pk["bf16_tflops_sustained"] if pk.get("bf16_tflops_sustained") else None}
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, args.seed, X_cpu, zeta_cpu, make_experts(cfg, args.seed))
+        cpu, parity = cpu_baseline(cfg, args.seed, X_cpu, zeta_cpu, make_experts(cfg, args.seed),
+                                   codes.cpu().numpy() if args.hash == "cp" else None)
 
     if rank == 0:
         line = {"metric": METRIC, "value": world * n / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -624,6 +754,9 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 "compress_kernels_us": compress_phases,
                 "compress_centroid_cta_us": compress_cta,
                 "roofline": roof,
+                "kernels": kernels,
+                "t_dc": t_dc_block,
+                "layer_roofline": layer_roofline,
                 "e2e": {"value": world * n / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                         "how": "K steps, each: pinned H2D of x and zeta, the step, D2H of y; copies on two side "
@@ -631,6 +764,7 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 "clocks": clk.summary(),
                 "uncompressed_baseline": unc,
                 "backward_lsh": bwd,
+                "parity_in_run": parity,
                 "cpu_baseline": cpu}
         if args.share_gpu:
             line["share_gpu"] = "all ranks time-slice cuda:0: a correctness run of the N>1 path, not a measurement"

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 __all__ = ["LayerConfig", "CONFIGS", "make_centers", "make_tokens", "make_gate", "make_experts",
-           "rotation_seed", "make_rank_inputs", "torch_dtype", "make_codes", "make_zipf_gate"]
+           "rotation_seed", "make_rank_inputs", "torch_dtype", "make_codes", "make_zipf_gate", "gate_matrix"]
 
 
 @dataclass(frozen=True)
@@ -96,9 +96,14 @@ def make_tokens(cfg: LayerConfig, master_seed: int, rank: int = 0, n: Optional[i
     return torch.from_numpy(X).to(torch.float32).to(torch_dtype(cfg.dtype)).contiguous()
 
 
+def gate_matrix(cfg: LayerConfig, master_seed: int) -> np.ndarray:
+    """The linear gate scorer W_g [E, d] ~ N(0, 1/d) (fp64) that make_gate draws."""
+    return _rng(master_seed, 2).standard_normal((cfg.E, cfg.d)) / np.sqrt(cfg.d)
+
+
 def make_gate(cfg: LayerConfig, master_seed: int, X: torch.Tensor, with_weights: bool = False):
     """zeta int32 [n, k] (ascending expert ids per row) and optional softmax weights fp32."""
-    Wg = _rng(master_seed, 2).standard_normal((cfg.E, cfg.d)) / np.sqrt(cfg.d)
+    Wg = gate_matrix(cfg, master_seed)
     S = X.to(torch.float64).numpy() @ Wg.T
     order = np.argsort(-S, axis=1, kind="stable")          # ties keep the smaller expert id first
     top = np.sort(order[:, :cfg.k], axis=1).astype(np.int32)
