@@ -38,9 +38,10 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--q", type=int, default=None, help="override the number of hash functions")
     p.add_argument("--impl", default="lsh", choices=["lsh", "reference"])
-    p.add_argument("--hash", default="cp", choices=["cp", "sp", "cp8"],
-                   help="hash family: cross-polytope (paper default, Eq. 3), spherical-plane (NEXT-3), or "
-                        "cross-polytope on e4m3 operands (NEXT-2 fp8 option)")
+    p.add_argument("--hash", default="cp", choices=["cp", "sp", "cp8", "hd3"],
+                   help="hash family: cross-polytope (paper default, Eq. 3), spherical-plane (NEXT-3), "
+                        "cross-polytope on e4m3 operands (NEXT-2 fp8 option), or cross-polytope under the "
+                        "structured rotation H D3 H D2 H D1 (NEXT-4, reading R30)")
     p.add_argument("--sp-bits", type=int, default=12, help="sign bits per SP hash function")
     p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p", "p2p-fused"],
                    help="a6/a8 at N>1: phase 1 (NCCL, one host count sync), phase 2 (device-initiated stores "
@@ -81,6 +82,14 @@ def peaks():
     except Exception:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
                 "source": "fallback (B200_PROFILING.md)"}
+
+
+def pk_clock_ghz():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)["sm_max_mhz"] / 1e3
+    except Exception:
+        return 1.965
 
 
 def ncu_traffic():
@@ -189,6 +198,8 @@ def workload_config(cfg, world, args=None):
         hashing = f"spherical-plane sign bits, {args.sp_bits} per hash (NEXT-3)"
     if args is not None and args.hash == "cp8":
         hashing = "cross-polytope on e4m3-quantised x and R (NEXT-2 fp8 option, reading R28)"
+    if args is not None and args.hash == "hd3":
+        hashing = "cross-polytope under H D3 H D2 H D1 on x padded to 1024 (NEXT-4 structured rotation, reading R30)"
     return {"workload": f"{cfg.name}: {cfg.note}", "hash": hashing, "tokens_per_gpu": cfg.n, "d_model": cfg.d,
             "experts": cfg.E,
             "experts_per_gpu": cfg.E // world, "top_k": cfg.k, "hash_functions": cfg.q, "d_ffn": cfg.d_ffn,
@@ -334,6 +345,7 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     Nrm = L.sp_normals(R, args.sp_bits) if args.hash == "sp" else None
     R8 = L.rotation_e4m3(cfg.d, cfg.q, rotation_seed(args.seed)).to(dev) if args.hash == "cp8" else None
     x8 = torch.empty((n, d), dtype=torch.uint8, device=dev) if args.hash == "cp8" else None
+    S3 = L.hd3_signs(cfg.q, rotation_seed(args.seed)).to(dev) if args.hash == "hd3" else None
 
     def make_stages(Xb, zb, yb):
         """The six calls of one step on token / gate / output buffers (Xb, zb, yb); the
@@ -342,6 +354,8 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
             h = lambda: L.sp_hash(Xb, Nrm, cfg.q, args.sp_bits, codes)   # noqa: E731
         elif args.hash == "cp8":
             h = lambda: (L.quantize_e4m3(Xb, out=x8), L.hash_e4m3(x8, R8, codes))   # noqa: E731
+        elif args.hash == "hd3":
+            h = lambda: L.hash_hd3(Xb, S3, codes)   # noqa: E731
         else:
             h = lambda: L.hash(Xb, R, codes)   # noqa: E731
         return [
@@ -644,7 +658,8 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
         ach = work / (us / 1e6) / 1e9
         return {"kernel": name, "bound": bound, "bytes": work, "us": us, "achieved": ach, "unit": "GB/s",
                 "peak": hbm, "frac": ach / hbm}
-    kernels = [kern("hash: tc_gemm_kernel<ArgmaxEpi>", "tensor", hash_flops, t_hash)]
+    kernels = [kern("hash: tc_gemm_kernel<ArgmaxEpi>", "tensor", hash_flops, t_hash)] if args.hash == "cp" else \
+        [{"kernel": f"hash ({args.hash})", "us": t_hash, "note": "see roofline"}]
     kernels.append(kern("compress: tile + bucket + centroid (3 launches)", "hbm", comp_bytes, t_comp))
     if span.get("centroid"):
         kernels.append(kern("centroid_kernel (span, diagnostics stamps)", "hbm", cent_bytes, span["centroid"]))
@@ -711,6 +726,17 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 "frac": achieved / (2 * pk["bf16_tflops"]), "traffic": None,
                 "per_launch": {"flops": flops, "avg_ms": hash_dev_ms, "eager_stage_ms": hash_ms},
                 "peak_source": pk["source"] + " bf16 dense (burst) x 2 (the guide's fp8:bf16 nominal ratio)"}
+    elif args.hash == "hd3":
+        adds = 3.0 * 1024 * 10 * n * cfg.q                 # three 1024-point FWHTs per (token, hash)
+        alu_peak = 148 * 128 * pk_clock_ghz() * 1e9 / 1e12   # fp32 add lanes per SM x SMs x max clock
+        achieved = adds / (hash_dev_ms / 1e3) / 1e12
+        roof = {"bound": "alu", "kernel": "hd3_hash_kernel (lshmoe_hash_hd3)", "achieved": achieved,
+                "peak": alu_peak, "unit": "Tadd/s", "frac": achieved / alu_peak, "traffic": None,
+                "per_launch": {"fp32_adds": adds, "avg_ms": hash_dev_ms, "eager_stage_ms": hash_ms,
+                               "dense_equivalent_tflops": 2.0 * n * cfg.q * d * d / (hash_dev_ms / 1e3) / 1e12},
+                "peak_source": "148 SMs x 128 fp32 lanes x sm_max_mhz (B200_PROFILING.md / MEASURED_PEAKS.json): "
+                               "the CUDA-core fp32 add rate; the algorithmic work is 3 x 1024 x log2(1024) "
+                               "add/sub per (token, hash)"}
     elif args.hash == "sp":
         nbytes = n * d * 2 + L.sp_rows(cfg.q, args.sp_bits) * d * 2 + n * cfg.q * 2
         achieved = nbytes / (hash_dev_ms / 1e3) / 1e9
@@ -735,6 +761,8 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu, parity = cpu_baseline(cfg, args.seed, X_cpu, zeta_cpu, make_experts(cfg, args.seed),
                                    codes.cpu().numpy() if args.hash == "cp" else None)
+        if args.hash != "cp":
+            parity["note"] = "hash near-ties / mismatches above refer to the Eq. 3 dense-rotation hash (the oracle's cp_hash)"
 
     if rank == 0:
         line = {"metric": METRIC, "value": world * n / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,

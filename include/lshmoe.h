@@ -134,6 +134,22 @@ lshmoe_status lshmoe_quantize_e4m3(const void* x, int64_t n, int d, uint8_t* x8,
 lshmoe_status lshmoe_hash_e4m3(const uint8_t* x8, int64_t n, int d, const uint8_t* rotation8, int q, int16_t* codes,
                                void* workspace, size_t workspace_bytes, lshmoe_stream stream);
 
+/* ---- NEXT-4: structured pseudo-random rotation (Eq. 3's R) ---------------
+   Reading R30: x is zero-padded to d' = 1024 and rotated by R_j = H D3_j H D2_j H D1_j (H the
+   unnormalised Sylvester Hadamard matrix of order 1024, D_r,j random +-1 diagonals); the code is
+   Eq. 3's signed argmax over the 1024 outputs: code_tj = sign(y_i*) (i* + 1), i* in [0, 1024),
+   ties to the smallest i, a zero winner '+'.  Codes feed lshmoe_compress like lshmoe_hash's.
+   lshmoe_hd3_signs: [host] out [q][3][32] uint32: bit (i % 32) of word (j*3 + r)*32 + i/32 is 1 iff
+     D_(r+1),j[i] = -1, where that is bit 63 of SplitMix64 output r*1024 + i + 1 of the stream seeded
+     with rotation_seed ^ (0xD1B54A32D192ED03 * (j+1)).  Pure host function, deterministic.
+   lshmoe_hash_hd3: x [n, d] dtype (device), signs [q][3][32] (device copy of the above) -> codes
+     int16 [n, q].  Three fast Walsh-Hadamard transforms per hash in fp32 on the CUDA cores (no
+     tensor cores); the result differs from exact arithmetic only where the oracle's top-two margin
+     is below ~1e-5 (reported as near-ties).  Requires d <= 1024, d % 8 == 0 (bf16) / % 4 (f32). */
+lshmoe_status lshmoe_hd3_signs(int q, uint64_t rotation_seed, uint32_t* out /* [host] */);
+lshmoe_status lshmoe_hash_hd3(const void* x, lshmoe_dtype dtype, int64_t n, int d, const uint32_t* signs, int q,
+                              int16_t* codes, lshmoe_stream stream);
+
 /* ---- NEXT-3: spherical-plane (SP) hash, the paper's other evaluated family (§4.5) --
    The paper gives no construction; SPEC's sign-bit reading (reading R26): hash
    function j owns the b unit normals in rows j*b .. j*b+b-1 of `normals`, and

@@ -47,6 +47,8 @@ _SIGS = {
     "lshmoe_quantize_e4m3": ([_vp, _i64, _i32, _vp, _vp], _i32),
     "lshmoe_hash_e4m3": ([_vp, _i64, _i32, _vp, _i32, _vp, _vp, _sz, _vp], _i32),
     "lshmoe_sp_rows": ([_i32, _i32], _i32),
+    "lshmoe_hd3_signs": ([_i32, _u64, _vp], _i32),
+    "lshmoe_hash_hd3": ([_vp, _i32, _i64, _i32, _vp, _i32, _vp, _vp], _i32),
     "lshmoe_sp_hash": ([_vp, _i32, _i64, _i32, _vp, _i32, _i32, _vp, _vp], _i32),
     "lshmoe_expert_ffn_backward": ([_vp, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp],
                                    _i32),
@@ -269,6 +271,29 @@ def sp_hash(x: torch.Tensor, normals: torch.Tensor, q: int, b: int, codes: Optio
         codes = torch.empty((n, q), dtype=torch.int16, device=x.device)
     _check(_lib.lshmoe_sp_hash(_ptr(x), _dt(x), n, d, _ptr(normals), q, b, _ptr(codes), _stream(stream)),
            "lshmoe_sp_hash")
+    return codes
+
+
+# ---- NEXT-4: structured rotation (reading R30) ----------------------------------------------------
+def hd3_signs(q: int, seed: int) -> torch.Tensor:
+    """The +-1 diagonals of the q structured rotations as sign bits: host int32 tensor [q, 3, 32]
+    (bit i % 32 of word i / 32 set = -1)."""
+    out = torch.empty((q, 3, 32), dtype=torch.int32)
+    _check(_lib.lshmoe_hd3_signs(q, seed & (2 ** 64 - 1), _ptr(out)), "lshmoe_hd3_signs")
+    return out
+
+
+def hash_hd3(x: torch.Tensor, signs: torch.Tensor, codes: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Cross-polytope codes int16 [n, q] in +-1..+-1024 under H D3 H D2 H D1 on x padded to 1024."""
+    _require_cuda(x, signs)
+    n, d = x.shape
+    q = signs.shape[0]
+    if signs.dtype != torch.int32 or tuple(signs.shape) != (q, 3, 32) or not signs.is_contiguous():
+        raise ValueError("signs must be a contiguous int32 [q, 3, 32] device tensor (hd3_signs)")
+    if codes is None:
+        codes = torch.empty((n, q), dtype=torch.int16, device=x.device)
+    _check(_lib.lshmoe_hash_hd3(_ptr(x), _dt(x), n, d, _ptr(signs), q, _ptr(codes), _stream(stream)),
+           "lshmoe_hash_hd3")
     return codes
 
 

@@ -153,6 +153,28 @@ lshmoe_status lshmoe_hash_e4m3(const uint8_t* x8, int64_t n, int d, const uint8_
   return cuda_status(launch_hash_e4m3(x8, n, d, R8, q, codes, workspace, stream), "lshmoe_hash_e4m3");
 }
 
+lshmoe_status lshmoe_hd3_signs(int q, uint64_t rotation_seed, uint32_t* out) {
+  REQUIRE(q >= 1, LSHMOE_EINVAL, "q < 1");
+  REQUIRE(q <= LSHMOE_MAX_Q, LSHMOE_EUNSUPPORTED, "q > LSHMOE_MAX_Q");
+  REQUIRE(out != nullptr, LSHMOE_EINVAL, "out is NULL");
+  hd3_signs_host(q, rotation_seed, out);
+  return LSHMOE_OK;
+}
+
+lshmoe_status lshmoe_hash_hd3(const void* x, lshmoe_dtype dtype, int64_t n, int d, const uint32_t* signs, int q,
+                              int16_t* codes, lshmoe_stream stream) {
+  REQUIRE(dtype == LSHMOE_F32 || dtype == LSHMOE_BF16, LSHMOE_EINVAL, "bad dtype");
+  REQUIRE(n >= 0 && d >= 1, LSHMOE_EINVAL, "n < 0 or d < 1");
+  REQUIRE(q >= 1, LSHMOE_EINVAL, "q < 1");
+  REQUIRE(q <= LSHMOE_MAX_Q, LSHMOE_EUNSUPPORTED, "q > LSHMOE_MAX_Q");
+  REQUIRE(d <= 1024, LSHMOE_EUNSUPPORTED, "the structured rotation pads x to 1024: d <= 1024");
+  REQUIRE(d % (dtype == LSHMOE_BF16 ? 8 : 4) == 0, LSHMOE_EUNSUPPORTED, "needs d % 8 == 0 (bf16) / d % 4 == 0 (f32)");
+  if (n == 0) return LSHMOE_OK;
+  REQUIRE(x && signs && codes, LSHMOE_EINVAL, "NULL pointer");
+  REQUIRE(aligned16(x), LSHMOE_EINVAL, "x must be 16-byte aligned");
+  return cuda_status(launch_hd3_hash(x, dtype == LSHMOE_BF16, n, d, signs, q, codes, stream), "lshmoe_hash_hd3");
+}
+
 int lshmoe_sp_rows(int q, int b) { return (q >= 1 && b >= 1 && q * b <= 256) ? sp_rows(q, b) : 0; }
 
 lshmoe_status lshmoe_sp_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, const void* normals, int q, int b,

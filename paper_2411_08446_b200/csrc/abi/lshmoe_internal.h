@@ -16,6 +16,9 @@ lshmoe_status cuda_status(int cuda_err, const char* what);   // ECUDA with cudaG
 // ---- host ---------------------------------------------------------------------------------
 lshmoe_status rotation_host(int d, int q, uint64_t seed, lshmoe_dtype dtype, void* out);
 lshmoe_status rotation_e4m3_host(int d, int q, uint64_t seed, uint8_t* out);
+void hd3_signs_host(int q, uint64_t seed, uint32_t* out);   // NEXT-4 sign bits [q][3][32]
+int launch_hd3_hash(const void* x, int is_bf16, int64_t n, int d, const uint32_t* signs, int q, int16_t* codes,
+                    void* stream);
 int launch_quantize_e4m3(const void* x, int64_t n, int d, uint8_t* out, void* stream);
 int launch_gate_hash_bf16(const void* x, int64_t n, int d, const void* RG, int q, int E, int k, int16_t* codes,
                           int32_t* zeta, float* gw, void* ws, void* stream);

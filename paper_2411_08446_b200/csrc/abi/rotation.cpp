@@ -146,4 +146,23 @@ lshmoe_status rotation_e4m3_host(int d, int q, uint64_t seed, uint8_t* out) {
   return LSHMOE_OK;
 }
 
+// NEXT-4 (reading R30): the +-1 diagonals D_1..D_3 of hash j as bit vectors over the d' = 1024
+// padded coordinates.  Entry i of round r is -1 iff bit 63 of SplitMix64 output number
+// r*1024 + i + 1 of the stream seeded with rotation_seed ^ (0xD1B54A32D192ED03 * (j + 1)) is set;
+// out[(j*3 + r)*32 + i/32] bit i%32.
+void hd3_signs_host(int q, uint64_t seed, uint32_t* out) {
+  for (int j = 0; j < q; ++j) {
+    const uint64_t state = seed ^ (0xD1B54A32D192ED03ull * static_cast<uint64_t>(j + 1));
+    for (int r = 0; r < 3; ++r)
+      for (int w = 0; w < 32; ++w) {
+        uint32_t word = 0;
+        for (int b = 0; b < 32; ++b) {
+          const uint64_t z = splitmix64_at(state, static_cast<uint64_t>(r) * 1024 + 32 * w + b + 1);
+          word |= static_cast<uint32_t>(z >> 63) << b;
+        }
+        out[(j * 3 + r) * 32 + w] = word;
+      }
+  }
+}
+
 }  // namespace lshmoe

@@ -127,3 +127,14 @@ def test_no_oracle_import_in_product():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle", src, flags=re.M), f
                 assert "lshmoe_oracle" not in src, f
+
+
+@pytest.mark.parametrize("q,seed", [(1, 0), (6, 2 ** 63 + 11), (3, None)])
+def test_hd3_sign_bits_equal_oracle(L, q, seed):
+    """NEXT-4 (reading R30): the library's host sign generator == the oracle's independent one."""
+    if seed is None:
+        seed = rotation_seed(0)
+    bits = L.hd3_signs(q, seed).numpy().view(np.uint32)                 # [q, 3, 32]
+    D = O.hd3_signs(q, seed)                                            # [q, 3, 1024] of +-1
+    lib = np.where((bits[..., :, None] >> np.arange(32, dtype=np.uint32)) & 1, -1.0, 1.0).reshape(q, 3, 1024)
+    assert np.array_equal(lib, D)
