@@ -929,12 +929,33 @@ __device__ __forceinline__ void prefetch_cut_extent(const Params& P, CentroidCtx
   }
 }
 
+// The index entries i = tid + kThreads u (u < kPre) of a CTA's range, loaded right after the
+// kernel's dependency wait so that their latency overlaps the expert-count scan.
+constexpr int kPre = 4;
+struct IndexPre {
+  int l[kPre], c[kPre];
+};
+__device__ __forceinline__ void preload_index(const Params& P, IndexPre& pre) {
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const int pb = range_begin(b, P.nk, G), range = range_begin(b + 1, P.nk, G) - pb;
+#pragma unroll
+  for (int u = 0; u < kPre; ++u) {
+    const int i = tid + kThreads * u, p = pb - 1 + i;
+    pre.l[u] = 0;
+    pre.c[u] = 0;
+    if (i < range + 2 && p >= 0 && p < P.nk) {
+      pre.l[u] = ldcg(P.rowl + p);
+      if (i >= 1 && i <= range) pre.c[u] = ldcg(P.perm + p);
+    }
+  }
+}
+
 // Phase B of one CTA: its perm range's rows (global ids = row offset of the expert + local row),
 // token ids and bucket outputs, then the centroid reduction.  s_cut[0..1] receive the (expert,
 // local row) of the range's first and last entries for the cut-row merge.
 template <typename T, bool kF = false>
-__device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_roff, const int* s_mrow, int* s_cut,
-                               CentroidCtx& X) {
+__device__ __forceinline__ void centroid_phase(const Params& P, const int* s_goff, const int* s_roff, const int* s_mrow,
+                                               int* s_cut, CentroidCtx& X, const IndexPre& pre) {
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
   X.p_begin = range_begin(b, P.nk, G);
   X.p_end = range_begin(b + 1, P.nk, G);
@@ -945,15 +966,22 @@ __device__ void centroid_phase(const Params& P, const int* s_goff, const int* s_
   X.tok_off = P.max_range + 2;
   uint32_t* s_row = X.s_row();
   int32_t* s_tok = X.s_tok();
-  for (int i = tid; i < X.range + 2; i += kThreads) {
+#pragma unroll 1
+  for (int i = tid, u = 0; i < X.range + 2; i += kThreads, ++u) {
     const int p = X.p_begin - 1 + i;
     uint32_t row = 0xFFFFFFFFu;
     if (p >= 0 && p < P.nk) {
       const int e = expert_at(s_goff, P.E, p);
-      const int lr = ldcg(P.rowl + p);
+      int lr, c = 0;
+      if (u < kPre) {                        // preloaded (registers, static indices)
+        lr = u == 0 ? pre.l[0] : u == 1 ? pre.l[1] : u == 2 ? pre.l[2] : pre.l[3];
+        c = u == 0 ? pre.c[0] : u == 1 ? pre.c[1] : u == 2 ? pre.c[2] : pre.c[3];
+      } else {
+        lr = ldcg(P.rowl + p);
+        if (i >= 1 && i <= X.range) c = ldcg(P.perm + p);
+      }
       row = static_cast<uint32_t>(s_roff[e] + lr);
       if (i >= 1 && i <= X.range) {
-        const int c = ldcg(P.perm + p);
         s_tok[i - 1] = c / P.k;
         P.bucket[c] = static_cast<int32_t>(row);
         if (i == 1) { s_cut[0] = e; s_cut[1] = lr; }
@@ -994,8 +1022,7 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
   const int G = gridDim.x, tid = threadIdx.x;
   if (X.range == 0) return;
   __syncthreads();                            // the CTA's partial writes precede the arrivals (bar.sync),
-  if (tid < 2) {                              // and the arriving thread's gpu fence is cumulative
-    __threadfence();                          // publish this CTA's partials before arriving
+  if (tid < 2) {                              // and the arriving thread's release is cumulative
     // thread `which` handles one candidate row
     const int which = tid;
     s_job[4 * which] = -1;
@@ -1011,9 +1038,10 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
         expected = 0;
         for (int bb = b0; bb <= b1; ++bb) expected += range_begin(bb + 1, P.nk, G) > range_begin(bb, P.nk, G);
       }
-      const int old = atomicAdd(reinterpret_cast<int*>(P.bar) + kArrive + b0, 1);   // counters start at -1
+      int old;                                // counters start at -1; acq_rel: publish ours, acquire theirs
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                   : "=r"(old) : "l"(reinterpret_cast<int*>(P.bar) + kArrive + b0) : "memory");
       if (old + 2 == expected) {
-        __threadfence();                      // acquire the other CTAs' partials
         reinterpret_cast<int*>(P.bar)[kArrive + b0] = -1;   // leave the counter at rest for the next call
         s_job[4 * which + 0] = static_cast<int>(which == 0 ? r0 : rl);
         s_job[4 * which + 1] = rs;
@@ -1186,6 +1214,8 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   pdl_wait();                                // K2's perm, rows and counts are complete
   pdl_trigger();
   dstamp(P, 2, 0);
+  IndexPre pre;
+  if (!P.permute) preload_index(P, pre);      // in flight during the expert-count scan below
   if (!P.permute)                             // K2 was the table's last reader: leave it at rest (-1)
     for (int64_t i = blockIdx.x * int64_t(kThreads) + tid; i <= P.mask; i += int64_t(gridDim.x) * kThreads)
       P.table[i] = -1;
@@ -1196,10 +1226,11 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   }
   {
     const int m_e = tid < P.E ? ldcg(P.expert_rows + tid) : 0;
+    const int go = tid < P.E ? ldcg(P.gofs + tid) : 0;   // in flight with m_e (and the index preload)
     int m;
     const int ro = block_excl_scan<kWarps>(m_e, s_scan, &m);
     if (tid < P.E) {
-      s_goff[tid] = ldcg(P.gofs + tid);
+      s_goff[tid] = go;
       s_roff[tid] = ro;
       s_mrow[tid] = m_e;
     }
@@ -1213,21 +1244,42 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
     }
     __syncthreads();
   }
-  for (int e = blockIdx.x; e < P.E; e += gridDim.x)   // row_start of every global row
-    for (int r = tid; r < s_mrow[e]; r += kThreads) P.row_start[s_roff[e] + r] = ldcg(P.rsl + s_goff[e] + r);
+  // row_start of every global row: rows r = blockIdx.x + G (tid + kThreads u) of this CTA, loaded now
+  // and stored after the reduction, so the load's round trip is off every CTA's critical path
+  constexpr int kRS = 2;
+  int rs_val[kRS];
+  const int m_all = s_roff[P.E];
+#pragma unroll
+  for (int u = 0; u < kRS; ++u) {
+    const int r = blockIdx.x + gridDim.x * (tid + kThreads * u);
+    rs_val[u] = 0;
+    if (r < m_all) {
+      const int e = expert_at(s_roff, P.E, r);
+      rs_val[u] = ldcg(P.rsl + s_goff[e] + (r - s_roff[e]));
+    }
+  }
   uint32_t f_epoch = 0;
   if constexpr (kF) fused_prologue(P, s_roff, s_mrow, &f_epoch);
   // per-CTA centroid-phase start / end stamps (diagnostics, bar[64 + 2 * cta])
   if (P.diag && tid == 0 && blockIdx.x < 1024) P.bar[64 + 2 * blockIdx.x] = globaltimer_lo();
   CentroidCtx X;
   if (P.is_bf16) {
-    centroid_phase<__nv_bfloat16, kF>(P, s_goff, s_roff, s_mrow, s_cut, X);
+    centroid_phase<__nv_bfloat16, kF>(P, s_goff, s_roff, s_mrow, s_cut, X, pre);
     dstamp(P, 2, 2);
     merge_cut_rows<__nv_bfloat16, kF>(P, X, s_goff, s_mrow, s_cut, s_job);
   } else {
-    centroid_phase<float, kF>(P, s_goff, s_roff, s_mrow, s_cut, X);
+    centroid_phase<float, kF>(P, s_goff, s_roff, s_mrow, s_cut, X, pre);
     dstamp(P, 2, 2);
     merge_cut_rows<float, kF>(P, X, s_goff, s_mrow, s_cut, s_job);
+  }
+#pragma unroll
+  for (int u = 0; u < kRS; ++u) {
+    const int r = blockIdx.x + gridDim.x * (tid + kThreads * u);
+    if (r < m_all) P.row_start[r] = rs_val[u];
+  }
+  for (int r = blockIdx.x + gridDim.x * (tid + kThreads * kRS); r < m_all; r += gridDim.x * kThreads) {
+    const int e = expert_at(s_roff, P.E, r);     // (m > G * 512 rows only)
+    P.row_start[r] = ldcg(P.rsl + s_goff[e] + (r - s_roff[e]));
   }
   __syncthreads();
   if constexpr (kF) fused_close(P, f_epoch);   // every row was stored to its owner in the loop
@@ -1342,6 +1394,14 @@ int launch_pdl(K kernel, int grid, int block, int smem, cudaStream_t st, const P
   return err;
 }
 
+bool carveout_max() {
+  static const bool on = [] {
+    const char* e = getenv("LSHMOE_CARVEOUT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int launch_chain(const Params& P, cudaStream_t st) {
   static bool configured = false;
   const int max_range = centroid_max_range(P.nk);
@@ -1351,6 +1411,10 @@ int launch_chain(const Params& P, cudaStream_t st) {
     int err = cudaFuncSetAttribute(centroid_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCentroidSmemMax);
     if (!err) err = cudaFuncSetAttribute(centroid_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCentroidSmemMax);
     if (!err) err = cudaFuncSetAttribute(bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBucketSmem);
+    // every kernel of the step prefers the full shared-memory carveout, so an SM never has to drain
+    // and re-partition L1 / shared memory between two kernels of the chain (LSHMOE_CARVEOUT=0: off)
+    if (!err && carveout_max()) err = cudaFuncSetAttribute(tile_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                           cudaSharedmemCarveoutMaxShared);
     if (err) return err;
     configured = true;
   }

@@ -65,21 +65,75 @@ struct WorkItem {
   int valid_rows;  // rows of this CTA's slice that are real outputs (may be <= 0)
   int tag0, tag1;  // epilogue-specific (hash: (m tile, j) id, j; FFN: expert, n0)
   int part, nparts;  // hash: which BN-column slice of the d coordinates this unit covers
+  int pmask;         // hash: bit s set = a piece of this (tile, j) starts at slice s (merge slots)
 };
 
 // ---- schedulers (units are per cluster; bm = 128 * kCta rows per unit) ----------------------
 // Hash units are (token tile, hash j, BN-column slice): d / BN times more units than (tile, j),
 // so the persistent grid's last wave is nearly full (C2: 2304 units over 148 SMs instead of 768).
 // The slices of one (tile, j) are merged by the last one to finish (ArgmaxEpi::finish).
+// Contiguous mode (contig = 1, no gate): cluster g takes the contiguous range [g T / G, (g+1) T / G)
+// of the T = m_tiles * q * (d / BN) accumulator chunks, ordered (tile, j, slice); its k-th unit is
+// the k-th (tile, j) piece inside that range, all of whose chunks it drains with one running argmax.
+// Only a (tile, j) cut by a range boundary (at most two per cluster) needs the cross-CTA merge, so
+// the per-unit merge protocol (a global atomic round trip and three epilogue barriers) that bounded
+// the round-robin split schedule is gone from all other units.  Units past a cluster's last piece
+// are empty (nchunks = 0).
+__device__ __forceinline__ int crange_begin(int g, int T, int G) {
+  return static_cast<int>(static_cast<int64_t>(g) * T / G);
+}
+__device__ __forceinline__ int crange_owner(int c, int T, int G) {   // cluster whose range holds chunk c
+  return static_cast<int>((static_cast<int64_t>(c + 1) * G - 1) / T);
+}
+
 struct HashSched {
   int n, q, d, bn, bm;
   int prefetch_b;   // 0: the rotations are L2-resident
   int m_tiles;
   int gate;         // NEXT-2: 1 = one extra unit per token tile for the gate scores (B rows q*d ..)
+  int contig;       // 1: contiguous chunk ranges per cluster (see above)
+  int G;            // clusters (contig)
+  int max_pieces;   // units per cluster (contig)
   __device__ void init(void*) {}
   int split;   // 1: one unit per BN slice; 0: one unit covers all d / BN slices (no merge)
-  __device__ int units() const { return m_tiles * (q * (split ? d / bn : 1) + gate); }
+  __device__ int units() const {
+    if (contig) return G * max_pieces;
+    return m_tiles * (q * (split ? d / bn : 1) + gate);
+  }
+  __device__ WorkItem get_contig(int u, int rank) const {
+    WorkItem w;
+    const int np = d / bn;
+    const int T = m_tiles * q * np;
+    const int g = u % G, k = u / G;
+    const int c0 = crange_begin(g, T, G), c1 = crange_begin(g + 1, T, G);
+    const int p = c0 / np + k;                 // (tile, j) pair of this piece
+    const int first = max(c0, p * np), last = min(c1, p * np + np);
+    const int mt = p / q, j = p - (p / q) * q;
+    w.a_row = mt * bm + rank * BM;
+    w.valid_rows = min(BM, n - w.a_row);
+    w.nparts = np;
+    w.tag1 = j;
+    w.tag0 = (mt * (bm / BM) + rank) * q + j;
+    if (first >= last || c0 >= c1) {           // past this cluster's last piece
+      w.nchunks = 0;
+      w.part = 0;
+      w.b_row0 = 0;
+      w.pmask = 0;
+      return w;
+    }
+    w.part = first - p * np;
+    w.nchunks = last - first;
+    w.b_row0 = j * d + w.part * bn;
+    int mask = 0;                              // where the pieces of pair p start (one per cluster)
+    for (int gg = crange_owner(p * np, T, G); gg <= crange_owner(p * np + np - 1, T, G); ++gg) {
+      const int b0 = max(crange_begin(gg, T, G), p * np), b1 = min(crange_begin(gg + 1, T, G), p * np + np);
+      if (b0 < b1) mask |= 1 << (b0 - p * np);
+    }
+    w.pmask = mask;
+    return w;
+  }
   __device__ WorkItem get(int u, int rank) const {
+    if (contig) return get_contig(u, rank);
     WorkItem w;
     const int np = split ? d / bn : 1;
     const int upt = q * np + gate;             // units per token tile: slices fastest, then j, then the gate
@@ -93,6 +147,7 @@ struct HashSched {
       w.tag1 = q;
       w.part = 0;
       w.nparts = 1;
+      w.pmask = 1;
       return w;
     }
     const int j = r / np, c = r - j * np;
@@ -103,11 +158,13 @@ struct HashSched {
       w.nchunks = d / bn;
       w.part = 0;
       w.nparts = 1;
+      w.pmask = 1;
     } else {
       w.b_row0 = j * d + c * bn;
       w.nchunks = 1;
       w.part = c;
       w.nparts = np;
+      w.pmask = (1 << np) - 1;
     }
     return w;
   }
@@ -195,6 +252,7 @@ struct FfnSched {
     w.tag1 = nt * bn;
     w.part = 0;
     w.nparts = 1;
+    w.pmask = 1;
     return w;
   }
 };
@@ -288,7 +346,7 @@ struct ArgmaxEpiT {
       // acq_rel: releases this CTA's winners (ordered before by bar.sync), acquires the others'
       int old;
       asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(counter + w.tag0) : "memory");
-      const int last = old == w.nparts - 1;
+      const int last = old == __popc(w.pmask) - 1;
       if (last) counter[w.tag0] = 0;                        // leave the workspace zeroed
       *flag = last;
     }
@@ -298,7 +356,8 @@ struct ArgmaxEpiT {
     if (!last || half != 0 || row >= w.valid_rows) return;
     float b = -1.0f;
     uint32_t bi = 0;
-    for (int p = 0; p < w.nparts; ++p) {
+    for (int p = 0; p < w.nparts; ++p) {             // the pieces in slice order
+      if (!((w.pmask >> p) & 1)) continue;
       const uint2 v = __ldcg(partial + (static_cast<int64_t>(p) * rows_pad + t) * q + w.tag1);
       const float a = __uint_as_float(v.x);
       if (a > b) {
@@ -410,6 +469,7 @@ struct ArgmaxEpiT {
         return;
       }
     }
+    if (w.nchunks == 0) return;                      // an empty unit (contiguous schedule)
     merge_chains();
     if (nthr > 128) {   // combine the two column halves of each row; the lower half wins ties
       uint2* mb = reinterpret_cast<uint2*>(scratch + 64);
@@ -425,7 +485,7 @@ struct ArgmaxEpiT {
       }
       asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
     }
-    if (w.nparts > 1) {
+    if (w.nchunks < w.nparts) {                      // a piece of a cut (tile, j): merge
       finish_split(w, row, scratch, half, nthr);
       return;
     }
@@ -907,6 +967,21 @@ size_t hash_workspace_bytes(int64_t n, int d, int q) {
   return counters + sizeof(uint2) * static_cast<size_t>(d / bn) * rows_pad * q;
 }
 
+// Contiguous chunk ranges per cluster (HashSched::contig) unless LSHMOE_HASH_CONTIG=0; returns the
+// cluster count G the launch must use.
+int set_contig(HashSched& s, int cta, int np) {
+  const int T = s.m_tiles * s.q * np;
+  int G = device_sm_count() / cta;
+  if (T < G) G = T;
+  const char* env = getenv("LSHMOE_HASH_CONTIG");
+  if (env && env[0] == '0') return T;   // round-robin split units (A/B)
+  s.contig = 1;
+  s.G = G;
+  const int per = (T + G - 1) / G;
+  s.max_pieces = (per + np - 1) / np + 1;
+  return G;
+}
+
 int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int16_t* codes, void* ws, void* stream) {
   const int cta = cta_mode("LSHMOE_HASH_CTA", 1);
   HashSched s{};
@@ -929,8 +1004,9 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
     e.counter = static_cast<int*>(ws);
     e.partial = reinterpret_cast<uint2*>(static_cast<uint8_t*>(ws) + counters);
   }
-  return launch_bn(bn, cta, x, n, R, static_cast<int64_t>(q) * d, d, s, e, s.m_tiles * q * (s.split ? d / bn : 1),
-                   static_cast<cudaStream_t>(stream));
+  int hint = s.m_tiles * q * (s.split ? d / bn : 1);
+  if (s.split) hint = set_contig(s, cta, d / bn);
+  return launch_bn(bn, cta, x, n, R, static_cast<int64_t>(q) * d, d, s, e, hint, static_cast<cudaStream_t>(stream));
 }
 
 // NEXT-2 gate + hash in one pass over x (reading R29): B = [R ; W_g] ([q*d + E, d]); per token
@@ -992,7 +1068,7 @@ int launch_hash_e4m3(const void* x8, int64_t n, int d, const void* R8, int q, in
   if (err) return err;
   err = make_map(&mb, R8, static_cast<int64_t>(q) * d, d, bn, 1);
   if (err) return err;
-  const int units = s.m_tiles * q * (s.split ? d / bn : 1);
+  const int units = s.split ? set_contig(s, 1, d / bn) : s.m_tiles * q;
   const int grid = std::min(device_sm_count(), units);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (bn) {

@@ -50,6 +50,74 @@ __global__ void __launch_bounds__(256) restore_kernel(const T* x /* y may alias 
   }
 }
 
+// Warp per token row: lanes over the row's 16-byte chunks, the row's k bucket ids loaded once, and
+// the next row's bucket id and x chunks fetched before the current row's c~ / E(c~) gathers are
+// combined, so the dependent bucket -> gather chain of the next row overlaps this row's.  Measured
+// (C2, graph-replayed, clean cold L2): 14.3 us against 18.4 us for the flat thread-per-chunk kernel;
+// at d = 1024 (C3, C4) the flat kernel stays ahead, so the row kernel serves k = 1 rows of <= 96
+// chunks (LSHMOE_RESTORE_VAR: 0 forces the flat kernel, 2 / 4 the row kernel with 2 / 4 CTAs per SM).
+template <typename T, int CPL>
+__global__ void __launch_bounds__(256) restore_row_kernel(const T* x, const T* __restrict__ ct,
+                                                          const T* __restrict__ ret, int64_t n, int d, int cpr,
+                                                          const int32_t* __restrict__ bucket, int k,
+                                                          const float* __restrict__ g, T* y) {
+  constexpr int VN = Vec<T>::N;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) >> 5;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * 8;
+  uint4 xr[CPL];
+  int32_t bn = 0;
+  auto fetch = [&](int64_t t) {
+    bn = __ldg(bucket + t * k);
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int c = lane + 32 * j;
+      if (c < cpr) xr[j] = __ldg(reinterpret_cast<const uint4*>(x + t * d) + c);
+    }
+  };
+  if (w0 < n) fetch(w0);
+  for (int64_t t = w0; t < n; t += nw) {
+    float acc[CPL][VN];
+    const int32_t b0 = bn;
+    float xv[CPL][VN];
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) Vec<T>::load(&xr[j], xv[j]);
+    if (t + nw < n) fetch(t + nw);
+    for (int s = 0; s < k; ++s) {
+      const int64_t b = s == 0 ? b0 : __ldg(bucket + t * k + s);
+      const float gw = g ? g[t * k + s] : 1.0f;
+      uint4 cr[CPL], rr[CPL];
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        const int c = lane + 32 * j;
+        if (c < cpr) {
+          cr[j] = __ldg(reinterpret_cast<const uint4*>(ct + b * d) + c);
+          rr[j] = __ldg(reinterpret_cast<const uint4*>(ret + b * d) + c);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        float cv[VN], rv[VN];
+        Vec<T>::load(&cr[j], cv);
+        Vec<T>::load(&rr[j], rv);
+#pragma unroll
+        for (int v = 0; v < VN; ++v) {
+          float term = rv[v] + (xv[j][v] - cv[v]);
+          if (g) term = gw * term;
+          acc[j][v] = (s == 0) ? term : acc[j][v] + term;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int c = lane + 32 * j;
+      if (c < cpr) Vec<T>::store(y + t * d + c * VN, acc[j]);
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) unpermute_kernel(const T* __restrict__ ret, int64_t n, int d,
                                                         const int32_t* __restrict__ slot, int k,
@@ -190,11 +258,18 @@ int grid_for(int64_t work) {
 
 }  // namespace
 
+int restore_variant() {   // -1: the measured default (see restore_row_kernel)
+  const char* v = getenv("LSHMOE_RESTORE_VAR");
+  return v ? atoi(v) : -1;
+}
+
 template <typename T>
 int launch_restore_pdl(const void* x, const void* ct, const void* ret, int64_t n, int d, const int32_t* bucket, int k,
                        const float* g, void* y, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid_for(n * (d / Vec<T>::N)));
+  const int cpr = d / Vec<T>::N;
+  const int64_t total = n * cpr;
+  cfg.gridDim = dim3(grid_for(total));
   cfg.blockDim = dim3(256);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -202,8 +277,33 @@ int launch_restore_pdl(const void* x, const void* ct, const void* ret, int64_t n
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, restore_kernel<T>, static_cast<const T*>(x), static_cast<const T*>(ct),
-                            static_cast<const T*>(ret), n, d, bucket, k, g, static_cast<T*>(y));
+  static bool carve = [] {   // full shared-memory carveout like the step's other kernels (no re-partition)
+    const char* e = getenv("LSHMOE_CARVEOUT");
+    if (e && e[0] == '0') return false;
+    cudaFuncSetAttribute(restore_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(restore_row_kernel<T, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(restore_row_kernel<T, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(restore_row_kernel<T, 3>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(restore_row_kernel<T, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    return true;
+  }();
+  (void)carve;
+  int var = restore_variant();
+  if (var < 0) var = (k == 1 && cpr >= 32 && cpr <= 96) ? 2 : 0;
+  const T* xp = static_cast<const T*>(x);
+  const T* cp = static_cast<const T*>(ct);
+  const T* rp = static_cast<const T*>(ret);
+  T* yp = static_cast<T*>(y);
+  if (var >= 2 && cpr >= 32 && cpr <= 128) {
+    const int warps = static_cast<int>(std::min<int64_t>(n, int64_t(var) * 8 * device_sm_count()));
+    cfg.gridDim = dim3(std::max(1, (warps + 7) / 8));
+    const int cpl = (cpr + 31) / 32;
+    if (cpl == 1) return cudaLaunchKernelEx(&cfg, restore_row_kernel<T, 1>, xp, cp, rp, n, d, cpr, bucket, k, g, yp);
+    if (cpl == 2) return cudaLaunchKernelEx(&cfg, restore_row_kernel<T, 2>, xp, cp, rp, n, d, cpr, bucket, k, g, yp);
+    if (cpl == 3) return cudaLaunchKernelEx(&cfg, restore_row_kernel<T, 3>, xp, cp, rp, n, d, cpr, bucket, k, g, yp);
+    return cudaLaunchKernelEx(&cfg, restore_row_kernel<T, 4>, xp, cp, rp, n, d, cpr, bucket, k, g, yp);
+  }
+  return cudaLaunchKernelEx(&cfg, restore_kernel<T>, xp, cp, rp, n, d, bucket, k, g, yp);
 }
 
 int launch_restore(const void* x, const void* ct, const void* ret, lshmoe_dtype dtype, int64_t n, int d,

@@ -13,6 +13,18 @@ import paper_2411_08446_b200 as L  # noqa: E402
 from lshmoe_inputs import CONFIGS, make_experts, make_rank_inputs, rotation_seed  # noqa: E402
 
 
+_RB = {}
+
+
+def _settle(flush):
+    """Read a second buffer larger than L2: evicts the flush's dirty lines (their write-back happens
+    here, outside the timed region) and leaves L2 holding clean, unrelated lines."""
+    rb = _RB.get(flush.device)
+    if rb is None:
+        rb = _RB[flush.device] = torch.ones(64 * 1024 * 1024, dtype=torch.int32, device=flush.device)
+    rb.max()
+
+
 def timeit(fn, iters=30, flush=None):
     """Device time of fn: captured once into a CUDA graph (no host launch overhead in the timed
     region), replayed between CUDA events; L2 flushed before each replay when flush is given."""
@@ -23,9 +35,13 @@ def timeit(fn, iters=30, flush=None):
     with torch.cuda.graph(g):
         fn()
     ts = []
+    mode = os.environ.get("AB_FLUSH", "write")
     for _ in range(iters):
         if flush is not None:
-            flush.zero_()
+            if mode in ("write", "writeread"):
+                flush.zero_()
+            if mode in ("read", "writeread"):
+                _settle(flush)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         g.replay()
@@ -54,14 +70,24 @@ def main():
             print(f"hash_e4m3 exp={ex}: median {med:.1f} us  min {mn:.1f} us  {flops / med / 1e6:.0f} TFLOP/s", flush=True)
         os.environ.pop("LSHMOE_HASH_EXP")
     if what in ("hash", "all"):
-        for cta in ("1", "2"):
+        for cta in ("1", "2") if not os.environ.get("AB_QUICK") else ():
             for ex in ("1", "2"):
                 os.environ["LSHMOE_HASH_EXP"] = ex
                 os.environ["LSHMOE_HASH_CTA"] = cta
                 med, mn = timeit(lambda: L.hash(X, R, codes), flush=flush)
                 print(f"hash cta={cta} exp={ex} (1: no argmax scan, 2: no MMA): median {med:.1f} us", flush=True)
-        os.environ.pop("LSHMOE_HASH_EXP")
-        os.environ.pop("LSHMOE_HASH_CTA")
+        os.environ.pop("LSHMOE_HASH_EXP", None)
+        os.environ.pop("LSHMOE_HASH_CTA", None)
+        for contig in ("1", "0"):
+            for cta in ("1", "2"):
+                os.environ["LSHMOE_HASH_CONTIG"] = contig
+                os.environ["LSHMOE_HASH_CTA"] = cta
+                med, mn = timeit(lambda: L.hash(X, R, codes), flush=flush)
+                print(f"hash contig={contig} cta={cta}: median {med:.1f} us  min {mn:.1f} us  "
+                      f"{flops / med / 1e6:.0f} TFLOP/s", flush=True)
+        os.environ.pop("LSHMOE_HASH_CONTIG")
+        if os.environ.get("AB_QUICK"):
+            return
         for split in ("1", "2"):
             for cta in ("1", "2"):
                 os.environ["LSHMOE_HASH_SPLIT"] = split
