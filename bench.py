@@ -625,32 +625,35 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     base_off_rows = off_gpu_rows(er)
     nccl_base = None
     if world > 1 and not args.share_gpu:
-        nrecv = torch.empty((cap, d), dtype=X.dtype, device=dev)
-        nret = torch.empty((nk, d), dtype=X.dtype, device=dev)
-        rcnt = torch.empty(world, dtype=torch.int64, device=dev)
+        try:
+            nrecv = torch.empty((cap, d), dtype=X.dtype, device=dev)
+            nret = torch.empty((nk, d), dtype=X.dtype, device=dev)
+            rcnt = torch.empty(world, dtype=torch.int64, device=dev)
 
-        def nccl_step(s_):
-            Xs_, zs_, ys_ = sets[s_]
-            L.permute(Xs_, zs_, cfg.E, send, slot, er, ws)          # rows grouped by destination rank
-            cnt = er.view(world, E_local).sum(1).to(torch.int64)
-            dist.all_to_all_single(rcnt, cnt)
-            ins, outs = cnt.tolist(), rcnt.tolist()                   # one host sync, like phase 1
-            dist.all_to_all_single(nrecv[:sum(outs)], send[:nk], outs, ins)
-            dist.all_to_all_single(nret, nrecv[:sum(outs)], ins, outs)   # the reverse (FFN excluded)
-            L.unpermute(nret, slot, ys_)
-        t_nccl = graph_time(lambda s_: [lambda: nccl_step(s_)], graph=False)
-        # the in-run NCCL all-to-all peak: 256 MiB per rank, equal splits
-        big = torch.empty(128 << 20, dtype=torch.bfloat16, device=dev)
-        bigo = torch.empty_like(big)
-        t_peak = graph_time(lambda s_: [lambda: dist.all_to_all_single(bigo, big)], graph=False)
-        peak_gbs = big.numel() * 2 * (world - 1) / world / (t_peak / 1e6) / 1e9
-        del big, bigo
-        nccl_base = {"t_dc_us": t_nccl, "tokens_per_s": world * n / (t_nccl / 1e6),
-                     "what": "permute -> torch.distributed.all_to_all_single (NCCL) of every routed token -> "
-                             "the reverse -> unpermute (FFN excluded; splits learned by one count all-to-all + "
-                             "host sync)",
-                     "nccl_alltoall_peak_gbs": peak_gbs,
-                     "nccl_alltoall_peak_how": "all_to_all_single of 256 MiB per rank, off-GPU bytes per direction / time"}
+            def nccl_step(s_):
+                Xs_, zs_, ys_ = sets[s_]
+                L.permute(Xs_, zs_, cfg.E, send, slot, er, ws)          # rows grouped by destination rank
+                cnt = er.view(world, E_local).sum(1).to(torch.int64)
+                dist.all_to_all_single(rcnt, cnt)
+                ins, outs = cnt.tolist(), rcnt.tolist()                   # one host sync, like phase 1
+                dist.all_to_all_single(nrecv[:sum(outs)], send[:nk], outs, ins)
+                dist.all_to_all_single(nret, nrecv[:sum(outs)], ins, outs)   # the reverse (FFN excluded)
+                L.unpermute(nret, slot, ys_)
+            t_nccl = graph_time(lambda s_: [lambda: nccl_step(s_)], graph=False)
+            # the in-run NCCL all-to-all peak: 256 MiB per rank, equal splits
+            big = torch.empty(128 << 20, dtype=torch.bfloat16, device=dev)
+            bigo = torch.empty_like(big)
+            t_peak = graph_time(lambda s_: [lambda: dist.all_to_all_single(bigo, big)], graph=False)
+            peak_gbs = big.numel() * 2 * (world - 1) / world / (t_peak / 1e6) / 1e9
+            del big, bigo
+            nccl_base = {"t_dc_us": t_nccl, "tokens_per_s": world * n / (t_nccl / 1e6),
+                         "what": "permute -> torch.distributed.all_to_all_single (NCCL) of every routed token -> "
+                                 "the reverse -> unpermute (FFN excluded; splits learned by one count all-to-all + "
+                                 "host sync)",
+                         "nccl_alltoall_peak_gbs": peak_gbs,
+                         "nccl_alltoall_peak_how": "all_to_all_single of 256 MiB per rank, off-GPU bytes per direction / time"}
+        except Exception as ex:   # noqa: BLE001  (a context baseline must not cost the measured line)
+            nccl_base = {"error": f"{type(ex).__name__}: {str(ex)[:300]}"}
     pk = peaks()
     nvlink_gbs = 770.0                       # B200_PROFILING.md: measured peer copy per direction
     t_dc_block = {
@@ -662,7 +665,7 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
         "uncompressed_same_exchange_tokens_per_s": world * n / (t_base_dc / 1e6),
         "speedup_vs_same_exchange": t_base_dc / t_dc,
         "uncompressed_nccl_all_to_all_single": nccl_base,
-        "speedup_vs_nccl": (nccl_base["t_dc_us"] / t_dc) if nccl_base else None,
+        "speedup_vs_nccl": (nccl_base["t_dc_us"] / t_dc) if nccl_base and "t_dc_us" in nccl_base else None,
         "exchange_pair_us": t_exch if world > 1 else None,
         "off_gpu_bytes_per_direction": off_rows * row_bytes,
         "uncompressed_off_gpu_bytes_per_direction": base_off_rows * row_bytes,
@@ -706,7 +709,18 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
             kk["bound"] = "latency"
             kk["note"] = "integer index work of < 1 MB: dependent global round trips and barriers, not bytes"
             kernels.append(kk)
-    kernels.append(kern("expert FFN: tc_gemm_kernel<BiasActEpi> x2 (on the m centroid rows)", "tensor", ffn_flops, t_ffn))
+    # the expert FFN on the m centroid rows: both rooflines; the binding one (more time) is its bound.
+    # Bytes: the local experts' W1 / W2 (read once), the received rows, the hidden activation written
+    # by GEMM 1 and read by GEMM 2, and the output rows.
+    ffn_bytes = E_local * 2 * d * cfg.d_ffn * sb + m * row_bytes + 2 * m * cfg.d_ffn * sb + m * row_bytes
+    kf = kern("expert FFN: tc_gemm_kernel<BiasActEpi> x2 (on the m centroid rows)", "tensor", ffn_flops, t_ffn)
+    kh = kern("expert FFN: tc_gemm_kernel<BiasActEpi> x2 (on the m centroid rows)", "hbm", ffn_bytes, t_ffn)
+    if ffn_bytes / (hbm * 1e9) > ffn_flops / (tc_peak * 1e12):
+        kh["tensor_frac"] = kf["frac"]
+        kernels.append(kh)
+    else:
+        kf["hbm_frac"] = kh["frac"]
+        kernels.append(kf)
     kernels.append(kern("restore_kernel", "hbm", rest_bytes, t_rest))
     t_lower = max(hash_flops / (tc_peak * 1e12), hash_bytes / (hbm * 1e9)) * 1e6 + comp_bytes / (hbm * 1e9) * 1e6 \
         + rest_bytes / (hbm * 1e9) * 1e6 + 2 * off_rows * row_bytes / (nvlink_gbs * 1e9) * 1e6

@@ -835,7 +835,10 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
     seg_start = p + 1;
     row = next;
   }
-  cp_async_wait<0>();                         // the ring is free: it may hold the slot-1 partial
+  cp_async_wait<0>();                         // this lane's copies have landed ...
+  __syncwarp();                               // ... and every lane's: the ring may hold the slot-1 partial
+                                              // (a lane's partial overlays bytes other lanes copied;
+                                              // compute-sanitizer racecheck r2)
   if (cb == 0 && X.w == 0) dstamp(P, 2, 5);   // diagnostics: warp 0's rows reduced
   const int nrows = w_end - w_begin;
   const uint32_t r_last = X.row_at(w_end - 1);

@@ -231,8 +231,13 @@ struct FfnSched {
   __device__ WorkItem get(int u, int rank) const {
     int e = 0, mt, nt;
     const int ntn = N / bn;
-    if (order == 0) {
-      while (tiles_pre[e + 1] <= u) ++e;
+    if (order == 0) {         // expert of unit u: the last e with tiles_pre[e] <= u (binary search;
+      int lo = 0, hi = E_local - 1;   // empty experts share their successor's prefix, so "last" skips them)
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tiles_pre[mid] <= u) lo = mid; else hi = mid - 1;
+      }
+      e = lo;
       const int local = u - tiles_pre[e];
       mt = local / ntn;
       nt = local - mt * ntn;
