@@ -33,7 +33,8 @@ def launches(path, tag):
     h, data = rows[hi], rows[hi + 1:]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
     # the last step: from the last hash launch to the end
-    last = max(i for i, r in enumerate(data) if "HashSched" in r[ki] or "hash_f32" in r[ki])
+    last = max(i for i, r in enumerate(data) if "HashSched" in r[ki] or "hash_f32" in r[ki] or "tc_gemm_kernel" in r[ki]
+               and data[i + 1:] and "tile_kernel" in data[i + 1][ki])
     step = data[last:]
     tot = sum(float(r[vi]) for r in step if "lshmoe" in r[ki])
     lines = [f"# {tag}: kernel launches of one bench step (ncu --metrics gpu__time_duration.sum "

@@ -23,7 +23,7 @@ def main():
     tag = sys.argv[1]
     lines = {}
     for nm, f in [("default", f"bench_{tag}.json"), ("reference", f"bench_ref_{tag}.json"),
-                  ("sp", f"bench_{tag}_sp.json"), ("cp8", f"bench_{tag}_cp8.json"),
+                  ("sp", f"bench_{tag}_sp.json"), ("cp8", f"bench_{tag}_cp8.json"), ("hd3", f"bench_{tag}_hd3.json"),
                   ("C3", f"bench_{tag}_C3.json"), ("C4", f"bench_{tag}_C4.json"), ("C5", f"bench_{tag}_C5.json"),
                   ("p2p_n2_share_gpu", f"bench_{tag}_p2p_n2share.json")]:
         d = load(os.path.join(SRC, f))
@@ -32,8 +32,9 @@ def main():
     with open(os.path.join(OUT, f"bench_{tag}_lines.json"), "w") as f:
         json.dump(lines, f, indent=1)
     rows = ["# C5 (Swin-MoE-shaped, 25,088 tokens, d=768, 32 experts top-1) hash-count sweep, one B200",
-            "", "q | compression ratio | centroids | step ms | hash ms | compress ms | FFN ms | uncompressed ms | LSH/uncompressed",
-            "---:|---:|---:|---:|---:|---:|---:|---:|---:"]
+            "", "q | compression ratio | centroids | step ms | hash ms | compress ms | FFN ms | uncompressed ms | LSH/uncompressed"
+            " | T_dc LSH us | T_dc uncompressed us | T_dc speedup",
+            "---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:"]
     for q in range(1, 9):
         d = load(os.path.join(SRC, f"qsweep_{tag}_q{q}.json"))
         if not d:
@@ -42,7 +43,9 @@ def main():
         unc = d.get("uncompressed_baseline") or {}
         rows.append(f"{q} | {d['compression_ratio']:.3f} | {d['centroids']} | {d['ms_per_step']:.3f} | {st['hash']:.3f} | "
                     f"{st['compress']:.3f} | {st['expert_ffn']:.3f} | {unc.get('ms_per_step', float('nan')):.3f} | "
-                    f"{unc.get('speedup_of_lsh', float('nan')):.2f}")
+                    f"{unc.get('speedup_of_lsh', float('nan')):.2f} | {d.get('t_dc', {}).get('lsh_us', float('nan')):.1f} | "
+                    f"{d.get('t_dc', {}).get('uncompressed_same_exchange_us', float('nan')):.1f} | "
+                    f"{d.get('t_dc', {}).get('speedup_vs_same_exchange', float('nan')):.2f}")
     with open(os.path.join(OUT, f"q_sweep_C5_{tag}.md"), "w") as f:
         f.write("\n".join(rows) + "\n")
     reps = sorted(glob.glob(os.path.join(SRC, f"prof_{tag}_*.ncu-rep")))
