@@ -92,6 +92,8 @@ struct HashSched {
   int m_tiles;
   int gate;         // NEXT-2: 1 = one extra unit per token tile for the gate scores (B rows q*d ..)
   int contig;       // 1: contiguous chunk ranges per cluster (see above)
+  int groups = 1;   // contig: MMA groups (CTAs or CTA pairs) per cluster, each on its own token tile of
+                    // the cluster tile, all walking the same (j, slice) chunk sequence (same B loads)
   int G;            // clusters (contig)
   int max_pieces;   // units per cluster (contig)
   __device__ void init(void*) {}
@@ -100,21 +102,21 @@ struct HashSched {
     if (contig) return G * max_pieces;
     return m_tiles * (q * (split ? d / bn : 1) + gate);
   }
-  __device__ WorkItem get_contig(int u, int rank) const {
+  __device__ WorkItem get_contig(int u, int rank, int group) const {
     WorkItem w;
     const int np = d / bn;
-    const int T = m_tiles * q * np;
+    const int T = ((m_tiles + groups - 1) / groups) * q * np;   // chunks of the cluster tiles
     const int g = u % G, k = u / G;
     const int c0 = crange_begin(g, T, G), c1 = crange_begin(g + 1, T, G);
-    const int p = c0 / np + k;                 // (tile, j) pair of this piece
+    const int p = c0 / np + k;                 // (cluster tile, j) pair of this piece
     const int first = max(c0, p * np), last = min(c1, p * np + np);
-    const int mt = p / q, j = p - (p / q) * q;
+    const int mt = (p / q) * groups + group, j = p - (p / q) * q;   // this group's token tile
     w.a_row = mt * bm + rank * BM;
     w.valid_rows = min(BM, n - w.a_row);
     w.nparts = np;
     w.tag1 = j;
     w.tag0 = (mt * (bm / BM) + rank) * q + j;
-    if (first >= last || c0 >= c1) {           // past this cluster's last piece
+    if (first >= last || c0 >= c1 || mt >= m_tiles) {   // past this cluster's last piece / the tokens
       w.nchunks = 0;
       w.part = 0;
       w.b_row0 = 0;
@@ -132,8 +134,8 @@ struct HashSched {
     w.pmask = mask;
     return w;
   }
-  __device__ WorkItem get(int u, int rank) const {
-    if (contig) return get_contig(u, rank);
+  __device__ WorkItem get(int u, int rank, int group) const {
+    if (contig) return get_contig(u, rank, group);
     WorkItem w;
     const int np = split ? d / bn : 1;
     const int upt = q * np + gate;             // units per token tile: slices fastest, then j, then the gate
@@ -228,7 +230,7 @@ struct FfnSched {
   }
   int order;        // 0: units expert-major (e, mt, nt); 1: N-tile-major (nt, e, mt)
   __device__ int units() const { return tiles_pre[E_local]; }
-  __device__ WorkItem get(int u, int rank) const {
+  __device__ WorkItem get(int u, int rank, int /*group*/) const {
     int e = 0, mt, nt;
     const int ntn = N / bn;
     if (order == 0) {         // expert of unit u: the last e with tiles_pre[e] <= u (binary search;
@@ -646,10 +648,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x % 32;
   constexpr int kBKe = 128 / kEB;            // K elements per k-block
   const int kblocks = K / kBKe;
-  const int rank = kCta == 2 ? static_cast<int>(cluster_ctarank()) : 0;
+  // A cluster holds `groups` MMA groups of kCta CTAs (a lone CTA or a cta_group::2 pair, whose
+  // peer differs in rank bit 0); all groups of a cluster walk the same unit sequence.
+  const int crank = static_cast<int>(cluster_ctarank());
+  const int csize = static_cast<int>(cluster_nctarank());
+  const int rank = crank % kCta;              // rank inside the MMA group
+  const int group = crank / kCta;
+  const int gbase = group * kCta;             // cluster rank of the group's leader
   const bool leader = rank == 0;
-  const int cluster = blockIdx.x / kCta;
-  const int nclusters = gridDim.x / kCta;
+  const int cluster = blockIdx.x / csize;
+  const int nclusters = gridDim.x / csize;
+  const uint16_t gmask = static_cast<uint16_t>(((1u << kCta) - 1u) << gbase);   // the group's CTAs
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -683,43 +692,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int units = sched.units();
 
   if (warp == 0) {
-    // ===== TMA producer (every CTA loads its A slice and its half of B) =====
-    if (lane == 0) {
+    // ===== TMA producer (every CTA loads its A slice and its half of B; warp converged, one
+    // elected lane issues) =====
+    {
       int stage = 0;
       uint32_t phase = 0;
       // L2 prefetch cursor running kPrefetchB k-blocks ahead of the loads (B operand only: the
       // FFN's weights stream from HBM once; the tokens are L2-resident)
       int pu = cluster, pc = 0, pkb = 0;
       WorkItem pw{};
-      if (sched.prefetch_b > 0 && pu < units) pw = sched.get(pu, rank);
+      if (sched.prefetch_b > 0 && pu < units) pw = sched.get(pu, rank, group);
       auto prefetch_next = [&]() {
         if (sched.prefetch_b == 0 || pu >= units) return;
-        tma_prefetch_l2_2d(&tmB, pkb * kBKe, pw.b_row0 + pc * BN + rank * C::kBRows);
+        if (lane == 0) tma_prefetch_l2_2d(&tmB, pkb * kBKe, pw.b_row0 + pc * BN + rank * C::kBRows);
         if (++pkb == kblocks) {
           pkb = 0;
           if (++pc == pw.nchunks) {
             pc = 0;
             pu += nclusters;
-            if (pu < units) pw = sched.get(pu, rank);
+            if (pu < units) pw = sched.get(pu, rank, group);
           }
         }
       };
       for (int i = 0; i < sched.prefetch_b; ++i) prefetch_next();
       for (int u = cluster; u < units; u += nclusters) {
-        const WorkItem w = sched.get(u, rank);
+        const WorkItem w = sched.get(u, rank, group);
         for (int c = 0; c < w.nchunks; ++c) {
           const int brow = w.b_row0 + c * BN + rank * C::kBRows;
           for (int kb = 0; kb < kblocks; ++kb) {
             prefetch_next();
             mbar_wait(&empty[stage], phase ^ 1);
             if (kCta == 2) {
-              if (leader) mbar_arrive_expect_tx(&full[stage], C::kTxBytes);
-              tma_load_2d_2sm(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBKe, w.a_row);
-              tma_load_2d_2sm(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBKe, brow);
+              if (leader) mbar_arrive_expect_tx_w(&full[stage], C::kTxBytes);
+              tma_load_2d_2sm_w(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBKe, w.a_row);
+              tma_load_2d_2sm_w(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBKe, brow);
             } else {
-              mbar_arrive_expect_tx(&full[stage], C::kTxBytes);
-              tma_load_2d(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBKe, w.a_row);
-              tma_load_2d(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBKe, brow);
+              mbar_arrive_expect_tx_w(&full[stage], C::kTxBytes);
+              tma_load_2d_w(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBKe, w.a_row);
+              tma_load_2d_w(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBKe, brow);
             }
             if (++stage == C::kStages) {
               stage = 0;
@@ -731,15 +741,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ===== MMA issuer (one thread of the leader CTA) =====
-    if (leader && lane == 0) {
+    // ===== MMA issuer (the leader CTA's warp 1, converged; one elected lane issues) =====
+    if (leader) {
       constexpr uint32_t idesc = kEB == 1 ? idesc_e4m3_f32(BM * kCta, BN) : idesc_bf16_f32(BM * kCta, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = cluster; u < units; u += nclusters) {
-        const WorkItem w = sched.get(u, rank);
+        const WorkItem w = sched.get(u, rank, group);
         for (int c = 0; c < w.nchunks; ++c) {
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
@@ -747,30 +757,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + stage * C::kABytes);
-            const uint32_t b0 = smem_u32(sB + stage * C::kBBytes);
+            // descriptors of the stage's k-block; +32 B of K = +2 in the 16-byte start-address field
+            const uint64_t ad = smem_desc_sw128(smem_u32(sA + stage * C::kABytes));
+            const uint64_t bd = smem_desc_sw128(smem_u32(sB + stage * C::kBBytes));
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               if (epi_skip_mma(epi)) break;
-              if (kEB == 1)             // 32 e4m3 = 32 bytes of K per instruction
-                mma_fp8_ss(d_tmem, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), idesc,
-                           (kb | kk) != 0);
+              if (kEB == 1 && kCta == 2)   // 32 e4m3 = 32 bytes of K per instruction
+                mma_fp8_ss_2cta_w(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+              else if (kEB == 1)
+                mma_fp8_ss_w(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
               else if (kCta == 2)
-                mma_bf16_ss_2cta(d_tmem, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), idesc,
-                                 (kb | kk) != 0);
+                mma_bf16_ss_2cta_w(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
               else
-                mma_bf16_ss(d_tmem, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), idesc,
-                            (kb | kk) != 0);
+                mma_bf16_ss_w(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
             }
-            if (kCta == 2) mma_commit_2cta_mc(&empty[stage], 0x3);   // frees the slot in both CTAs
-            else mma_commit(&empty[stage]);
+            if (kCta == 2) mma_commit_2cta_mc_w(&empty[stage], gmask);   // frees the slot in both CTAs
+            else mma_commit_w(&empty[stage]);
             if (++stage == C::kStages) {
               stage = 0;
               phase ^= 1;
             }
           }
-          if (kCta == 2) mma_commit_2cta_mc(&tfull[acc], 0x3);      // both epilogues may read
-          else mma_commit(&tfull[acc]);
+          if (kCta == 2) mma_commit_2cta_mc_w(&tfull[acc], gmask);      // both epilogues may read
+          else mma_commit_w(&tfull[acc]);
           acc ^= 1;
           if (acc == 0) acc_phase ^= 1;
         }
@@ -784,11 +794,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kBlkPer = (BN / 32) * 4 / kEpiWarps;
     const int row = quad * 32 + lane;
     uint8_t* scratch = epi_scratch + (warp - 2) * EpiScratch<Epi>::value;
-    const uint32_t tempty_leader0 = kCta == 2 ? mapa_shared(&tempty[0], 0) : 0;
+    const uint32_t tempty_leader0 = kCta == 2 ? mapa_shared(&tempty[0], gbase) : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = cluster; u < units; u += nclusters) {
-      const WorkItem w = sched.get(u, rank);
+      const WorkItem w = sched.get(u, rank, group);
       epi.begin(w, scratch);
       for (int c = 0; c < w.nchunks; ++c) {
         mbar_wait(&tfull[acc], acc_phase);
@@ -858,15 +868,48 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int b
 }
 
 template <int BN, int kCta, class Sched, class Epi, int kEB = 2>
-int launch_tc(const CUtensorMap& a, const CUtensorMap& b, int K, const Sched& s, const Epi& e, int grid,
-              cudaStream_t st) {
+int configure_tc() {
   auto kern = tc_gemm_kernel<BN, kCta, Sched, Epi, kEB>;
-  static bool configured = false;     // one attribute call per instantiation
-  if (!configured) {
-    int err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, kCta, EpiScratch<Epi>::value>::kSmem);
-    if (err) return err;
-    configured = true;
+  static int configured = -1;     // one attribute call per instantiation
+  if (configured < 0) {
+    configured = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg<BN, kCta, EpiScratch<Epi>::value>::kSmem);
+    if (!configured)   // clusters of up to 16 CTAs (8 are portable)
+      configured = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
+  return configured;
+}
+
+// Clusters of csize CTAs of this instantiation that can be resident at once (0 on error): the
+// persistent grid must not exceed it (GPCs whose SM count is not a multiple of csize leave SMs idle).
+template <int BN, int kCta, class Sched, class Epi, int kEB = 2>
+int active_clusters(int csize) {
+  if (configure_tc<BN, kCta, Sched, Epi, kEB>()) return 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(csize * 512);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg<BN, kCta, EpiScratch<Epi>::value>::kSmem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<BN, kCta, Sched, Epi, kEB>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// groups: MMA groups per cluster (cluster = kCta * groups CTAs); grid is a multiple of the cluster.
+template <int BN, int kCta, class Sched, class Epi, int kEB = 2>
+int launch_tc(const CUtensorMap& a, const CUtensorMap& b, int K, const Sched& s, const Epi& e, int grid,
+              cudaStream_t st, int groups = 1) {
+  auto kern = tc_gemm_kernel<BN, kCta, Sched, Epi, kEB>;
+  if (int err = configure_tc<BN, kCta, Sched, Epi, kEB>()) return err;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -874,7 +917,7 @@ int launch_tc(const CUtensorMap& a, const CUtensorMap& b, int K, const Sched& s,
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCta;
+  attr[0].val.clusterDim.x = kCta * groups;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see the kernel's wait)
@@ -898,7 +941,7 @@ int env_bn(const char* name, int N, int dflt) {   // experiment override: 64 / 1
 // kCta = 2 needs BN / 2 rows per CTA to stay a multiple of 8 (SW128 atoms) and N >= 16 per CTA.
 template <class Sched, class Epi>
 int launch_bn(int bn, int cta, const void* A, int64_t a_rows, const void* B, int64_t b_rows, int K, Sched s, Epi e,
-              int units_hint, cudaStream_t st) {
+              int units_hint, cudaStream_t st, int groups = 1) {
   CUtensorMap ma, mb;
   int err = make_map(&ma, A, a_rows, K, BM);
   if (err) return err;
@@ -907,20 +950,38 @@ int launch_bn(int bn, int cta, const void* A, int64_t a_rows, const void* B, int
   s.bn = bn;
   s.bm = BM * cta;
   const int sms = device_sm_count();
-  int clusters = sms / cta;
+  int clusters = sms / (cta * groups);
   if (units_hint > 0 && units_hint < clusters) clusters = units_hint;
-  const int grid = clusters * cta;
+  const int grid = clusters * cta * groups;
   if (cta == 2) {
     switch (bn) {
-      case 256: return launch_tc<256, 2>(ma, mb, K, s, e, grid, st);
-      case 128: return launch_tc<128, 2>(ma, mb, K, s, e, grid, st);
-      default: return launch_tc<64, 2>(ma, mb, K, s, e, grid, st);
+      case 256: return launch_tc<256, 2>(ma, mb, K, s, e, grid, st, groups);
+      case 128: return launch_tc<128, 2>(ma, mb, K, s, e, grid, st, groups);
+      default: return launch_tc<64, 2>(ma, mb, K, s, e, grid, st, groups);
     }
   }
   switch (bn) {
-    case 256: return launch_tc<256, 1>(ma, mb, K, s, e, grid, st);
-    case 128: return launch_tc<128, 1>(ma, mb, K, s, e, grid, st);
-    default: return launch_tc<64, 1>(ma, mb, K, s, e, grid, st);
+    case 256: return launch_tc<256, 1>(ma, mb, K, s, e, grid, st, groups);
+    case 128: return launch_tc<128, 1>(ma, mb, K, s, e, grid, st, groups);
+    default: return launch_tc<64, 1>(ma, mb, K, s, e, grid, st, groups);
+  }
+}
+
+// Resident clusters of the hash kernel for (bn, cta, groups) (the persistent grid's size).
+template <class Epi>
+int hash_active_clusters(int bn, int cta, int groups) {
+  const int cs = cta * groups;
+  if (cta == 2) {
+    switch (bn) {
+      case 256: return active_clusters<256, 2, HashSched, Epi>(cs);
+      case 128: return active_clusters<128, 2, HashSched, Epi>(cs);
+      default: return active_clusters<64, 2, HashSched, Epi>(cs);
+    }
+  }
+  switch (bn) {
+    case 256: return active_clusters<256, 1, HashSched, Epi>(cs);
+    case 128: return active_clusters<128, 1, HashSched, Epi>(cs);
+    default: return active_clusters<64, 1, HashSched, Epi>(cs);
   }
 }
 
@@ -974,12 +1035,13 @@ size_t hash_workspace_bytes(int64_t n, int d, int q) {
 
 // Contiguous chunk ranges per cluster (HashSched::contig) unless LSHMOE_HASH_CONTIG=0; returns the
 // cluster count G the launch must use.
-int set_contig(HashSched& s, int cta, int np) {
-  const int T = s.m_tiles * s.q * np;
-  int G = device_sm_count() / cta;
+int set_contig(HashSched& s, int cta, int np, int groups = 1, int max_clusters = 0) {
+  const int T = ((s.m_tiles + groups - 1) / groups) * s.q * np;
+  int G = max_clusters > 0 ? max_clusters : device_sm_count() / (cta * groups);
   if (T < G) G = T;
+  s.groups = groups;
   const char* env = getenv("LSHMOE_HASH_CONTIG");
-  if (env && env[0] == '0') return T;   // round-robin split units (A/B)
+  if (groups == 1 && env && env[0] == '0') return T;   // round-robin split units (A/B)
   s.contig = 1;
   s.G = G;
   const int per = (T + G - 1) / G;
@@ -988,7 +1050,9 @@ int set_contig(HashSched& s, int cta, int np) {
 }
 
 int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int16_t* codes, void* ws, void* stream) {
-  const int cta = cta_mode("LSHMOE_HASH_CTA", 1);
+  // CTA pairs (M = 256, each CTA stages half of B): C2 75.7 vs 82.4 us, C4 499 vs 552 us per launch
+  // (scripts/hash_groups_ab.py, graph-timed over cycled token copies)
+  const int cta = cta_mode("LSHMOE_HASH_CTA", 2);
   HashSched s{};
   s.n = static_cast<int>(n);
   s.q = q;
@@ -1009,9 +1073,19 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
     e.counter = static_cast<int*>(ws);
     e.partial = reinterpret_cast<uint2*>(static_cast<uint8_t*>(ws) + counters);
   }
+  s.groups = 1;
   int hint = s.m_tiles * q * (s.split ? d / bn : 1);
-  if (s.split) hint = set_contig(s, cta, d / bn);
-  return launch_bn(bn, cta, x, n, R, static_cast<int64_t>(q) * d, d, s, e, hint, static_cast<cudaStream_t>(stream));
+  int groups = 1;
+  if (s.split) {
+    // groups > 1: clusters of `groups` MMA groups on adjacent token tiles issue the same B loads
+    // at the same time (experiment LSHMOE_HASH_GROUPS)
+    if (const char* g = getenv("LSHMOE_HASH_GROUPS")) groups = std::max(1, std::min(8 / cta, atoi(g)));
+    const int mc = groups > 1 ? hash_active_clusters<ArgmaxEpi>(bn, cta, groups) : 0;
+    if (groups > 1 && mc <= 0) groups = 1;
+    hint = set_contig(s, cta, d / bn, groups, mc);
+  }
+  return launch_bn(bn, cta, x, n, R, static_cast<int64_t>(q) * d, d, s, e, hint, static_cast<cudaStream_t>(stream),
+                   groups);
 }
 
 // NEXT-2 gate + hash in one pass over x (reading R29): B = [R ; W_g] ([q*d + E, d]); per token
@@ -1050,13 +1124,15 @@ int launch_gate_hash_bf16(const void* x, int64_t n, int d, const void* RG, int q
 // k-blocks (half as many as bf16), the argmax epilogue unchanged.
 int launch_hash_e4m3(const void* x8, int64_t n, int d, const void* R8, int q, int16_t* codes, void* ws, void* stream) {
   const int bn = pick_bn(d);
+  const int cta = cta_mode("LSHMOE_HASH_CTA", 2);   // CTA pairs as the bf16 hash
   HashSched s{};
   s.n = static_cast<int>(n);
   s.q = q;
   s.d = d;
   s.bn = bn;
-  s.bm = BM;
-  s.m_tiles = static_cast<int>((n + BM - 1) / BM);
+  s.bm = BM * cta;
+  s.groups = 1;
+  s.m_tiles = static_cast<int>((n + BM * cta - 1) / (BM * cta));
   ArgmaxEpi e{};
   e.codes = codes;
   e.q = q;
@@ -1071,11 +1147,18 @@ int launch_hash_e4m3(const void* x8, int64_t n, int d, const void* R8, int q, in
   CUtensorMap ma, mb;
   int err = make_map(&ma, x8, n, d, BM, 1);
   if (err) return err;
-  err = make_map(&mb, R8, static_cast<int64_t>(q) * d, d, bn, 1);
+  err = make_map(&mb, R8, static_cast<int64_t>(q) * d, d, bn / cta, 1);
   if (err) return err;
-  const int units = s.split ? set_contig(s, 1, d / bn) : s.m_tiles * q;
-  const int grid = std::min(device_sm_count(), units);
+  const int units = s.split ? set_contig(s, cta, d / bn) : s.m_tiles * q;
+  const int grid = std::min(device_sm_count() / cta, units) * cta;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cta == 2) {
+    switch (bn) {
+      case 256: return launch_tc<256, 2, HashSched, ArgmaxEpi, 1>(ma, mb, d, s, e, grid, st);
+      case 128: return launch_tc<128, 2, HashSched, ArgmaxEpi, 1>(ma, mb, d, s, e, grid, st);
+      default: return launch_tc<64, 2, HashSched, ArgmaxEpi, 1>(ma, mb, d, s, e, grid, st);
+    }
+  }
   switch (bn) {
     case 256: return launch_tc<256, 1, HashSched, ArgmaxEpi, 1>(ma, mb, d, s, e, grid, st);
     case 128: return launch_tc<128, 1, HashSched, ArgmaxEpi, 1>(ma, mb, d, s, e, grid, st);
