@@ -345,6 +345,8 @@ def compress_phase_times(workspace: torch.Tensor) -> dict:
         return {}
     out, prev_end = {}, None
     for kern, st in D.items():
+        if np.all(np.isnan(st["start"])) or np.all(np.isnan(st["end"])):
+            continue                      # kernel not on this path (the group path has no K1)
         s, e = np.nanmin(st["start"]), np.nanmax(st["end"])
         if prev_end is not None:
             out[f"gap_before_{kern}"] = round(float(s - prev_end), 2)

@@ -1,9 +1,10 @@
 // a3-a5: group the routed copies by expert, bucket them by their composite LSH key, and reduce
 // each bucket to its centroid (Alg. 1 L3, L5-L8: P:L520; §2.3).
 //
-// Three kernels chained by programmatic dependent launch (PDL: each kernel's launch and prologue
-// overlap its predecessor's tail; cudaGridDependencySynchronize orders the data), one memset, no
-// host synchronisation:
+// Two or three kernels chained by programmatic dependent launch (PDL: each kernel's launch and
+// prologue overlap its predecessor's tail; griddepcontrol.wait orders the data), no host
+// synchronisation.  Group path (n*k <= 16K copies, see group_path): K12 group_kernel (one CTA per
+// expert, everything in shared memory; described at its definition) -> K3.  Tiles path:
 //   K1 tile_kernel   (one CTA per 256-copy tile): insert every copy into an open-addressing hash
 //                    table keyed by (expert, q-tuple of codes) whose slot value converges
 //                    (atomicMin) to the smallest copy id with that key = the bucket's first
@@ -121,6 +122,7 @@ struct Params {
   int grad;                        // 1: NEXT-1 grad_compress: weighted per-row SUMS (no 1/count)
   const float* gw;                 // grad: gate weights [nk] or nullptr (weight 1)
   int diag;                        // 1: record per-CTA globaltimer stamps (diagnostics)
+  int table_clean;                 // 1: the global hash table was not used (group path): K3 skips its reset
   // phase-2 dispatch fused into K3 (lshmoe_compress_p2p); p2p_peers == nullptr: off
   uint8_t* const* p2p_peers;
   int64_t p2p_mailbox, p2p_recv, p2p_data_flag, p2p_recv_cap;
@@ -586,6 +588,374 @@ __global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
   if (tid == 0 && r == 0) P.expert_rows[e] = m_e;
   dstamp(P, 1, 5);                         // (the exchanges go through global memory: no exit barrier)
 }
+
+// ---- K12: the group path — one CTA per expert does K1 + K2 in shared memory -------------------
+// CTA e scans the gate map, compacts its expert's copies in ascending copy id (ordered ballots),
+// stores each member's composite key (its token's q codes) and inserts the members into a
+// shared-memory hash table keyed by the codes alone (the table is private to the expert): the slot
+// keeps the smallest member index with that key (= the bucket's first appearance, reading R7) and
+// the bucket's size.  Local row ids = ordered prefix count of the first appearances; each member
+// reads its row from its slot; row starts = exclusive scan of the sizes in row order; within-row
+// ranks by W warps over contiguous member sub-ranges (match_any batches, per-(warp, row) counters,
+// prefix over warps), so perm lists each row's members in ascending copy id (reading R8).  No
+// global hash table, no cross-CTA round trip, no cluster barrier: the dependent global accesses
+// are the gate-map reads, the code gathers and the output stores.  A group whose arrays do not fit
+// in shared memory runs the same code on per-group regions of the workspace (global mode).
+constexpr int kGThreads = 1024;
+constexpr int kGWarps = kGThreads / 32;
+constexpr int kGRound = 16;              // gate-map entries per thread per compaction round
+constexpr int kGroupSmem = 222 * 1024;   // dynamic shared memory of group_kernel (+ 2.2 KB static)
+
+template <bool kS>
+__device__ __forceinline__ int gld(const int32_t* p) {   // global mode: L2 (atomics live there)
+  if constexpr (kS) return *p;
+  else return __ldcg(p);
+}
+template <bool kS>
+__device__ __forceinline__ uint32_t gldu(const uint32_t* p) {
+  if constexpr (kS) return *p;
+  else return __ldcg(p);
+}
+
+// Sum over the CTA (all threads receive it).  s = [kGWarps + 1].
+__device__ __forceinline__ int group_sum(int v, int* s) {
+  int t;
+  block_excl_scan<kGWarps>(v, s, &t);
+  return t;
+}
+
+// mem: the expert's members (copy ids, ascending), n_e of them, in shared memory at g_dsmem[0]
+// (smem mode) or in the workspace (global mode).  Shared-memory layout (smem mode):
+// [mem n_e][slot n_e][aux n_e][rs n_e][fa T][free] — 16 B per member + 4 B per table slot; the
+// keys live in the workspace (read only by a warp's leader, against a claimed slot's owner), and the
+// per-(warp, row) rank counters reuse the table region once the rows are assigned.
+template <bool kS>
+__device__ void group_body(const Params& P, int e, int n_e, int goff, int T, int KW, int32_t* mem, int* s_scan,
+                           bool smem_keys) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int nk = P.nk;
+  int32_t *slot, *aux, *fa, *rs, *wc;
+  int64_t wc_cap;                           // ints available for the per-(warp, row) counters
+  int32_t* b = P.big;
+  const int64_t N = nk;
+  uint32_t* key = reinterpret_cast<uint32_t*>(b + 5 * N) + static_cast<int64_t>(goff) * KW;
+  if constexpr (kS) {
+    int32_t* sm = reinterpret_cast<int32_t*>(g_dsmem);
+    slot = sm + n_e;
+    aux = slot + n_e;
+    rs = aux + n_e;
+    fa = rs + n_e;
+    if (smem_keys) key = reinterpret_cast<uint32_t*>(fa + T);   // [key n_e x KW] after the table
+    wc = fa;                                // after the rows are assigned (table and keys are free)
+    wc_cap = P.dyn_smem / 4 - (wc - sm);
+  } else {                                  // per-group regions of the workspace's big arrays
+    slot = b + N + goff;
+    aux = b + 2 * N + goff;
+    rs = b + 3 * N + goff;
+    fa = b + 13 * N + 4 * static_cast<int64_t>(goff);   // T <= 4 n_e in global mode
+    wc = b + 21 * N + 16 * static_cast<int64_t>(goff);  // 16 warps x m_e <= 16 n_e
+    wc_cap = 16ll * n_e;
+  }
+  if (P.permute) {                          // baseline: slot = group offset + rank in the group
+    for (int j = tid; j < n_e; j += kGThreads) {
+      const int c = gld<kS>(mem + j);
+      P.bucket[c] = goff + j;
+      P.rowl[goff + j] = c;
+    }
+    if (tid == 0) {
+      P.expert_rows[e] = n_e;
+      P.gofs[e] = goff;
+    }
+    return;
+  }
+  for (int i = tid; i < T; i += kGThreads) fa[i] = -1;
+  // keys: the member's token's q codes packed two per word (workspace); the hash goes to aux.
+  // kGB members per thread per batch, all their code loads issued before any is used.
+  const int q = P.q, k = P.k;
+  const bool even = (q & 1) == 0;           // rows of q int16 are 4-byte aligned: word loads
+  constexpr int kGB = 2;
+  for (int j0 = tid; j0 < n_e; j0 += kGB * kGThreads) {
+    uint32_t wv[kGB][kMaxQ / 2];
+#pragma unroll
+    for (int m = 0; m < kGB; ++m) {
+      const int j = j0 + m * kGThreads;
+      if (j < n_e) {
+        const int c = gld<kS>(mem + j);
+        const int64_t t = c / k;
+        if (even) {
+          const uint32_t* kc = reinterpret_cast<const uint32_t*>(P.codes + t * q);
+#pragma unroll
+          for (int w = 0; w < kMaxQ / 2; ++w)
+            if (w < KW) wv[m][w] = __ldg(kc + w);
+        } else {
+          const uint16_t* kc = reinterpret_cast<const uint16_t*>(P.codes + t * q);
+#pragma unroll
+          for (int w = 0; w < kMaxQ / 2; ++w)
+            if (w < KW) wv[m][w] = static_cast<uint32_t>(__ldg(kc + 2 * w)) |
+                                   (2 * w + 1 < q ? static_cast<uint32_t>(__ldg(kc + 2 * w + 1)) << 16 : 0u);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kGB; ++m) {
+      const int j = j0 + m * kGThreads;
+      if (j < n_e) {
+        uint32_t h = 0x9E3779B9u;
+#pragma unroll
+        for (int w = 0; w < kMaxQ / 2; ++w)
+          if (w < KW) {
+            key[static_cast<int64_t>(j) * KW + w] = wv[m][w];
+            h = fmix32(h ^ (wv[m][w] + 0x632BE5ABu * static_cast<uint32_t>(w + 1)));
+          }
+        aux[j] = static_cast<int32_t>(h);
+      }
+    }
+  }
+  __syncthreads();                          // every key is stored before any slot is claimed
+  dstamp(P, 1, 1);
+  // insert: a slot's value converges (atomicMin) to the smallest member index with its key (a
+  // claimed slot never changes key); a plain read first keeps claimed slots free of CAS traffic
+  for (int j = tid; j < n_e; j += kGThreads) {
+    uint32_t kw[kMaxQ / 2];
+#pragma unroll
+    for (int w = 0; w < kMaxQ / 2; ++w)
+      if (w < KW) kw[w] = key[static_cast<int64_t>(j) * KW + w];
+    int sl = static_cast<int>(static_cast<uint32_t>(gld<kS>(aux + j)) & static_cast<uint32_t>(T - 1));
+    while (true) {
+      int cur = gld<kS>(fa + sl);
+      if (cur < 0) {
+        cur = atomicCAS(fa + sl, -1, j);
+        if (cur < 0) break;
+      }
+      bool eq = true;
+#pragma unroll
+      for (int w = 0; w < kMaxQ / 2; ++w)
+        if (w < KW) eq &= key[static_cast<int64_t>(cur) * KW + w] == kw[w];
+      if (eq) {
+        if (j < cur) atomicMin(fa + sl, j);
+        break;
+      }
+      sl = (sl + 1) & (T - 1);
+    }
+    slot[j] = sl;
+  }
+  __syncthreads();
+  dstamp(P, 1, 2);
+  for (int j0 = tid; j0 < n_e; j0 += 4 * kGThreads) {   // first?  (4 members' loads in flight)
+    int sv[4], fv[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) sv[m] = j0 + m * kGThreads < n_e ? gld<kS>(slot + j0 + m * kGThreads) : 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) fv[m] = j0 + m * kGThreads < n_e ? gld<kS>(fa + sv[m]) : 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (j0 + m * kGThreads < n_e) aux[j0 + m * kGThreads] = fv[m] == j0 + m * kGThreads ? 1 : 0;
+  }
+  __syncthreads();
+  // local row ids of the first appearances in member order (contiguous chunks per thread); the
+  // slot's fa becomes the row id (every first-flag read is done)
+  int m_e;
+  {
+    const int L = (n_e + kGThreads - 1) / kGThreads;
+    const int j0 = min(n_e, tid * L), j1 = min(n_e, j0 + L);
+    int nf = 0;
+    for (int j = j0; j < j1; ++j) nf += gld<kS>(aux + j);
+    int id = block_excl_scan<kGWarps>(nf, s_scan, &m_e);
+    for (int j = j0; j < j1; ++j)
+      if (gld<kS>(aux + j)) fa[gld<kS>(slot + j)] = id++;
+  }
+  __syncthreads();
+  for (int j0 = tid; j0 < n_e; j0 += 4 * kGThreads) {   // slot -> row
+    int sv[4], fv[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) sv[m] = j0 + m * kGThreads < n_e ? gld<kS>(slot + j0 + m * kGThreads) : 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) fv[m] = j0 + m * kGThreads < n_e ? gld<kS>(fa + sv[m]) : 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (j0 + m * kGThreads < n_e) slot[j0 + m * kGThreads] = fv[m];
+  }
+  __syncthreads();                          // the table is free: the rank counters take its place
+  dstamp(P, 1, 3);
+  // within-row ranks: W warps own contiguous member sub-ranges, per-(warp, row) counters
+  int W = static_cast<int>(min(static_cast<int64_t>(kGWarps), wc_cap / max(m_e, 1)));
+  if (W < 1) W = 1;
+  const int sub = (((n_e + W - 1) / W) + 31) & ~31;
+  for (int i = tid; i < W * m_e; i += kGThreads) wc[i] = 0;
+  __syncthreads();
+  if (warp < W) {
+    int32_t* w_c = wc + static_cast<int64_t>(warp) * m_e;
+    const int b0 = min(n_e, warp * sub), b1 = min(n_e, b0 + sub);
+    for (int bb = b0; bb < b1; bb += 32) {
+      const int i = bb + lane;
+      const bool ok = i < b1;
+      const int rr = ok ? gld<kS>(slot + i) : -1;
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, rr);
+      const int leader = __ffs(peers) - 1;
+      const int cv = ok ? gld<kS>(w_c + rr) : 0;
+      __syncwarp();
+      if (ok && lane == leader) w_c[rr] = cv + __popc(peers);
+      __syncwarp();
+      if (ok) aux[i] = cv + __popc(peers & lt);
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < m_e; r += kGThreads) {   // prefix over warps per row; the total = row size
+    int run = 0;
+    for (int w = 0; w < W; ++w) {
+      const int v = gld<kS>(wc + static_cast<int64_t>(w) * m_e + r);
+      wc[static_cast<int64_t>(w) * m_e + r] = run;
+      run += v;
+    }
+    rs[r] = run;
+  }
+  __syncthreads();
+  {                                         // row starts: ordered exclusive scan of the sizes
+    const int L = (m_e + kGThreads - 1) / kGThreads;
+    const int r0 = min(m_e, tid * L), r1 = min(m_e, r0 + L);
+    int sz = 0;
+    for (int r = r0; r < r1; ++r) sz += gld<kS>(rs + r);
+    int tot;
+    int run = block_excl_scan<kGWarps>(sz, s_scan, &tot);
+    for (int r = r0; r < r1; ++r) {
+      const int v = gld<kS>(rs + r);
+      rs[r] = run;
+      P.rsl[goff + r] = goff + run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  dstamp(P, 1, 4);
+  for (int j0 = tid; j0 < n_e; j0 += 4 * kGThreads) {   // 4 members' loads in flight
+    int rv[4], pv[4], cv[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int j = j0 + m * kGThreads;
+      rv[m] = j < n_e ? gld<kS>(slot + j) : 0;
+      cv[m] = j < n_e ? gld<kS>(mem + j) : 0;
+      pv[m] = j < n_e ? gld<kS>(aux + j) : 0;
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int j = j0 + m * kGThreads;
+      if (j < n_e) pv[m] += gld<kS>(rs + rv[m]) + gld<kS>(wc + static_cast<int64_t>(j / sub) * m_e + rv[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (j0 + m * kGThreads < n_e) {
+        P.perm[goff + pv[m]] = cv[m];
+        P.rowl[goff + pv[m]] = rv[m];
+      }
+  }
+  if (tid == 0) {
+    P.expert_rows[e] = m_e;
+    P.gofs[e] = goff;
+  }
+}
+
+// Ordered compaction of expert e's copies (ascending copy id) into mem[0, cap): rounds of
+// kGRound x 1024 gate-map entries, entry c = r0 + u * 1024 + tid, so (u, warp, lane) is ascending
+// copy order within a round; the next round's entries are loaded before this round's scan.
+// Returns n_e; *clt = copies of experts < e (invalid ids count as expert 0).  Ids outside [0, E)
+// in [c0, c1) raise error bit 0.
+__device__ int group_compact(const Params& P, int e, int32_t* mem, int cap, int c0, int c1, int* s_scan, int* s_cnt,
+                             int* clt_out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int nk = P.nk, E = P.E;
+  int base = 0, clt = 0;
+  int v[kGRound];
+#pragma unroll
+  for (int u = 0; u < kGRound; ++u) v[u] = u * kGThreads + tid < nk ? P.experts[u * kGThreads + tid] : 0x7FFFFFFF;
+  for (int r0 = 0; r0 < nk; r0 += kGRound * kGThreads) {
+    unsigned bl[kGRound];
+#pragma unroll
+    for (int u = 0; u < kGRound; ++u) {
+      const int c = r0 + u * kGThreads + tid;
+      int x = v[u];
+      if (c < nk && static_cast<unsigned>(x) >= static_cast<unsigned>(E)) {
+        if (c >= c0 && c < c1) atomicOr(&g_device_error, 1);
+        x = 0;
+      }
+      clt += x < e;
+      bl[u] = __ballot_sync(0xFFFFFFFFu, x == e);
+      if (lane == 0) s_cnt[u * kGWarps + warp] = __popc(bl[u]);
+    }
+    if (r0 + kGRound * kGThreads < nk)      // the next round's entries, in flight during the scan
+#pragma unroll
+      for (int u = 0; u < kGRound; ++u) {
+        const int c = r0 + kGRound * kGThreads + u * kGThreads + tid;
+        v[u] = c < nk ? P.experts[c] : 0x7FFFFFFF;
+      }
+    __syncthreads();
+    constexpr int kEnt = kGRound * kGWarps;   // 512 (u, warp) counts, scanned in (u, warp) order
+    const int x = tid < kEnt ? s_cnt[tid] : 0;
+    int tot;
+    const int ex = block_excl_scan<kGWarps>(x, s_scan, &tot);
+    if (tid < kEnt) s_cnt[tid] = ex;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kGRound; ++u)
+      if ((bl[u] >> lane) & 1u) {
+        const int pos = base + s_cnt[u * kGWarps + warp] + __popc(bl[u] & lt);
+        if (pos < cap) mem[pos] = r0 + u * kGThreads + tid;
+      }
+    base += tot;
+    __syncthreads();                        // s_cnt is rewritten by the next round
+  }
+  *clt_out = clt;
+  return base;
+}
+
+__global__ void __launch_bounds__(kGThreads, 1) group_kernel(Params P) {
+  __shared__ int s_scan[kGWarps + 1];
+  __shared__ int s_cnt[kGRound * kGWarps];
+  const int tid = threadIdx.x;
+  const int e = blockIdx.x, E = P.E, nk = P.nk;
+  pdl_wait();                               // the hash kernel's codes (and the gate map) are visible
+  pdl_trigger();
+  dstamp(P, 1, 0);
+  // this CTA validates the copies [c0, c1): ids in [0, E) (bit 0, in the compaction pass) and,
+  // for k > 1, distinct within a token (bit 1)
+  const int c0 = static_cast<int>(static_cast<int64_t>(e) * nk / E);
+  const int c1 = static_cast<int>(static_cast<int64_t>(e + 1) * nk / E);
+  if (P.k > 1)
+    for (int c = c0 + tid; c < c1; c += kGThreads) {
+      const int v = P.experts[c], sl = c % P.k;
+      for (int s2 = 0; s2 < sl; ++s2)
+        if (P.experts[c - sl + s2] == v) atomicOr(&g_device_error, 2);
+    }
+  // one pass over the gate map: the members into shared memory (as many as fit), n_e, goff
+  int32_t* sm = reinterpret_cast<int32_t*>(g_dsmem);
+  const int cap = P.dyn_smem / 4;
+  int clt;
+  const int n_e = group_compact(P, e, sm, cap, c0, c1, s_scan, s_cnt, &clt);
+  const int goff = group_sum(clt, s_scan);
+  dstamp(P, 1, 7);
+  const int KW = (P.q + 1) / 2;
+  int T = 64;
+  while (T < n_e + n_e / 2) T <<= 1;        // load factor <= 2/3
+  const int64_t need = P.permute ? 4ll * n_e : 16ll * n_e + 4ll * T;
+  if (need <= P.dyn_smem) {                 // the keys too when they fit (else in the workspace)
+    const bool sk = !P.permute && need + 4ll * KW * n_e <= P.dyn_smem;
+    group_body<true>(P, e, n_e, goff, T, KW, sm, s_scan, sk);
+  } else {                                  // global mode: the members move to the workspace
+    while (T < 2 * n_e) T <<= 1;
+    int32_t* gm = P.big + goff;
+    if (n_e <= cap) {
+      for (int j = tid; j < n_e; j += kGThreads) gm[j] = sm[j];
+    } else {
+      int dummy;
+      group_compact(P, e, gm, n_e, 0, 0, s_scan, s_cnt, &dummy);
+    }
+    __syncthreads();
+    group_body<false>(P, e, n_e, goff, T, KW, gm, s_scan, false);
+  }
+  dstamp(P, 1, 5);
+}
+
+
 
 // ---- centroid phase ------------------------------------------------------------------------
 // CTA b owns the perm range [b*nk/G, (b+1)*nk/G), split again into one contiguous sub-range per
@@ -1219,7 +1589,7 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   dstamp(P, 2, 0);
   IndexPre pre;
   if (!P.permute) preload_index(P, pre);      // in flight during the expert-count scan below
-  if (!P.permute)                             // K2 was the table's last reader: leave it at rest (-1)
+  if (!P.permute && !P.table_clean)          // K2 was the table's last reader: leave it at rest (-1)
     for (int64_t i = blockIdx.x * int64_t(kThreads) + tid; i <= P.mask; i += int64_t(gridDim.x) * kThreads)
       P.table[i] = -1;
   if (P.permute) {
@@ -1405,6 +1775,20 @@ bool carveout_max() {
   return on;
 }
 
+// The group path (group_kernel, one CTA per expert) when the gate map is one compaction round
+// (n*k <= 16K copies), else K1 tiles + K2 clusters, whose per-expert CTA clusters spread the big
+// groups of the 64K-copy layers.  Measured (scripts/compress_diag.py, graph-timed per call):
+// C2 39.5 vs 44.7 us, C5 49.4 vs 48.9, C3 119.0 vs 93.3, C4 108.9 vs 95.6.
+// LSHMOE_COMPRESS_PATH=group / tiles forces one.
+bool group_path(int nk) {
+  static const int force = [] {
+    const char* e = getenv("LSHMOE_COMPRESS_PATH");
+    return !e ? 0 : (e[0] == 'g' ? 1 : (e[0] == 't' ? 2 : 0));
+  }();
+  if (force) return force == 1;
+  return nk <= kGRound * kGThreads;
+}
+
 int launch_chain(const Params& P, cudaStream_t st) {
   static bool configured = false;
   const int max_range = centroid_max_range(P.nk);
@@ -1414,6 +1798,7 @@ int launch_chain(const Params& P, cudaStream_t st) {
     int err = cudaFuncSetAttribute(centroid_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCentroidSmemMax);
     if (!err) err = cudaFuncSetAttribute(centroid_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCentroidSmemMax);
     if (!err) err = cudaFuncSetAttribute(bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBucketSmem);
+    if (!err) err = cudaFuncSetAttribute(group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGroupSmem);
     // every kernel of the step prefers the full shared-memory carveout, so an SM never has to drain
     // and re-partition L1 / shared memory between two kernels of the chain (LSHMOE_CARVEOUT=0: off)
     if (!err && carveout_max()) err = cudaFuncSetAttribute(tile_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -1423,11 +1808,18 @@ int launch_chain(const Params& P, cudaStream_t st) {
   }
   Params p = P;
   p.max_range = max_range;
-  p.dyn_smem = kBucketSmem;
   p.diag = diag_enabled() ? 1 : 0;
-  p.cs = bucket_cluster_size(P.E);
-  int err = launch_pdl(tile_kernel, P.ntiles, kThreads, 0, st, p, true);
-  if (!err) err = launch_pdl(bucket_kernel, P.E * p.cs, kBThreads, kBucketSmem, st, p, true, p.cs);
+  int err = 0;
+  if (group_path(P.nk)) {                        // one CTA per expert (group_kernel), then K3
+    p.dyn_smem = kGroupSmem;
+    p.table_clean = 1;
+    err = launch_pdl(group_kernel, P.E, kGThreads, kGroupSmem, st, p, true);
+  } else {                                   // K1 tiles + K2 clusters (LSHMOE_COMPRESS_PATH=tiles)
+    p.dyn_smem = kBucketSmem;
+    p.cs = bucket_cluster_size(P.E);
+    err = launch_pdl(tile_kernel, P.ntiles, kThreads, 0, st, p, true);
+    if (!err) err = launch_pdl(bucket_kernel, P.E * p.cs, kBThreads, kBucketSmem, st, p, true, p.cs);
+  }
   if (!err) err = p.p2p_peers ? launch_pdl(centroid_kernel<true>, centroid_grid(), kThreads, csmem, st, p, true)
                               : launch_pdl(centroid_kernel<false>, centroid_grid(), kThreads, P.permute ? 0 : csmem, st, p, true);
   return err;

@@ -57,6 +57,8 @@ m = int(out.num_rows.item())
 print(f"m={m} expert_rows max={int(out.expert_rows.max())}")
 for kern, st in L.compress_diag(ws).items():
     D = {k: np.array(v) for k, v in st.items()}
+    if np.all(np.isnan(D["end"])):
+        continue
     print(kern)
     for k, v in D.items():
         if np.all(np.isnan(v)):
