@@ -614,7 +614,12 @@ struct EpiScratch<BiasActEpi<BN>> { static constexpr int value = 0; };   // bias
 template <class Epi>
 __device__ __forceinline__ bool epi_skip_mma(const Epi&) { return false; }
 template <int BN>
-__device__ __forceinline__ bool epi_skip_mma(const BiasActEpi<BN>& e) { return e.exp == 2; }
+__device__ __forceinline__ bool epi_skip_mma(const BiasActEpi<BN>& e) { return e.exp == 2 || e.exp == 3; }
+// experiment 3 (FFN): no MMAs and no accumulator drain (TMEM loads, bias, stores): the TMA stream alone
+template <class Epi>
+__device__ __forceinline__ bool epi_skip_drain(const Epi&) { return false; }
+template <int BN>
+__device__ __forceinline__ bool epi_skip_drain(const BiasActEpi<BN>& e) { return e.exp == 3; }
 template <bool G>
 __device__ __forceinline__ bool epi_skip_mma(const ArgmaxEpiT<G>& e) { return e.exp == 2; }
 
@@ -805,7 +810,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN;
 #pragma unroll 1
-        for (int cb = half * kBlkPer; cb < (half + 1) * kBlkPer; ++cb) {
+        for (int cb = half * kBlkPer; cb < (half + 1) * kBlkPer && !epi_skip_drain(epi); ++cb) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + cb * 32, r);
           tmem_ld_wait();
@@ -997,7 +1002,8 @@ int cta_mode(const char* env_name, int dflt) {
 int experiment_mode(const char* env_name) {
   const char* on = getenv("LSHMOE_EXPERIMENTS");
   if (!on || on[0] != '1') return 0;
-  return cta_mode(env_name, 0);
+  const char* env = getenv(env_name);
+  return env && env[0] >= '0' && env[0] <= '9' ? env[0] - '0' : 0;
 }
 
 int ffn_order() {   // experiment override LSHMOE_FFN_ORDER (0 expert-major, 1 N-tile-major)

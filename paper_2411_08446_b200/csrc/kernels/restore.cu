@@ -54,8 +54,9 @@ __global__ void __launch_bounds__(256) restore_kernel(const T* x /* y may alias 
 // the next row's bucket id and x chunks fetched before the current row's c~ / E(c~) gathers are
 // combined, so the dependent bucket -> gather chain of the next row overlaps this row's.  Measured
 // (C2, graph-replayed, clean cold L2): 14.3 us against 18.4 us for the flat thread-per-chunk kernel;
-// at d = 1024 (C3, C4) the flat kernel stays ahead, so the row kernel serves k = 1 rows of <= 96
-// chunks (LSHMOE_RESTORE_VAR: 0 forces the flat kernel, 2 / 4 the row kernel with 2 / 4 CTAs per SM).
+// at d = 1024 (C3, C4) the flat kernel stays ahead.  Superseded for k = 1 rows of <= 96 chunks by
+// restore_row2_kernel (below); LSHMOE_RESTORE_VAR: 0 forces the flat kernel, 2 / 4 this kernel
+// with 2 / 4 CTAs per SM, 12 / 14 the two-row kernel.
 template <typename T, int CPL>
 __global__ void __launch_bounds__(256) restore_row_kernel(const T* x, const T* __restrict__ ct,
                                                           const T* __restrict__ ret, int64_t n, int d, int cpr,
@@ -114,6 +115,82 @@ __global__ void __launch_bounds__(256) restore_row_kernel(const T* x, const T* _
     for (int j = 0; j < CPL; ++j) {
       const int c = lane + 32 * j;
       if (c < cpr) Vec<T>::store(y + t * d + c * VN, acc[j]);
+    }
+  }
+}
+
+// k = 1, two consecutive token rows per warp iteration: the pair's c~ / E(c~) gathers (6 KB per
+// warp) are in flight together with the next pair's x rows and bucket ids (3 KB), twice the bytes
+// in flight of restore_row_kernel per warp.
+template <typename T, int CPL>
+__global__ void __launch_bounds__(256) restore_row2_kernel(const T* x, const T* __restrict__ ct,
+                                                           const T* __restrict__ ret, int64_t n, int d, int cpr,
+                                                           const int32_t* __restrict__ bucket,
+                                                           const float* __restrict__ g, T* y) {
+  constexpr int VN = Vec<T>::N;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) >> 5;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * 8;
+  uint4 xr[2][CPL];
+  int32_t bn[2] = {0, 0};
+  auto fetch = [&](int64_t t) {               // rows t, t + 1
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = t + h;
+      if (r < n) {
+        bn[h] = __ldg(bucket + r);
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+          const int c = lane + 32 * j;
+          if (c < cpr) xr[h][j] = __ldg(reinterpret_cast<const uint4*>(x + r * d) + c);
+        }
+      }
+    }
+  };
+  if (2 * w0 < n) fetch(2 * w0);
+  for (int64_t t = 2 * w0; t < n; t += 2 * nw) {
+    uint4 xc[2][CPL];
+    int32_t b[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      b[h] = bn[h];
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) xc[h][j] = xr[h][j];
+    }
+    uint4 cr[2][CPL], rr[2][CPL];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (t + h < n)
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+          const int c = lane + 32 * j;
+          if (c < cpr) {
+            cr[h][j] = __ldg(reinterpret_cast<const uint4*>(ct + static_cast<int64_t>(b[h]) * d) + c);
+            rr[h][j] = __ldg(reinterpret_cast<const uint4*>(ret + static_cast<int64_t>(b[h]) * d) + c);
+          }
+        }
+    if (t + 2 * nw < n) fetch(t + 2 * nw);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (t + h >= n) break;
+      const float gw = g ? g[t + h] : 1.0f;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        const int c = lane + 32 * j;
+        if (c >= cpr) continue;
+        float xv[VN], cv[VN], rv[VN], acc[VN];
+        Vec<T>::load(&xc[h][j], xv);
+        Vec<T>::load(&cr[h][j], cv);
+        Vec<T>::load(&rr[h][j], rv);
+#pragma unroll
+        for (int v = 0; v < VN; ++v) {
+          const float term = rv[v] + (xv[v] - cv[v]);
+          acc[v] = g ? gw * term : term;
+        }
+        Vec<T>::store(y + (t + h) * d + c * VN, acc);
+      }
     }
   }
 }
@@ -288,8 +365,24 @@ int launch_restore_pdl(const void* x, const void* ct, const void* ret, int64_t n
     return true;
   }();
   (void)carve;
+  // k = 1 rows of <= 96 chunks: two rows per warp iteration, 2 CTAs per SM (graph-timed over cycled
+  // token copies, scripts/restore_ab2.py: C2 13.45 vs 14.50 us for one row per warp, C5 18.9 vs 21.9)
   int var = restore_variant();
-  if (var < 0) var = (k == 1 && cpr >= 32 && cpr <= 96) ? 2 : 0;
+  if (var < 0) var = (k == 1 && cpr >= 32 && cpr <= 96) ? 12 : 0;
+  if (var >= 12 && k == 1 && cpr >= 32 && cpr <= 128) {   // 10 + CTAs per SM, two rows per warp
+    const int64_t pairs = (n + 1) / 2;
+    const int warps = static_cast<int>(std::min<int64_t>(pairs, int64_t(var - 10) * 8 * device_sm_count()));
+    cfg.gridDim = dim3(std::max(1, (warps + 7) / 8));
+    const int cpl = (cpr + 31) / 32;
+    const T* xp2 = static_cast<const T*>(x);
+    const T* cp2 = static_cast<const T*>(ct);
+    const T* rp2 = static_cast<const T*>(ret);
+    T* yp2 = static_cast<T*>(y);
+    if (cpl == 1) return cudaLaunchKernelEx(&cfg, restore_row2_kernel<T, 1>, xp2, cp2, rp2, n, d, cpr, bucket, g, yp2);
+    if (cpl == 2) return cudaLaunchKernelEx(&cfg, restore_row2_kernel<T, 2>, xp2, cp2, rp2, n, d, cpr, bucket, g, yp2);
+    if (cpl == 3) return cudaLaunchKernelEx(&cfg, restore_row2_kernel<T, 3>, xp2, cp2, rp2, n, d, cpr, bucket, g, yp2);
+    return cudaLaunchKernelEx(&cfg, restore_row2_kernel<T, 4>, xp2, cp2, rp2, n, d, cpr, bucket, g, yp2);
+  }
   const T* xp = static_cast<const T*>(x);
   const T* cp = static_cast<const T*>(ct);
   const T* rp = static_cast<const T*>(ret);
