@@ -765,20 +765,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             // descriptors of the stage's k-block; +32 B of K = +2 in the 16-byte start-address field
             const uint64_t ad = smem_desc_sw128(smem_u32(sA + stage * C::kABytes));
             const uint64_t bd = smem_desc_sw128(smem_u32(sB + stage * C::kBBytes));
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              if (epi_skip_mma(epi)) break;
-              if (kEB == 1 && kCta == 2)   // 32 e4m3 = 32 bytes of K per instruction
-                mma_fp8_ss_2cta_w(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
-              else if (kEB == 1)
-                mma_fp8_ss_w(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
-              else if (kCta == 2)
-                mma_bf16_ss_2cta_w(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
-              else
-                mma_bf16_ss_w(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+            static_assert(BK / 16 == 4, "mma4_commit issues four MMAs per k-block");
+            if (epi_skip_mma(epi)) {      // experiment: no MMAs, the slot is freed at once
+              if (kCta == 2) mma_commit_2cta_mc_w(&empty[stage], gmask);
+              else mma_commit_w(&empty[stage]);
+            } else if (kEB == 1 && kCta == 2) {   // 32 e4m3 = 32 bytes of K per instruction
+              mma4_commit_2cta_fp8(d_tmem, ad, bd, idesc, kb != 0, &empty[stage], gmask);
+            } else if (kEB == 1) {
+              mma4_commit_1cta_fp8(d_tmem, ad, bd, idesc, kb != 0, &empty[stage]);
+            } else if (kCta == 2) {             // the commit frees the slot in both CTAs of the pair
+              mma4_commit_2cta_bf16(d_tmem, ad, bd, idesc, kb != 0, &empty[stage], gmask);
+            } else {
+              mma4_commit_1cta_bf16(d_tmem, ad, bd, idesc, kb != 0, &empty[stage]);
             }
-            if (kCta == 2) mma_commit_2cta_mc_w(&empty[stage], gmask);   // frees the slot in both CTAs
-            else mma_commit_w(&empty[stage]);
             if (++stage == C::kStages) {
               stage = 0;
               phase ^= 1;

@@ -279,6 +279,64 @@ __device__ __forceinline__ void mma_commit_2cta_mc_w(uint64_t* bar, uint16_t cta
       : "memory");
 }
 
+// High word of smem_desc_sw128 (SBO = 1024 B, version 1, SWIZZLE_128B); the low word carries the
+// start address and LBO.
+constexpr uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+// One k-block of 64 bytes x 2 of K per operand row (four MMAs: descriptors advanced by 2 = 32 B
+// each) and the commit of the stage's empty barrier, all issued by one elected lane of a converged
+// warp inside a single asm block: one ELECT and one operand conversion per k-block instead of one
+// per instruction.  kMma: the tcgen05.mma instruction (cta_group and kind); kCommit: the commit.
+// The descriptors are passed as their low words (start address | LBO): the high word is the
+// constant SBO / version / SWIZZLE_128B part, and +2 on the 14-bit start field never carries.
+#define LSHMOE_MMA4_BODY(MMA)                                                              \
+  "{\n\t.reg .pred e, p, t;\n\t.reg .b32 l1, l2, l3, m1, m2, m3;\n\t"                     \
+  ".reg .b64 a0, a1, a2, a3, b0, b1, b2, b3;\n\t"                                          \
+  "elect.sync _|e, 0xffffffff;\n\t"                                                        \
+  "setp.ne.b32 p, %4, 0;\n\t"                                                              \
+  "setp.eq.u32 t, 0, 0;\n\t"                                                               \
+  "add.u32 l1, %1, 2;\n\tadd.u32 l2, %1, 4;\n\tadd.u32 l3, %1, 6;\n\t"                     \
+  "add.u32 m1, %2, 2;\n\tadd.u32 m2, %2, 4;\n\tadd.u32 m3, %2, 6;\n\t"                     \
+  "mov.b64 a0, {%1, %7};\n\tmov.b64 a1, {l1, %7};\n\tmov.b64 a2, {l2, %7};\n\t"           \
+  "mov.b64 a3, {l3, %7};\n\tmov.b64 b0, {%2, %7};\n\tmov.b64 b1, {m1, %7};\n\t"           \
+  "mov.b64 b2, {m2, %7};\n\tmov.b64 b3, {m3, %7};\n\t"                                    \
+  "@e " MMA " [%0], a0, b0, %3, p;\n\t"                                                    \
+  "@e " MMA " [%0], a1, b1, %3, t;\n\t"                                                    \
+  "@e " MMA " [%0], a2, b2, %3, t;\n\t"                                                    \
+  "@e " MMA " [%0], a3, b3, %3, t;\n\t"
+__device__ __forceinline__ void mma4_commit_1cta_bf16(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                                      uint32_t acc, uint64_t* bar) {
+  asm volatile(LSHMOE_MMA4_BODY("tcgen05.mma.cta_group::1.kind::f16")
+               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(d),
+               "r"(static_cast<uint32_t>(ad)), "r"(static_cast<uint32_t>(bd)), "r"(idesc), "r"(acc), "r"(smem_u32(bar)),
+               "h"(static_cast<uint16_t>(0)), "n"(kDescHi)
+               : "memory");
+}
+__device__ __forceinline__ void mma4_commit_1cta_fp8(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                                     uint32_t acc, uint64_t* bar) {
+  asm volatile(LSHMOE_MMA4_BODY("tcgen05.mma.cta_group::1.kind::f8f6f4")
+               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(d),
+               "r"(static_cast<uint32_t>(ad)), "r"(static_cast<uint32_t>(bd)), "r"(idesc), "r"(acc), "r"(smem_u32(bar)),
+               "h"(static_cast<uint16_t>(0)), "n"(kDescHi)
+               : "memory");
+}
+__device__ __forceinline__ void mma4_commit_2cta_bf16(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                                      uint32_t acc, uint64_t* bar, uint16_t mask) {
+  asm volatile(LSHMOE_MMA4_BODY("tcgen05.mma.cta_group::2.kind::f16")
+               "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n\t}" ::"r"(d),
+               "r"(static_cast<uint32_t>(ad)), "r"(static_cast<uint32_t>(bd)), "r"(idesc), "r"(acc), "r"(smem_u32(bar)),
+               "h"(mask), "n"(kDescHi)
+               : "memory");
+}
+__device__ __forceinline__ void mma4_commit_2cta_fp8(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                                     uint32_t acc, uint64_t* bar, uint16_t mask) {
+  asm volatile(LSHMOE_MMA4_BODY("tcgen05.mma.cta_group::2.kind::f8f6f4")
+               "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n\t}" ::"r"(d),
+               "r"(static_cast<uint32_t>(ad)), "r"(static_cast<uint32_t>(bd)), "r"(idesc), "r"(acc), "r"(smem_u32(bar)),
+               "h"(mask), "n"(kDescHi)
+               : "memory");
+}
+#undef LSHMOE_MMA4_BODY
+
 // Shared-memory matrix descriptor, K-major operand staged by TMA with SWIZZLE_128B: rows of 128 B
 // (64 bf16), 8-row swizzle atoms of 1024 B.  start address and strides in 16-byte units;
 // LBO unused for swizzled K-major (1); SBO = 1024 B between 8-row groups; bits 46-47 = version 1
@@ -287,9 +345,7 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t smem_addr) {
   uint64_t desc = 0;
   desc |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
   desc |= static_cast<uint64_t>(1) << 16;                    // LBO (ignored)
-  desc |= static_cast<uint64_t>(1024 >> 4) << 32;            // SBO
-  desc |= static_cast<uint64_t>(1) << 46;                    // descriptor version (sm_100)
-  desc |= static_cast<uint64_t>(2) << 61;                    // SWIZZLE_128B
+  desc |= static_cast<uint64_t>(kDescHi) << 32;             // SBO 1024 B | version 1 (bit 46) | SWIZZLE_128B (61-63)
   return desc;
 }
 
