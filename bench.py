@@ -700,12 +700,15 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 "peak": hbm, "frac": ach / hbm}
     kernels = [kern("hash: tc_gemm_kernel<ArgmaxEpi>", "tensor", hash_flops, t_hash)] if args.hash == "cp" else \
         [{"kernel": f"hash ({args.hash})", "us": t_hash, "note": "see roofline"}]
-    kernels.append(kern("compress: tile + bucket + centroid (3 launches)", "hbm", comp_bytes, t_comp))
+    group_path = bool(span) and not span.get("tiles")   # the group path has no tile kernel (compress.cu)
+    kernels.append(kern("compress: group + centroid (2 launches)" if group_path else
+                        "compress: tile + bucket + centroid (3 launches)", "hbm", comp_bytes, t_comp))
     if span.get("centroid"):
         kernels.append(kern("centroid_kernel (span, diagnostics stamps)", "hbm", cent_bytes, span["centroid"]))
     for nm_ in ("tiles", "bucket"):
         if span.get(nm_):
-            kk = kern(f"{nm_} kernel (span, diagnostics stamps)", "hbm", 4 * nk * (3 if nm_ == "tiles" else 4), span[nm_])
+            label = "group_kernel" if group_path and nm_ == "bucket" else f"{nm_} kernel"
+            kk = kern(f"{label} (span, diagnostics stamps)", "hbm", 4 * nk * (3 if nm_ == "tiles" else 4), span[nm_])
             kk["bound"] = "latency"
             kk["note"] = "integer index work of < 1 MB: dependent global round trips and barriers, not bytes"
             kernels.append(kk)
@@ -721,7 +724,8 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     else:
         kf["hbm_frac"] = kh["frac"]
         kernels.append(kf)
-    kernels.append(kern("restore_kernel", "hbm", rest_bytes, t_rest))
+    kernels.append(kern("restore (restore_row2_kernel for k = 1 rows <= 1.5 KB, else restore_kernel)", "hbm",
+                        rest_bytes, t_rest))
     t_lower = max(hash_flops / (tc_peak * 1e12), hash_bytes / (hbm * 1e9)) * 1e6 + comp_bytes / (hbm * 1e9) * 1e6 \
         + rest_bytes / (hbm * 1e9) * 1e6 + 2 * off_rows * row_bytes / (nvlink_gbs * 1e9) * 1e6
     layer_roofline = {"t_lower_us": t_lower, "t_dc_us": t_dc, "frac": t_lower / t_dc,
@@ -800,7 +804,10 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                                "timing": "K launches over the cycled token sets (tokens never L2-resident) back to "
                                          "back in one CUDA graph, events on its stream; us per launch"},
                 "peak_source": pk["source"] + " bf16 dense (burst) — cuBLAS bf16 GEMM",
-                "frac_of_sustained": achieved / pk["bf16_tflops_sustained"] if pk.get("bf16_tflops_sustained") else None}
+                "frac_of_sustained": achieved / pk["bf16_tflops_sustained"] if pk.get("bf16_tflops_sustained") else None,
+                # the measured cuBLAS figure is not the hardware ceiling: the kernel can exceed it (frac > 1);
+                # against NVIDIA's nominal dense bf16 figure it stays below 1
+                "frac_of_nominal": achieved / 2250.0, "nominal_tflops": 2250.0}
 
     cpu = None
     parity = None
