@@ -116,7 +116,9 @@ struct HashSched {
     w.nparts = np;
     w.tag1 = j;
     w.tag0 = (mt * (bm / BM) + rank) * q + j;
-    if (first >= last || c0 >= c1 || mt >= m_tiles) {   // past this cluster's last piece / the tokens
+    // (a group whose token tile lies past n keeps the unit: its A rows read as zeros, its epilogue
+    // writes nothing, and it still issues its share of the cluster's multicast B loads)
+    if (first >= last || c0 >= c1) {           // past this cluster's last piece
       w.nchunks = 0;
       w.part = 0;
       w.b_row0 = 0;
@@ -476,7 +478,7 @@ struct ArgmaxEpiT {
         return;
       }
     }
-    if (w.nchunks == 0) return;                      // an empty unit (contiguous schedule)
+    if (w.nchunks == 0 || w.valid_rows <= 0) return;   // an empty unit / a slice past n (CTA-uniform)
     merge_chains();
     if (nthr > 128) {   // combine the two column halves of each row; the lower half wins ties
       uint2* mb = reinterpret_cast<uint2*>(scratch + 64);
@@ -627,7 +629,11 @@ __device__ __forceinline__ bool epi_skip_mma(const ArgmaxEpiT<G>& e) { return e.
 // kEB: operand element bytes — 2 = bf16 (kind::f16, 16-element MMA K), 1 = e4m3 (kind::f8f6f4,
 // 32-element MMA K).  A k-block is always 128 bytes of K per row (one SWIZZLE_128B atom row), so
 // the shared-memory layout, descriptors and byte offsets are the same for both.
-template <int BN, int kCta, class Sched, class Epi, int kEB = 2>
+// kMC > 1 (CTA pairs only): the cluster holds kMC pairs walking the same B chunks on their own
+// token tiles; CTA (group g, rank r) loads 1/kMC of its half-B rows and multicasts them to the CTAs of
+// rank r in every group, so each B byte is read from L2 once per cluster instead of once per pair.
+// Every pair's commit then frees the stage in all CTAs of the cluster (empty barriers count kMC).
+template <int BN, int kCta, class Sched, class Epi, int kEB = 2, int kMC = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                    Sched sched, Epi epi) {
@@ -664,11 +670,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cluster = blockIdx.x / csize;
   const int nclusters = gridDim.x / csize;
   const uint16_t gmask = static_cast<uint16_t>(((1u << kCta) - 1u) << gbase);   // the group's CTAs
+  static_assert(kMC == 1 || kCta == 2, "B multicast is built on CTA pairs");
+  // stage frees go to every CTA whose stage this group's data (A, and B for kMC > 1) lands in
+  const uint16_t emask = kMC > 1 ? static_cast<uint16_t>((1u << (kCta * kMC)) - 1u) : gmask;
+  uint16_t bmask = 0;                         // the CTAs of this rank in every group (B multicast)
+#pragma unroll
+  for (int g2 = 0; g2 < kMC; ++g2) bmask |= static_cast<uint16_t>(1u << (g2 * kCta + rank));
+  constexpr int kBSubRows = C::kBRows / kMC;  // B rows this CTA loads for the cluster
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kMC);            // one commit from each group's MMA issuer
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -730,7 +743,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kCta == 2) {
               if (leader) mbar_arrive_expect_tx_w(&full[stage], C::kTxBytes);
               tma_load_2d_2sm_w(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBKe, w.a_row);
-              tma_load_2d_2sm_w(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBKe, brow);
+              if constexpr (kMC > 1)
+                tma_load_2d_2sm_mc_w(sB + stage * C::kBBytes + group * kBSubRows * 128, &tmB, &full[stage],
+                                     kb * kBKe, brow + group * kBSubRows, bmask);
+              else
+                tma_load_2d_2sm_w(sB + stage * C::kBBytes, &tmB, &full[stage], kb * kBKe, brow);
             } else {
               mbar_arrive_expect_tx_w(&full[stage], C::kTxBytes);
               tma_load_2d_w(sA + stage * C::kABytes, &tmA, &full[stage], kb * kBKe, w.a_row);
@@ -767,14 +784,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bd = smem_desc_sw128(smem_u32(sB + stage * C::kBBytes));
             static_assert(BK / 16 == 4, "mma4_commit issues four MMAs per k-block");
             if (epi_skip_mma(epi)) {      // experiment: no MMAs, the slot is freed at once
-              if (kCta == 2) mma_commit_2cta_mc_w(&empty[stage], gmask);
+              if (kCta == 2) mma_commit_2cta_mc_w(&empty[stage], emask);
               else mma_commit_w(&empty[stage]);
             } else if (kEB == 1 && kCta == 2) {   // 32 e4m3 = 32 bytes of K per instruction
-              mma4_commit_2cta_fp8(d_tmem, ad, bd, idesc, kb != 0, &empty[stage], gmask);
+              mma4_commit_2cta_fp8(d_tmem, ad, bd, idesc, kb != 0, &empty[stage], emask);
             } else if (kEB == 1) {
               mma4_commit_1cta_fp8(d_tmem, ad, bd, idesc, kb != 0, &empty[stage]);
             } else if (kCta == 2) {             // the commit frees the slot in both CTAs of the pair
-              mma4_commit_2cta_bf16(d_tmem, ad, bd, idesc, kb != 0, &empty[stage], gmask);
+              mma4_commit_2cta_bf16(d_tmem, ad, bd, idesc, kb != 0, &empty[stage], emask);
             } else {
               mma4_commit_1cta_bf16(d_tmem, ad, bd, idesc, kb != 0, &empty[stage]);
             }
@@ -871,9 +888,9 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int b
   return r == CUDA_SUCCESS ? 0 : cudaErrorInvalidValue;
 }
 
-template <int BN, int kCta, class Sched, class Epi, int kEB = 2>
+template <int BN, int kCta, class Sched, class Epi, int kEB = 2, int kMC = 1>
 int configure_tc() {
-  auto kern = tc_gemm_kernel<BN, kCta, Sched, Epi, kEB>;
+  auto kern = tc_gemm_kernel<BN, kCta, Sched, Epi, kEB, kMC>;
   static int configured = -1;     // one attribute call per instantiation
   if (configured < 0) {
     configured = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -886,9 +903,9 @@ int configure_tc() {
 
 // Clusters of csize CTAs of this instantiation that can be resident at once (0 on error): the
 // persistent grid must not exceed it (GPCs whose SM count is not a multiple of csize leave SMs idle).
-template <int BN, int kCta, class Sched, class Epi, int kEB = 2>
+template <int BN, int kCta, class Sched, class Epi, int kEB = 2, int kMC = 1>
 int active_clusters(int csize) {
-  if (configure_tc<BN, kCta, Sched, Epi, kEB>()) return 0;
+  if (configure_tc<BN, kCta, Sched, Epi, kEB, kMC>()) return 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(csize * 512);
   cfg.blockDim = dim3(kThreads);
@@ -901,7 +918,7 @@ int active_clusters(int csize) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<BN, kCta, Sched, Epi, kEB>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<BN, kCta, Sched, Epi, kEB, kMC>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -909,11 +926,11 @@ int active_clusters(int csize) {
 }
 
 // groups: MMA groups per cluster (cluster = kCta * groups CTAs); grid is a multiple of the cluster.
-template <int BN, int kCta, class Sched, class Epi, int kEB = 2>
+template <int BN, int kCta, class Sched, class Epi, int kEB = 2, int kMC = 1>
 int launch_tc(const CUtensorMap& a, const CUtensorMap& b, int K, const Sched& s, const Epi& e, int grid,
               cudaStream_t st, int groups = 1) {
-  auto kern = tc_gemm_kernel<BN, kCta, Sched, Epi, kEB>;
-  if (int err = configure_tc<BN, kCta, Sched, Epi, kEB>()) return err;
+  auto kern = tc_gemm_kernel<BN, kCta, Sched, Epi, kEB, kMC>;
+  if (int err = configure_tc<BN, kCta, Sched, Epi, kEB, kMC>()) return err;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -993,6 +1010,12 @@ int hash_active_clusters(int bn, int cta, int groups) {
 int cta_mode(const char* env_name, int dflt) {
   const char* env = getenv(env_name);
   if (env && (env[0] == '1' || env[0] == '2')) return env[0] - '0';
+  return dflt;
+}
+
+int cta_mode_any(const char* env_name, int dflt) {   // a small positive integer from the environment
+  const char* env = getenv(env_name);
+  if (env && env[0] >= '1' && env[0] <= '9') return env[0] - '0';
   return dflt;
 }
 
@@ -1079,6 +1102,25 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
     e.partial = reinterpret_cast<uint2*>(static_cast<uint8_t*>(ws) + counters);
   }
   s.groups = 1;
+  // B multicast across kMC CTA pairs of a cluster (LSHMOE_HASH_MC = 2 / 4; 1 = off)
+  const int mc = cta == 2 && bn == 256 && s.split ? cta_mode_any("LSHMOE_HASH_MC", 1) : 1;
+  if (mc == 2 || mc == 4) {
+    const int ac = mc == 2 ? active_clusters<256, 2, HashSched, ArgmaxEpi, 2, 2>(2 * mc)
+                           : active_clusters<256, 2, HashSched, ArgmaxEpi, 2, 4>(2 * mc);
+    if (ac > 0) {
+      const int G = set_contig(s, 2, d / bn, mc, ac);
+      s.bn = bn;
+      s.bm = BM * 2;
+      CUtensorMap ma, mb;
+      int err = make_map(&ma, x, n, d, BM);
+      if (!err) err = make_map(&mb, R, static_cast<int64_t>(q) * d, d, bn / 2 / mc);
+      if (err) return err;
+      const int grid = G * 2 * mc;
+      cudaStream_t st = static_cast<cudaStream_t>(stream);
+      return mc == 2 ? launch_tc<256, 2, HashSched, ArgmaxEpi, 2, 2>(ma, mb, d, s, e, grid, st, mc)
+                     : launch_tc<256, 2, HashSched, ArgmaxEpi, 2, 4>(ma, mb, d, s, e, grid, st, mc);
+    }
+  }
   int hint = s.m_tiles * q * (s.split ? d / bn : 1);
   int groups = 1;
   if (s.split) {

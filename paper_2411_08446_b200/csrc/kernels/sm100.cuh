@@ -223,6 +223,19 @@ __device__ __forceinline__ void tma_load_2d_2sm_w(void* smem_dst, const CUtensor
       "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1)
       : "memory");
 }
+// 2-SM TMA with cluster multicast: the box lands at the same shared-memory offset in every CTA of
+// cta_mask; each destination's pair leader (peer bit cleared) counts the bytes.
+__device__ __forceinline__ void tma_load_2d_2sm_mc_w(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                                     int c1, uint16_t cta_mask) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;\n\t}" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1), "h"(cta_mask)
+      : "memory");
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_2cta(uint32_t* smem_dst) {   // same warp in both CTAs
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
