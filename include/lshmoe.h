@@ -198,8 +198,11 @@ lshmoe_status lshmoe_compress(const void* x, lshmoe_dtype dtype, int64_t n, int 
 
 /* ---- a6/a8 communicator ----------------------------------------------------------------------
    Expert placement: rank p owns experts [p*E/w, (p+1)*E/w).  NCCL over NVLink; the
-   bootstrap id travels over torch.distributed.  world == 1 needs no id (pass NULL); id == NULL at
-   world > 1 makes a comm without NCCL, usable only by the phase-2 calls below. */
+   bootstrap id travels over torch.distributed.  world == 1 needs no id (pass NULL: dispatch /
+   combine are then the aliased local exchange); world == 1 WITH an id makes a one-rank NCCL comm
+   whose dispatch / combine run the phase-1 code (count all-gather, host plan, self segments,
+   grouped send/recv) — phase 1 exercised on one GPU.  id == NULL at world > 1 makes a comm without
+   NCCL, usable only by the phase-2 calls below. */
 lshmoe_status lshmoe_get_unique_id(uint8_t* id /* [host] LSHMOE_UNIQUE_ID_BYTES */);
 lshmoe_status lshmoe_comm_init(const uint8_t* id /* [host] */, int world, int rank,
                                lshmoe_comm** out /* [host] */);

@@ -510,7 +510,8 @@ class Comm:
         self.world, self.rank = world, rank
         h = ctypes.c_void_p()
         idbuf = None
-        if world > 1 and unique_id is not None:       # None: phase-2-only comm (no NCCL)
+        if unique_id is not None:                     # None: phase-2-only comm (no NCCL); world 1 with an
+            # id: a one-rank NCCL comm whose dispatch / combine run the phase-1 code
             if len(unique_id) != UNIQUE_ID_BYTES:
                 raise ValueError("the NCCL unique id is 128 bytes")
             idbuf = (ctypes.c_uint8 * UNIQUE_ID_BYTES).from_buffer_copy(unique_id)

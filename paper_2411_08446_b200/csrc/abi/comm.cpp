@@ -106,7 +106,10 @@ lshmoe_status lshmoe_comm_init(const uint8_t* id, int world, int rank, lshmoe_co
   auto* c = new lshmoe_comm();
   c->world = world;
   c->rank = rank;
-  if (world > 1 && id) {   // id == NULL at world > 1: a phase-2-only comm (no NCCL)
+  // id == NULL at world > 1: a phase-2-only comm (no NCCL).  world == 1 with an id: a one-rank NCCL
+  // communicator whose dispatch / combine run the phase-1 code (count all-gather, host plan, self
+  // segments, grouped send/recv) instead of the aliased local exchange — phase 1 on one GPU.
+  if (id) {
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof(u));
     lshmoe_status st = nccl_status(ncclCommInitRank(&c->nccl, world, u, rank), "ncclCommInitRank");
@@ -344,7 +347,7 @@ lshmoe_status lshmoe_comm_destroy(lshmoe_comm* c) {
 
 lshmoe_status lshmoe_comm_last_counts(const lshmoe_comm* c, int32_t* counts, int E) {
   if (!c || !counts) return set_error(LSHMOE_EINVAL, "lshmoe_comm_last_counts: NULL");
-  if (c->last_E != E || c->world == 1) return set_error(LSHMOE_EINVAL, "lshmoe_comm_last_counts: no plan for this E");
+  if (c->last_E != E || !c->nccl) return set_error(LSHMOE_EINVAL, "lshmoe_comm_last_counts: no plan for this E");
   std::memcpy(counts, c->counts.data(), sizeof(int32_t) * c->world * E);
   return LSHMOE_OK;
 }
@@ -358,7 +361,7 @@ lshmoe_status lshmoe_dispatch(lshmoe_comm* c, const void* centroids, lshmoe_dtyp
   if (!centroids || !expert_rows || !recv || !recv_rows) return set_error(LSHMOE_EINVAL, "lshmoe_dispatch: NULL pointer");
   const size_t row_bytes = static_cast<size_t>(d) * (dtype == LSHMOE_F32 ? 4 : 2);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (world == 1) {   // recv_rows [E, 1] == expert_rows: alias it to skip the copy
+  if (world == 1 && !(c && c->nccl)) {   // recv_rows [E, 1] == expert_rows: alias it to skip the copy
     int err = launch_local_exchange(centroids, recv == centroids ? nullptr : recv, recv_capacity,
                                     static_cast<int>(row_bytes), expert_rows, E,
                                     recv_rows == expert_rows ? nullptr : recv_rows, stream);
@@ -432,7 +435,7 @@ lshmoe_status lshmoe_combine(lshmoe_comm* c, const void* expert_out, lshmoe_dtyp
   if (!expert_out || !expert_rows || !returned) return set_error(LSHMOE_EINVAL, "lshmoe_combine: NULL pointer");
   const size_t row_bytes = static_cast<size_t>(d) * (dtype == LSHMOE_F32 ? 4 : 2);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (world == 1) {
+  if (world == 1 && !(c && c->nccl)) {
     int err = launch_local_exchange(expert_out, returned == expert_out ? nullptr : returned, returned_capacity,
                                     static_cast<int>(row_bytes), expert_rows, E, nullptr, stream);
     return cuda_status(err, "lshmoe_combine (local)");
