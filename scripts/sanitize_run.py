@@ -48,6 +48,8 @@ def layer(cfg, seed=0, giant=False):
 layer(CONFIGS["C1"])
 small = LayerConfig("S-bf16", 3000, 768, 8, 2, 6, "bf16", 512, 24, 0.1)
 Xd, zd, codes = layer(small, giant=True)
+layer(LayerConfig("S-bf16-k1", 2000, 768, 8, 1, 6, "bf16", 512, 24, 0.1))   # two-row restore, group path k = 1
+layer(LayerConfig("S-f32-tiles", 17000, 64, 4, 1, 2, "f32", 256, 16, 0.1))   # n*k > 16K: the tiles compress path
 # NEXT-2/3/4 hashes
 L.sp_hash(Xd, L.sp_normals(L.rotation(768, 6, 3, torch.bfloat16).cuda(), 12), 6, 12)
 L.hash_e4m3(L.quantize_e4m3(Xd), L.rotation_e4m3(768, 6, 3).cuda())
