@@ -969,12 +969,26 @@ __global__ void __launch_bounds__(kGThreads, 1) group_kernel(Params P) {
 // order.  Columns are processed in blocks of 128 chunks (2 KB of a row) to bound registers.
 constexpr int kBlkChunks = 128;          // 16-byte chunks per column block
 constexpr int kCPL = kBlkChunks / 32;    // chunks per lane per block
+// Centroid-phase CTA shape: kCWarps warps (LSHMOE_CWARPS, 8 or 16); the per-warp rings shrink with
+// more warps so the shared memory per SM stays within budget.  16 warps (one 512-thread CTA per SM)
+// hide more of the gathers' and the ring reads' latency: compress per call (scripts/compress_diag.py)
+// C2 39.4 -> 37.6 us, C3 93.3 -> 85.3, C4 ~98 -> 92.0 (centroid spans C2 19.5 -> 17.3, C3 57.4 -> 45.7,
+// C4 55 -> 45.8 us).
+#ifndef LSHMOE_CWARPS
+#define LSHMOE_CWARPS 16
+#endif
+static_assert(LSHMOE_CWARPS == 8 || LSHMOE_CWARPS == 16, "centroid warps: 8 or 16");
+constexpr int kCWarps = LSHMOE_CWARPS;
+constexpr int kCThreads = 32 * kCWarps;
 constexpr int kRingSlot = 16 * kBlkChunks;
 constexpr int kWpartFloats = kBlkChunks * 8;   // one warp partial slot (fp32, up to 8 per chunk)
-constexpr int kQ = 10;                   // ring rows per warp at the largest (2 KB) slot
+constexpr int kQ = kCWarps == 8 ? 10 : 4;   // ring rows per warp at the largest (2 KB) slot (16 warps:
+                                            // the slot-0 partials double, so the rings shrink more)
 constexpr int kRingWarp = kQ * kRingSlot;   // ring bytes per warp; slots are packed at 16*ncb bytes,
                                             // so short rows get a deeper ring (1.5 KB rows: 13 slots)
 static_assert(kWpartFloats * 4 <= kRingWarp, "a warp's slot-1 partial reuses its ring");
+// ring rows per warp for CPL chunks per lane (slots packed at CPL * 512 bytes), at most 16
+constexpr int ring_depth(int cpl) { return kRingWarp / (cpl * 512) < 16 ? kRingWarp / (cpl * 512) : 16; }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
@@ -1118,12 +1132,12 @@ struct CentroidCtx {                     // one CTA's view of its perm range (ce
   uint32_t prev_row;                     // row of entry w_begin - 1
   int cut_rs, cut_re;                    // threads 0 / 1: perm extent of the range's first / last row
   __device__ uint8_t* ring() const { return g_dsmem + w * kRingWarp; }
-  __device__ float* slot0() const { return reinterpret_cast<float*>(g_dsmem + kWarps * kRingWarp); }
-  __device__ uint32_t* s_row() const { return reinterpret_cast<uint32_t*>(slot0() + kWarps * kWpartFloats); }
+  __device__ float* slot0() const { return reinterpret_cast<float*>(g_dsmem + kCWarps * kRingWarp); }
+  __device__ uint32_t* s_row() const { return reinterpret_cast<uint32_t*>(slot0() + kCWarps * kWpartFloats); }
   __device__ int32_t* s_tok() const { return reinterpret_cast<int32_t*>(s_row()) + tok_off; }
   __device__ float* s_wt(int max_range) const { return reinterpret_cast<float*>(s_tok()) + max_range; }
   __device__ uint32_t row_at(int p) const { return s_row()[p - p_begin + 1]; }
-  __device__ int wbeg(int ww) const { return p_begin + range_begin(ww, range, kWarps); }
+  __device__ int wbeg(int ww) const { return p_begin + range_begin(ww, range, kCWarps); }
   __device__ float* wpart(int ww, int slot) const {   // slot 0: own region; slot 1: the warp's ring
     return slot == 0 ? slot0() + ww * kWpartFloats : reinterpret_cast<float*>(g_dsmem + ww * kRingWarp);
   }
@@ -1234,7 +1248,7 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
       if (X.row_at(mid) == r) a = mid + 1; else z = mid;
     }
     const int hi = a;
-    const int wl = range_cta(hi - 1 - X.p_begin, X.range, kWarps);
+    const int wl = range_cta(hi - 1 - X.p_begin, X.range, kCWarps);
     const bool before = lo == X.p_begin && X.row_at(X.p_begin - 1) == r;
     const bool after = hi == X.p_end && X.row_at(X.p_end) == r;
     const float rc = P.grad ? 1.0f : __frcp_rn(static_cast<float>(hi - lo));
@@ -1265,7 +1279,7 @@ __device__ void centroid_block(const Params& P, const CentroidCtx& X, int cb, in
     }
   };
   if (nrows > 0) {
-    const bool first_w = w == range_cta(0, X.range, kWarps);   // first non-empty sub-range of the CTA
+    const bool first_w = w == range_cta(0, X.range, kCWarps);   // first non-empty sub-range of the CTA
     if (cut_end && (first_w || !from_before)) own(r_last, seg_start);
     if (first_w) {                            // the CTA's first row, begun in an earlier CTA
       const uint32_t r0 = X.row_at(X.p_begin);
@@ -1302,7 +1316,7 @@ __device__ __forceinline__ void prefetch_cut_extent(const Params& P, CentroidCtx
   }
 }
 
-// The index entries i = tid + kThreads u (u < kPre) of a CTA's range, loaded right after the
+// The index entries i = tid + kCThreads u (u < kPre) of a CTA's range, loaded right after the
 // kernel's dependency wait so that their latency overlaps the expert-count scan.
 constexpr int kPre = 4;
 struct IndexPre {
@@ -1313,7 +1327,7 @@ __device__ __forceinline__ void preload_index(const Params& P, IndexPre& pre) {
   const int pb = range_begin(b, P.nk, G), range = range_begin(b + 1, P.nk, G) - pb;
 #pragma unroll
   for (int u = 0; u < kPre; ++u) {
-    const int i = tid + kThreads * u, p = pb - 1 + i;
+    const int i = tid + kCThreads * u, p = pb - 1 + i;
     pre.l[u] = 0;
     pre.c[u] = 0;
     if (i < range + 2 && p >= 0 && p < P.nk) {
@@ -1340,7 +1354,7 @@ __device__ __forceinline__ void centroid_phase(const Params& P, const int* s_gof
   uint32_t* s_row = X.s_row();
   int32_t* s_tok = X.s_tok();
 #pragma unroll 1
-  for (int i = tid, u = 0; i < X.range + 2; i += kThreads, ++u) {
+  for (int i = tid, u = 0; i < X.range + 2; i += kCThreads, ++u) {
     const int p = X.p_begin - 1 + i;
     uint32_t row = 0xFFFFFFFFu;
     if (p >= 0 && p < P.nk) {
@@ -1372,9 +1386,9 @@ __device__ __forceinline__ void centroid_phase(const Params& P, const int* s_gof
   for (int c0 = 0, cb = 0; c0 < P.nch; c0 += kBlkChunks, ++cb) {
     const int ncb = min(kBlkChunks, P.nch - c0);
     switch ((ncb + 31) / 32) {
-      case 1: centroid_block<T, 1, 16, kF>(P, X, cb, c0, ncb); break;
-      case 2: centroid_block<T, 2, 16, kF>(P, X, cb, c0, ncb); break;
-      case 3: centroid_block<T, 3, 13, kF>(P, X, cb, c0, ncb); break;
+      case 1: centroid_block<T, 1, ring_depth(1), kF>(P, X, cb, c0, ncb); break;
+      case 2: centroid_block<T, 2, ring_depth(2), kF>(P, X, cb, c0, ncb); break;
+      case 3: centroid_block<T, 3, ring_depth(3), kF>(P, X, cb, c0, ncb); break;
       default: centroid_block<T, 4, kQ, kF>(P, X, cb, c0, ncb); break;
     }
   }
@@ -1434,7 +1448,7 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
     const bool all_nonempty = P.nk >= G;
     uint8_t* fdst = nullptr;
     if constexpr (kF) fdst = fused_row_dst(P, row);   // owner row, once per merged row
-    for (int ch = tid; ch < nc8; ch += kThreads) {
+    for (int ch = tid; ch < nc8; ch += kCThreads) {
       float acc[VC];
       const float* src = P.partial + (static_cast<int64_t>(b0) * 2 + slot0) * P.d + ch * VC;
 #pragma unroll
@@ -1467,7 +1481,7 @@ __device__ void merge_cut_rows(const Params& P, const CentroidCtx& X, const int*
 template <typename T>
 __device__ void gather_rows(const Params& P) {   // baseline: send[p] = x[token of copy at p]
   const int64_t work = static_cast<int64_t>(P.nk) * P.nch;
-  for (int64_t w = blockIdx.x * int64_t(kThreads) + threadIdx.x; w < work; w += int64_t(gridDim.x) * kThreads) {
+  for (int64_t w = blockIdx.x * int64_t(kCThreads) + threadIdx.x; w < work; w += int64_t(gridDim.x) * kCThreads) {
     const int p = static_cast<int>(w / P.nch);
     const int ch = static_cast<int>(w - int64_t(p) * P.nch);
     const int t = ldcg(P.rowl + p) / P.k;
@@ -1509,13 +1523,13 @@ __device__ void fused_prologue(const Params& P, const int* s_roff, const int* s_
   const uint32_t ep = *reinterpret_cast<volatile unsigned*>(P.p2p_done + 2) + 1u;
   *epoch_out = ep;
   if (blockIdx.x == 0)
-    for (int i = tid; i < w * E; i += kThreads) {
+    for (int i = tid; i < w * E; i += kCThreads) {
       const int p = i / E, e = i - p * E;
       const uint64_t v = (static_cast<uint64_t>(ep) << 32) | static_cast<uint32_t>(s_mrow[e]);
       asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(f_slot(P, p, ep, P.p2p_me, e)), "l"(v) : "memory");
     }
   const uint64_t t0 = gtimer();
-  for (int i = tid; i < w * E; i += kThreads) {
+  for (int i = tid; i < w * E; i += kCThreads) {
     const int src = i / E, e = i - src * E;
     uint64_t v = ld_rlx_sys64(f_slot(P, P.p2p_me, ep, src, e));
     while (static_cast<uint32_t>(v >> 32) != ep) {
@@ -1530,8 +1544,8 @@ __device__ void fused_prologue(const Params& P, const int* s_roff, const int* s_
     s_fc[i] = static_cast<int>(v & 0xffffffffu);
   }
   __syncthreads();
-  for (int e = tid; e <= E; e += kThreads) g_f_roff[e] = s_roff[e];
-  for (int e = tid; e < E; e += kThreads) {
+  for (int e = tid; e <= E; e += kCThreads) g_f_roff[e] = s_roff[e];
+  for (int e = tid; e < E; e += kCThreads) {
     const int p = e / epr, el = e - p * epr;
     long long b = 0;
     for (int e2 = 0; e2 < el; ++e2)
@@ -1540,7 +1554,7 @@ __device__ void fused_prologue(const Params& P, const int* s_roff, const int* s_
     g_f_dst[e] = b;
   }
   if (blockIdx.x == 0 && P.p2p_recv_rows)
-    for (int i = tid; i < epr * w; i += kThreads) {
+    for (int i = tid; i < epr * w; i += kCThreads) {
       const int el = i / w, s2 = i - el * w;
       P.p2p_recv_rows[i] = s_fc[s2 * E + P.p2p_me * epr + el];
     }
@@ -1576,11 +1590,11 @@ __device__ void fused_close(const Params& P, uint32_t ep) {
 // kF: the fused dispatch (lshmoe_compress_p2p) — compiled separately, so the plain kernel's
 // reduction loop carries no remote-store code.
 template <bool kF>
-__global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
+__global__ void __launch_bounds__(kCThreads, 1) centroid_kernel(Params P) {
   __shared__ int s_goff[kRadix + 1];         // perm offset of each expert group
   __shared__ int s_roff[kRadix + 1];         // first global row of each expert
   __shared__ int s_mrow[kRadix];             // m_e
-  __shared__ int s_scan[kWarps + 1];
+  __shared__ int s_scan[kCWarps + 1];
   __shared__ int s_cut[4];
   __shared__ int s_job[8];
   const int tid = threadIdx.x;
@@ -1590,7 +1604,7 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   IndexPre pre;
   if (!P.permute) preload_index(P, pre);      // in flight during the expert-count scan below
   if (!P.permute && !P.table_clean)          // K2 was the table's last reader: leave it at rest (-1)
-    for (int64_t i = blockIdx.x * int64_t(kThreads) + tid; i <= P.mask; i += int64_t(gridDim.x) * kThreads)
+    for (int64_t i = blockIdx.x * int64_t(kCThreads) + tid; i <= P.mask; i += int64_t(gridDim.x) * kCThreads)
       P.table[i] = -1;
   if (P.permute) {
     if (P.is_bf16) gather_rows<__nv_bfloat16>(P);
@@ -1601,7 +1615,7 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
     const int m_e = tid < P.E ? ldcg(P.expert_rows + tid) : 0;
     const int go = tid < P.E ? ldcg(P.gofs + tid) : 0;   // in flight with m_e (and the index preload)
     int m;
-    const int ro = block_excl_scan<kWarps>(m_e, s_scan, &m);
+    const int ro = block_excl_scan<kCWarps>(m_e, s_scan, &m);
     if (tid < P.E) {
       s_goff[tid] = go;
       s_roff[tid] = ro;
@@ -1617,14 +1631,14 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
     }
     __syncthreads();
   }
-  // row_start of every global row: rows r = blockIdx.x + G (tid + kThreads u) of this CTA, loaded now
+  // row_start of every global row: rows r = blockIdx.x + G (tid + kCThreads u) of this CTA, loaded now
   // and stored after the reduction, so the load's round trip is off every CTA's critical path
   constexpr int kRS = 2;
   int rs_val[kRS];
   const int m_all = s_roff[P.E];
 #pragma unroll
   for (int u = 0; u < kRS; ++u) {
-    const int r = blockIdx.x + gridDim.x * (tid + kThreads * u);
+    const int r = blockIdx.x + gridDim.x * (tid + kCThreads * u);
     rs_val[u] = 0;
     if (r < m_all) {
       const int e = expert_at(s_roff, P.E, r);
@@ -1647,10 +1661,10 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
   }
 #pragma unroll
   for (int u = 0; u < kRS; ++u) {
-    const int r = blockIdx.x + gridDim.x * (tid + kThreads * u);
+    const int r = blockIdx.x + gridDim.x * (tid + kCThreads * u);
     if (r < m_all) P.row_start[r] = rs_val[u];
   }
-  for (int r = blockIdx.x + gridDim.x * (tid + kThreads * kRS); r < m_all; r += gridDim.x * kThreads) {
+  for (int r = blockIdx.x + gridDim.x * (tid + kCThreads * kRS); r < m_all; r += gridDim.x * kCThreads) {
     const int e = expert_at(s_roff, P.E, r);     // (m > G * 512 rows only)
     P.row_start[r] = ldcg(P.rsl + s_goff[e] + (r - s_roff[e]));
   }
@@ -1663,7 +1677,7 @@ __global__ void __launch_bounds__(kThreads, 1) centroid_kernel(Params P) {
 // ---- NEXT-1 grad_compress: G_b = sum_{(t,s) in b} g_ts dY_t over the forward's buckets --------
 // The centroid kernel's machinery with the row of perm entry p = bucket[perm[p]], the gate weight
 // of the copy staged beside its token id, and no 1/count; cut rows via the forward's row_start.
-__global__ void __launch_bounds__(kThreads, 1) grad_centroid_kernel(Params P) {
+__global__ void __launch_bounds__(kCThreads, 1) grad_centroid_kernel(Params P) {
   __shared__ int s_cut[4];
   __shared__ int s_job[8];
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
@@ -1678,7 +1692,7 @@ __global__ void __launch_bounds__(kThreads, 1) grad_centroid_kernel(Params P) {
   uint32_t* s_row = X.s_row();
   int32_t* s_tok = X.s_tok();
   float* s_w = X.s_wt(P.max_range);
-  for (int i = tid; i < X.range + 2; i += kThreads) {
+  for (int i = tid; i < X.range + 2; i += kCThreads) {
     const int p = X.p_begin - 1 + i;
     uint32_t row = 0xFFFFFFFFu;
     if (p >= 0 && p < P.nk) {
@@ -1701,16 +1715,16 @@ __global__ void __launch_bounds__(kThreads, 1) grad_centroid_kernel(Params P) {
     const int cpl = (ncb + 31) / 32;
     if (P.is_bf16) {
       switch (cpl) {
-        case 1: centroid_block<__nv_bfloat16, 1, 16>(P, X, cb, c0, ncb); break;
-        case 2: centroid_block<__nv_bfloat16, 2, 16>(P, X, cb, c0, ncb); break;
-        case 3: centroid_block<__nv_bfloat16, 3, 13>(P, X, cb, c0, ncb); break;
+        case 1: centroid_block<__nv_bfloat16, 1, ring_depth(1)>(P, X, cb, c0, ncb); break;
+        case 2: centroid_block<__nv_bfloat16, 2, ring_depth(2)>(P, X, cb, c0, ncb); break;
+        case 3: centroid_block<__nv_bfloat16, 3, ring_depth(3)>(P, X, cb, c0, ncb); break;
         default: centroid_block<__nv_bfloat16, 4>(P, X, cb, c0, ncb); break;
       }
     } else {
       switch (cpl) {
-        case 1: centroid_block<float, 1, 16>(P, X, cb, c0, ncb); break;
-        case 2: centroid_block<float, 2, 16>(P, X, cb, c0, ncb); break;
-        case 3: centroid_block<float, 3, 13>(P, X, cb, c0, ncb); break;
+        case 1: centroid_block<float, 1, ring_depth(1)>(P, X, cb, c0, ncb); break;
+        case 2: centroid_block<float, 2, ring_depth(2)>(P, X, cb, c0, ncb); break;
+        case 3: centroid_block<float, 3, ring_depth(3)>(P, X, cb, c0, ncb); break;
         default: centroid_block<float, 4>(P, X, cb, c0, ncb); break;
       }
     }
@@ -1728,7 +1742,7 @@ int centroid_max_range(int nk) {
 }
 // K3 shared memory: per-warp rings, warp partials, the range's index arrays.
 int centroid_smem(int max_range) {   // + the grad mode's per-entry weights
-  return kWarps * kRingWarp + kWarps * kWpartFloats * 4 + 4 * (3 * max_range + 2);
+  return kCWarps * kRingWarp + kCWarps * kWpartFloats * 4 + 4 * (3 * max_range + 2);
 }
 
 // K2 CTAs per expert: the largest power of two CS <= kMaxCS for which all E clusters of CS CTAs
@@ -1820,8 +1834,8 @@ int launch_chain(const Params& P, cudaStream_t st) {
     err = launch_pdl(tile_kernel, P.ntiles, kThreads, 0, st, p, true);
     if (!err) err = launch_pdl(bucket_kernel, P.E * p.cs, kBThreads, kBucketSmem, st, p, true, p.cs);
   }
-  if (!err) err = p.p2p_peers ? launch_pdl(centroid_kernel<true>, centroid_grid(), kThreads, csmem, st, p, true)
-                              : launch_pdl(centroid_kernel<false>, centroid_grid(), kThreads, P.permute ? 0 : csmem, st, p, true);
+  if (!err) err = p.p2p_peers ? launch_pdl(centroid_kernel<true>, centroid_grid(), kCThreads, csmem, st, p, true)
+                              : launch_pdl(centroid_kernel<false>, centroid_grid(), kCThreads, P.permute ? 0 : csmem, st, p, true);
   return err;
 }
 
@@ -2045,7 +2059,7 @@ int launch_grad_compress(const void* dy, lshmoe_dtype dtype, int64_t n, int d, c
   P.max_range = max_range;
   P.grad = 1;
   P.gw = gw;
-  grad_centroid_kernel<<<centroid_grid(), kThreads, smem, st>>>(P);
+  grad_centroid_kernel<<<centroid_grid(), kCThreads, smem, st>>>(P);
   count_launches(1);
   return cudaGetLastError();
 }
