@@ -150,7 +150,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(0.0002)   # a timed region of a few ms still gets several samples
 
     def __enter__(self):
         if self._ok:
