@@ -307,10 +307,25 @@ def main():
     assert cfg.E % world == 0, "experts must split evenly over ranks"
     E_local = cfg.E // world
     p2p = args.exchange in ("p2p", "p2p-fused")
+    comm = None
     if p2p:     # phase 2: a window per rank (receive + returned buffers), peers mapped over CUDA IPC
-        comm = L.Comm(world, rank, None).p2p_init(cfg.n * cfg.k * world, cfg.n * cfg.k, cfg.d, X_dtype(cfg), cfg.E,
-                                                  group=dist.group.WORLD if world > 1 else None)
-    else:
+        ok = 1
+        try:
+            comm = L.Comm(world, rank, None).p2p_init(cfg.n * cfg.k * world, cfg.n * cfg.k, cfg.d, X_dtype(cfg),
+                                                      cfg.E, group=dist.group.WORLD if world > 1 else None)
+        except Exception as ex:   # noqa: BLE001  (e.g. no peer access between these GPUs)
+            ok = 0
+            print(f"bench.py rank {rank}: phase-2 window setup failed ({str(ex)[:200]})", file=sys.stderr)
+        if world > 1:             # every rank takes the same exchange
+            flag = torch.tensor([ok], dtype=torch.int32, device="cpu" if args.share_gpu else dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            ok = int(flag.item())
+        if not ok:
+            if world == 1 or args.share_gpu:
+                raise SystemExit("bench.py: the phase-2 exchange could not be set up")
+            print("bench.py: falling back to the phase-1 (NCCL) exchange", file=sys.stderr)
+            args.exchange, p2p = "nccl", False
+    if not p2p:
         comm = L.Comm.from_process_group() if world > 1 else None
 
     # ---- inputs (seeded synthetic, per rank) and buffers ----
