@@ -984,7 +984,10 @@ constexpr int kRingSlot = 16 * kBlkChunks;
 constexpr int kWpartFloats = kBlkChunks * 8;   // one warp partial slot (fp32, up to 8 per chunk)
 constexpr int kQ = kCWarps == 8 ? 10 : 4;   // ring rows per warp at the largest (2 KB) slot (16 warps:
                                             // the slot-0 partials double, so the rings shrink more)
-constexpr int kRingWarp = kQ * kRingSlot;   // ring bytes per warp; slots are packed at 16*ncb bytes,
+#ifndef LSHMOE_CRING
+#define LSHMOE_CRING 0   // experiment: ring bytes per warp (0: kQ 2 KB slots)
+#endif
+constexpr int kRingWarp = LSHMOE_CRING ? LSHMOE_CRING : kQ * kRingSlot;   // ring bytes per warp; slots are packed at 16*ncb bytes,
                                             // so short rows get a deeper ring (1.5 KB rows: 13 slots)
 static_assert(kWpartFloats * 4 <= kRingWarp, "a warp's slot-1 partial reuses its ring");
 // ring rows per warp for CPL chunks per lane (slots packed at CPL * 512 bytes), at most 16
@@ -1389,7 +1392,7 @@ __device__ __forceinline__ void centroid_phase(const Params& P, const int* s_gof
       case 1: centroid_block<T, 1, ring_depth(1), kF>(P, X, cb, c0, ncb); break;
       case 2: centroid_block<T, 2, ring_depth(2), kF>(P, X, cb, c0, ncb); break;
       case 3: centroid_block<T, 3, ring_depth(3), kF>(P, X, cb, c0, ncb); break;
-      default: centroid_block<T, 4, kQ, kF>(P, X, cb, c0, ncb); break;
+      default: centroid_block<T, 4, ring_depth(4), kF>(P, X, cb, c0, ncb); break;
     }
   }
 }
@@ -1718,14 +1721,14 @@ __global__ void __launch_bounds__(kCThreads, 1) grad_centroid_kernel(Params P) {
         case 1: centroid_block<__nv_bfloat16, 1, ring_depth(1)>(P, X, cb, c0, ncb); break;
         case 2: centroid_block<__nv_bfloat16, 2, ring_depth(2)>(P, X, cb, c0, ncb); break;
         case 3: centroid_block<__nv_bfloat16, 3, ring_depth(3)>(P, X, cb, c0, ncb); break;
-        default: centroid_block<__nv_bfloat16, 4>(P, X, cb, c0, ncb); break;
+        default: centroid_block<__nv_bfloat16, 4, ring_depth(4)>(P, X, cb, c0, ncb); break;
       }
     } else {
       switch (cpl) {
         case 1: centroid_block<float, 1, ring_depth(1)>(P, X, cb, c0, ncb); break;
         case 2: centroid_block<float, 2, ring_depth(2)>(P, X, cb, c0, ncb); break;
         case 3: centroid_block<float, 3, ring_depth(3)>(P, X, cb, c0, ncb); break;
-        default: centroid_block<float, 4>(P, X, cb, c0, ncb); break;
+        default: centroid_block<float, 4, ring_depth(4)>(P, X, cb, c0, ncb); break;
       }
     }
   }
@@ -1733,7 +1736,7 @@ __global__ void __launch_bounds__(kCThreads, 1) grad_centroid_kernel(Params P) {
   else merge_cut_rows<float>(P, X, nullptr, nullptr, s_cut, s_job);
 }
 
-constexpr int kCentroidSmemMax = 200 * 1024;   // K3 dynamic smem + static <= 227 KB
+constexpr int kCentroidSmemMax = 216 * 1024;   // K3 dynamic smem + static <= 227 KB
 constexpr int kBucketSmem = 200 * 1024;        // K2 dynamic smem (+ 8 KB static)
 int centroid_grid() { return std::min(device_sm_count(), kMaxGrid); }
 int centroid_max_range(int nk) {
