@@ -365,10 +365,12 @@ int launch_restore_pdl(const void* x, const void* ct, const void* ret, int64_t n
     return true;
   }();
   (void)carve;
-  // k = 1 rows of <= 96 chunks: two rows per warp iteration, 2 CTAs per SM (graph-timed over cycled
-  // token copies, scripts/restore_ab2.py: C2 13.45 vs 14.50 us for one row per warp, C5 18.9 vs 21.9)
+  // k = 1 rows of <= 128 chunks: two rows per warp iteration, 2 CTAs per SM (graph-timed over cycled
+  // token copies, scripts/restore_ab2.py: C2 13.45 vs 14.50 us for one row per warp, C5 18.9 vs 21.9,
+  // C4 (d = 1024) 64.1 vs 75.4 us for the flat kernel); k > 1 keeps the flat kernel (C3 50.1 us vs
+  // 59-69 for the row kernels)
   int var = restore_variant();
-  if (var < 0) var = (k == 1 && cpr >= 32 && cpr <= 96) ? 12 : 0;
+  if (var < 0) var = (k == 1 && cpr >= 32 && cpr <= 128) ? 12 : 0;
   if (var >= 12 && k == 1 && cpr >= 32 && cpr <= 128) {   // 10 + CTAs per SM, two rows per warp
     const int64_t pairs = (n + 1) / 2;
     const int warps = static_cast<int>(std::min<int64_t>(pairs, int64_t(var - 10) * 8 * device_sm_count()));
