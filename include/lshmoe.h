@@ -187,7 +187,12 @@ lshmoe_status lshmoe_compress_workspace(int64_t n, int k, int num_experts, int q
    (rank, expert) group (Alg. 1 L4-L6, reading R5).  Centroid = fp32 sum in a fixed order
    scaled once by the correctly rounded reciprocal of the count (reading R10).  Stream-ordered; no
    host synchronisation.  n*k is bounded by the per-SM shared-memory staging of one perm range
-   (about 2700 * SM count copies, ~400K on B200); larger calls fail with an error. */
+   (about 2700 * SM count copies, ~400K on B200); larger calls fail with an error.
+   Ordering: the gate map (experts) is read as soon as the preceding kernel on the stream signals
+   its programmatic dependents, before that kernel has finished (the codes only after it has).  This
+   holds for any predecessor that does not trigger dependents early, and for lshmoe_hash (it does not
+   write the gate map); when the predecessor is lshmoe_gate_hash on the same stream the library waits
+   for it first.  LSHMOE_EARLY_GATE=0 disables the early read. */
 lshmoe_status lshmoe_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d,
                               const int16_t* codes, int q,
                               const int32_t* experts, int k, int num_experts,

@@ -119,6 +119,7 @@ lshmoe_status lshmoe_gate_hash(const void* x, int64_t n, int d, const void* RG, 
   const size_t need = hash_workspace_bytes(n, d, q);
   REQUIRE(workspace_bytes >= need, LSHMOE_EINVAL, "workspace too small (see lshmoe_hash_workspace)");
   REQUIRE(need == 0 || (workspace && aligned16(workspace)), LSHMOE_EINVAL, "workspace NULL or misaligned");
+  note_gate_hash_stream(stream);   // before the launch: a failed launch only costs the overlap
   return cuda_status(launch_gate_hash_bf16(x, n, d, RG, q, E, k, codes, zeta, gw, workspace, stream),
                      "lshmoe_gate_hash");
 }

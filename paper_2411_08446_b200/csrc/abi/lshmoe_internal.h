@@ -51,6 +51,9 @@ struct CompressWs {            // carved from the caller's workspace by compress
 };
 size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, CompressWs* ws);
 
+// lshmoe_gate_hash launched on `stream`: the next compress there reads the gate map only after
+// griddepcontrol.wait (compress.cu)
+void note_gate_hash_stream(void* stream);
 int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int16_t* codes, int q,
                     const int32_t* experts, int k, int E, int32_t* bucket, int32_t* perm,
                     int32_t* row_start, int32_t* expert_rows, int32_t* num_rows, void* centroids,

@@ -32,6 +32,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "../abi/lshmoe_internal.h"
 #include "common.cuh"
@@ -123,6 +125,9 @@ struct Params {
   const float* gw;                 // grad: gate weights [nk] or nullptr (weight 1)
   int diag;                        // 1: record per-CTA globaltimer stamps (diagnostics)
   int table_clean;                 // 1: the global hash table was not used (group path): K3 skips its reset
+  int early_gate;                  // 1: the gate map is complete before the preceding kernel signals its
+                                   // dependents (not lshmoe_gate_hash's output): group_kernel compacts it
+                                   // before griddepcontrol.wait, overlapping the hash kernel's tail
   // phase-2 dispatch fused into K3 (lshmoe_compress_p2p); p2p_peers == nullptr: off
   uint8_t* const* p2p_peers;
   int64_t p2p_mailbox, p2p_recv, p2p_data_flag, p2p_recv_cap;
@@ -624,6 +629,54 @@ __device__ __forceinline__ int group_sum(int v, int* s) {
   return t;
 }
 
+// Keys of members [0, n_e): the member's token's q codes packed two per word (KW words); the hash of
+// the key goes to aux.  kGB members per thread per batch, all their code loads issued before any is
+// used (kGB = 4 covers a 4K-member group in one round trip).
+template <bool kS, int kGB, int kKW>
+__device__ __forceinline__ void group_keys(const Params& P, int n_e, int KW, const int32_t* mem, uint32_t* key,
+                                           int32_t* aux) {
+  const int tid = threadIdx.x;
+  const int q = P.q, k = P.k;
+  const bool even = (q & 1) == 0;           // rows of q int16 are 4-byte aligned: word loads
+  for (int j0 = tid; j0 < n_e; j0 += kGB * kGThreads) {
+    uint32_t wv[kGB][kKW];
+#pragma unroll
+    for (int m = 0; m < kGB; ++m) {
+      const int j = j0 + m * kGThreads;
+      if (j < n_e) {
+        const int c = gld<kS>(mem + j);
+        const int64_t t = c / k;
+        if (even) {
+          const uint32_t* kc = reinterpret_cast<const uint32_t*>(P.codes + t * q);
+#pragma unroll
+          for (int w = 0; w < kKW; ++w)
+            if (w < KW) wv[m][w] = __ldg(kc + w);
+        } else {
+          const uint16_t* kc = reinterpret_cast<const uint16_t*>(P.codes + t * q);
+#pragma unroll
+          for (int w = 0; w < kKW; ++w)
+            if (w < KW) wv[m][w] = static_cast<uint32_t>(__ldg(kc + 2 * w)) |
+                                   (2 * w + 1 < q ? static_cast<uint32_t>(__ldg(kc + 2 * w + 1)) << 16 : 0u);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kGB; ++m) {
+      const int j = j0 + m * kGThreads;
+      if (j < n_e) {
+        uint32_t h = 0x9E3779B9u;
+#pragma unroll
+        for (int w = 0; w < kKW; ++w)
+          if (w < KW) {
+            key[static_cast<int64_t>(j) * KW + w] = wv[m][w];
+            h = fmix32(h ^ (wv[m][w] + 0x632BE5ABu * static_cast<uint32_t>(w + 1)));
+          }
+        aux[j] = static_cast<int32_t>(h);
+      }
+    }
+  }
+}
+
 // mem: the expert's members (copy ids, ascending), n_e of them, in shared memory at g_dsmem[0]
 // (smem mode) or in the workspace (global mode).  Shared-memory layout (smem mode):
 // [mem n_e][slot n_e][aux n_e][rs n_e][fa T][free] — 16 B per member + 4 B per table slot; the
@@ -672,46 +725,8 @@ __device__ void group_body(const Params& P, int e, int n_e, int goff, int T, int
   for (int i = tid; i < T; i += kGThreads) fa[i] = -1;
   // keys: the member's token's q codes packed two per word (workspace); the hash goes to aux.
   // kGB members per thread per batch, all their code loads issued before any is used.
-  const int q = P.q, k = P.k;
-  const bool even = (q & 1) == 0;           // rows of q int16 are 4-byte aligned: word loads
-  constexpr int kGB = 2;
-  for (int j0 = tid; j0 < n_e; j0 += kGB * kGThreads) {
-    uint32_t wv[kGB][kMaxQ / 2];
-#pragma unroll
-    for (int m = 0; m < kGB; ++m) {
-      const int j = j0 + m * kGThreads;
-      if (j < n_e) {
-        const int c = gld<kS>(mem + j);
-        const int64_t t = c / k;
-        if (even) {
-          const uint32_t* kc = reinterpret_cast<const uint32_t*>(P.codes + t * q);
-#pragma unroll
-          for (int w = 0; w < kMaxQ / 2; ++w)
-            if (w < KW) wv[m][w] = __ldg(kc + w);
-        } else {
-          const uint16_t* kc = reinterpret_cast<const uint16_t*>(P.codes + t * q);
-#pragma unroll
-          for (int w = 0; w < kMaxQ / 2; ++w)
-            if (w < KW) wv[m][w] = static_cast<uint32_t>(__ldg(kc + 2 * w)) |
-                                   (2 * w + 1 < q ? static_cast<uint32_t>(__ldg(kc + 2 * w + 1)) << 16 : 0u);
-        }
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < kGB; ++m) {
-      const int j = j0 + m * kGThreads;
-      if (j < n_e) {
-        uint32_t h = 0x9E3779B9u;
-#pragma unroll
-        for (int w = 0; w < kMaxQ / 2; ++w)
-          if (w < KW) {
-            key[static_cast<int64_t>(j) * KW + w] = wv[m][w];
-            h = fmix32(h ^ (wv[m][w] + 0x632BE5ABu * static_cast<uint32_t>(w + 1)));
-          }
-        aux[j] = static_cast<int32_t>(h);
-      }
-    }
-  }
+  if (KW <= 4) group_keys<kS, 4, 4>(P, n_e, KW, mem, key, aux);   // q <= 8: 4 members' loads in flight
+  else group_keys<kS, 2, kMaxQ / 2>(P, n_e, KW, mem, key, aux);
   __syncthreads();                          // every key is stored before any slot is claimed
   dstamp(P, 1, 1);
   // insert: a slot's value converges (atomicMin) to the smallest member index with its key (a
@@ -913,7 +928,10 @@ __global__ void __launch_bounds__(kGThreads, 1) group_kernel(Params P) {
   __shared__ int s_cnt[kGRound * kGWarps];
   const int tid = threadIdx.x;
   const int e = blockIdx.x, E = P.E, nk = P.nk;
-  pdl_wait();                               // the hash kernel's codes (and the gate map) are visible
+  // The gate map is an input of the step, complete before the hash kernel started (early_gate):
+  // its validation and compaction (shared memory only, no global writes but the error word) run
+  // while the hash kernel's last CTAs finish; the codes are read only after griddepcontrol.wait.
+  if (!P.early_gate) pdl_wait();            // lshmoe_gate_hash wrote the gate map: wait first
   pdl_trigger();
   dstamp(P, 1, 0);
   // this CTA validates the copies [c0, c1): ids in [0, E) (bit 0, in the compaction pass) and,
@@ -932,6 +950,7 @@ __global__ void __launch_bounds__(kGThreads, 1) group_kernel(Params P) {
   int clt;
   const int n_e = group_compact(P, e, sm, cap, c0, c1, s_scan, s_cnt, &clt);
   const int goff = group_sum(clt, s_scan);
+  if (P.early_gate) pdl_wait();             // the hash kernel's codes are complete and visible
   dstamp(P, 1, 7);
   const int KW = (P.q + 1) / 2;
   int T = 64;
@@ -1933,6 +1952,33 @@ size_t compress_workspace_layout(int64_t n, int k, int E, int d, void* base, Com
   return off;
 }
 
+// Streams whose last library launch was lshmoe_gate_hash: its kernel writes the gate map and
+// signals its dependents before finishing, so the next compress on that stream must not read the
+// gate map before griddepcontrol.wait.  Any other predecessor leaves the gate map complete when
+// it signals (kernels without an early trigger signal at completion).  LSHMOE_EARLY_GATE=0: off.
+static std::mutex g_gate_mu;
+static std::vector<void*> g_gate_streams;
+
+void note_gate_hash_stream(void* stream) {
+  std::lock_guard<std::mutex> lk(g_gate_mu);
+  if (std::find(g_gate_streams.begin(), g_gate_streams.end(), stream) == g_gate_streams.end())
+    g_gate_streams.push_back(stream);
+}
+
+static int early_gate_for(void* stream) {
+  static const bool off = [] {
+    const char* e = getenv("LSHMOE_EARLY_GATE");
+    return e && e[0] == '0';
+  }();
+  std::lock_guard<std::mutex> lk(g_gate_mu);
+  auto it = std::find(g_gate_streams.begin(), g_gate_streams.end(), stream);
+  if (it != g_gate_streams.end()) {
+    g_gate_streams.erase(it);
+    return 0;
+  }
+  return off ? 0 : 1;
+}
+
 static Params base_params(const void* x, lshmoe_dtype dtype, int64_t n, int d, const int32_t* experts, int k, int E,
                           const CompressWs& ws) {
   Params P{};
@@ -1984,6 +2030,7 @@ int launch_compress(const void* x, lshmoe_dtype dtype, int64_t n, int d, const i
   // the table, the last arriver its counter); the diagnostics stamps are cleared only when on.
   if (diag_enabled() && (err = cudaMemsetAsync(ws.hdr, 0xFF, sizeof(int32_t) * kHdr, st))) return err;
   Params P = base_params(x, dtype, n, d, experts, k, E, ws);
+  P.early_gate = early_gate_for(stream);
   P.codes = codes;
   P.q = q;
   P.bucket = bucket;
@@ -2074,6 +2121,7 @@ int launch_permute(const void* x, lshmoe_dtype dtype, int64_t n, int d, const in
   const int nk = static_cast<int>(n * k);
   if (nk == 0) return cudaMemsetAsync(expert_rows, 0, sizeof(int32_t) * E, st);
   Params P = base_params(x, dtype, n, d, experts, k, E, ws);
+  P.early_gate = early_gate_for(stream);
   P.bucket = slot;
   P.expert_rows = expert_rows;
   P.cent = static_cast<uint8_t*>(send);

@@ -37,3 +37,36 @@ def test_gate_hash(L, cfg):
           f"near-ties={int((~clean).sum())}")
     assert not (mism & clean).any()
     assert np.abs(gw.cpu().numpy()[clean] - g_o[clean]).max() <= 1e-4
+
+
+def test_gate_hash_then_compress_ordering(L):
+    """compress reads the gate map before griddepcontrol.wait unless the preceding kernel on the stream
+    is lshmoe_gate_hash (which writes it): gate_hash -> compress back to back on one stream, with the
+    gate map changing between calls (reversed tokens), must equal the same compress after a full
+    synchronisation (compress.cu early_gate; lshmoe.h ordering note)."""
+    cfg = CONFIGS["C2"]
+    case = make_case(L, cfg, seed=5, sanitize=False)
+    rng = np.random.default_rng(7)
+    Wg = torch.from_numpy(rng.standard_normal((cfg.E, cfg.d)) / np.sqrt(cfg.d)).to(torch.float32).to(case.X.dtype)
+    RG = L.rotation_gate(case.R_lib, Wg).cuda()
+    n, d = case.X.shape
+    ws = L.compress_workspace(n, cfg.k, cfg.E, cfg.q, d, case.X.dtype, "cuda")
+    outs = [L.alloc_compressed(n, cfg.k, cfg.E, d, case.X.dtype, "cuda") for _ in range(2)]
+    X0 = case.X.cuda()
+    xs = [X0, X0.flip(0).contiguous()]
+    torch.cuda.synchronize()
+    inputs = []
+    for X, out in zip(xs, outs):
+        codes, zeta, _ = L.gate_hash(X, RG, cfg.q, cfg.E, cfg.k)
+        L.compress(X, codes, zeta, cfg.E, out=out, workspace=ws)   # no launch in between
+        inputs.append((X, codes, zeta))
+    torch.cuda.synchronize()
+    for (X, codes, zeta), out in zip(inputs, outs):
+        ref = L.compress(X, codes, zeta, cfg.E)
+        torch.cuda.synchronize()
+        m = int(ref.num_rows.item())
+        assert int(out.num_rows.item()) == m
+        for f in ("bucket", "perm", "expert_rows"):
+            assert torch.equal(getattr(out, f), getattr(ref, f)), f
+        assert torch.equal(out.row_start[:m + 1], ref.row_start[:m + 1])
+        assert torch.equal(out.centroids[:m], ref.centroids[:m])
