@@ -739,7 +739,7 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     else:
         kf["hbm_frac"] = kh["frac"]
         kernels.append(kf)
-    kernels.append(kern("restore (restore_row2_kernel for k = 1 rows <= 1.5 KB, else restore_kernel)", "hbm",
+    kernels.append(kern("restore (restore_stage_kernel: rows staged by cp.async.bulk, k <= 4, rows <= 2 KB)", "hbm",
                         rest_bytes, t_rest))
     t_lower = max(hash_flops / (tc_peak * 1e12), hash_bytes / (hbm * 1e9)) * 1e6 + comp_bytes / (hbm * 1e9) * 1e6 \
         + rest_bytes / (hbm * 1e9) * 1e6 + 2 * off_rows * row_bytes / (nvlink_gbs * 1e9) * 1e6

@@ -3,7 +3,7 @@
 //
 // Two or three kernels chained by programmatic dependent launch (PDL: each kernel's launch and
 // prologue overlap its predecessor's tail; griddepcontrol.wait orders the data), no host
-// synchronisation.  Group path (n*k <= 16K copies, see group_path): K12 group_kernel (one CTA per
+// synchronisation.  Group path (n*k <= 16K copies or <= 1024 per expert, see group_path): K12 group_kernel (one CTA per
 // expert, everything in shared memory; described at its definition) -> K3.  Tiles path:
 //   K1 tile_kernel   (one CTA per 256-copy tile): insert every copy into an open-addressing hash
 //                    table keyed by (expert, q-tuple of codes) whose slot value converges
@@ -1812,17 +1812,18 @@ bool carveout_max() {
 }
 
 // The group path (group_kernel, one CTA per expert) when the gate map is one compaction round
-// (n*k <= 16K copies), else K1 tiles + K2 clusters, whose per-expert CTA clusters spread the big
-// groups of the 64K-copy layers.  Measured (scripts/compress_diag.py, graph-timed per call):
-// C2 39.5 vs 44.7 us, C5 49.4 vs 48.9, C3 119.0 vs 93.3, C4 108.9 vs 95.6.
-// LSHMOE_COMPRESS_PATH=group / tiles forces one.
-bool group_path(int nk) {
+// (n*k <= 16K copies) or the groups average at most 1024 copies; else K1 tiles + K2 clusters, whose
+// per-expert CTA clusters spread big groups.  Measured (scripts/compress_diag.py, graph-timed per
+// call, with the compaction overlapping the predecessor's tail): C2 32.6 us (group), C5 39.5 vs
+// 48.8 (group vs tiles, 784 copies per expert), C4 83.4 vs 93.5 (1024), C3 91.9 vs 86.7 (2048:
+// tiles).  LSHMOE_COMPRESS_PATH=group / tiles forces one.
+bool group_path(int nk, int E) {
   static const int force = [] {
     const char* e = getenv("LSHMOE_COMPRESS_PATH");
     return !e ? 0 : (e[0] == 'g' ? 1 : (e[0] == 't' ? 2 : 0));
   }();
   if (force) return force == 1;
-  return nk <= kGRound * kGThreads;
+  return nk <= kGRound * kGThreads || static_cast<int64_t>(nk) <= 1024ll * E;
 }
 
 int launch_chain(const Params& P, cudaStream_t st) {
@@ -1846,7 +1847,7 @@ int launch_chain(const Params& P, cudaStream_t st) {
   p.max_range = max_range;
   p.diag = diag_enabled() ? 1 : 0;
   int err = 0;
-  if (group_path(P.nk)) {                        // one CTA per expert (group_kernel), then K3
+  if (group_path(P.nk, P.E)) {                        // one CTA per expert (group_kernel), then K3
     p.dyn_smem = kGroupSmem;
     p.table_clean = 1;
     err = launch_pdl(group_kernel, P.E, kGThreads, kGroupSmem, st, p, true);

@@ -13,6 +13,7 @@
 
 #include "../abi/lshmoe_internal.h"
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace lshmoe {
 
@@ -195,6 +196,132 @@ __global__ void __launch_bounds__(256) restore_row2_kernel(const T* x, const T* 
   }
 }
 
+// Rows staged in shared memory by the bulk-copy engine (k <= 4): 16 warps per CTA (one CTA per SM),
+// each warp owns a ring of `slots` slots, a slot = one token's x row followed by the c~ and E(c~)
+// rows of its k copies, filled by one lane with 1 + 2k cp.async.bulk copies completing on the
+// slot's mbarrier.  The x copy is issued at once, the gathers as soon as the token's bucket ids are
+// known (the ids of a warp's next 32 / k tokens are loaded together, one batch ahead).  At d = 768
+// bf16, k = 1, three tokens per warp (13.5 KB) are in flight without holding registers, against two
+// rows in registers for restore_row2_kernel.  The arithmetic is restore_kernel's, term by term in
+// slot order (same bits as every other restore kernel).
+constexpr int kStageWarps = 16;
+constexpr int kStageSmem = 216 * 1024;
+constexpr int kStageMaxK = 4;
+
+template <typename T, int KK>   // KK = 1: k == 1 at compile time; KK = 0: runtime k <= kStageMaxK
+__global__ void __launch_bounds__(kStageWarps * 32, 1) restore_stage_kernel(const T* x, const T* __restrict__ ct,
+                                                                            const T* __restrict__ ret, int64_t n,
+                                                                            int d, int cpr, int k_arg, int slots, int pf,
+                                                                            const int32_t* __restrict__ bucket,
+                                                                            const float* __restrict__ g, T* y) {
+  using namespace sm100;
+  constexpr int VN = Vec<T>::N;
+  constexpr int kMaxSlots = 8;
+  constexpr int kKMax = KK ? KK : kStageMaxK;
+  const int k = KK ? KK : k_arg;
+  __shared__ __align__(8) uint64_t s_bar[kStageWarps][kMaxSlots];
+  extern __shared__ __align__(128) uint8_t s_ring[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t rb = static_cast<uint32_t>(cpr) * 16u;     // row bytes
+  const uint32_t sb = (1u + 2u * k) * rb;                   // slot bytes
+  const int tb = 32 / k;                                     // tokens per id batch
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kStageWarps;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kStageWarps + warp;
+  const int64_t cnt = gw < n ? (n - 1 - gw) / nw + 1 : 0;    // tokens t = gw + i * nw of this warp
+  uint8_t* ring = s_ring + static_cast<size_t>(warp) * slots * sb;
+  uint64_t* bar = s_bar[warp];
+  if (lane < slots) mbar_init(&bar[lane], 1);
+  fence_mbarrier_init();
+  __syncwarp();
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: the combined rows are complete
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+  auto bulk = [&](uint8_t* dst, const void* src, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(rb), "r"(smem_u32(b))
+                 : "memory");
+  };
+  // bucket ids of tokens [i0, i0 + tb): lane j < tb * k holds copy j % k of token i0 + j / k
+  auto load_ids = [&](int64_t i0) {
+    const int64_t i = i0 + lane / k;
+    return lane < tb * k && i < cnt ? __ldg(bucket + (gw + i * nw) * k + lane % k) : 0;
+  };
+  // lane 0 issues the c~ / E(c~) copies of the token at batch position bpos into `slot`
+  auto gathers = [&](uint8_t* slot, uint64_t* sbar, int ids, int bpos) {
+    for (int s2 = 0; s2 < k; ++s2) {
+      const int64_t b = __shfl_sync(0xFFFFFFFFu, ids, bpos * k + s2);
+      if (lane == 0) {
+        bulk(slot + (1 + 2 * s2) * rb, ct + b * d, sbar);
+        bulk(slot + (2 + 2 * s2) * rb, ret + b * d, sbar);
+      }
+    }
+  };
+  // optional L2 prefetch of the x rows `pf` tokens beyond the ring (more DRAM reads in flight
+  // without shared memory)
+  auto prefetch_x = [&](int64_t i) {
+    if (pf && lane == 0 && i < cnt)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + (gw + i * nw) * d), "r"(rb) : "memory");
+  };
+  int ids = load_ids(0), ids_next = 0;
+  if (lane == 0)                             // x rows of the first `slots` tokens: no dependency
+    for (int s2 = 0; s2 < slots && s2 < cnt; ++s2) {
+      mbar_arrive_expect_tx(&bar[s2], sb);
+      bulk(ring + s2 * sb, x + (gw + s2 * nw) * d, &bar[s2]);
+    }
+  for (int u = 0; u < pf; ++u) prefetch_x(slots + u);
+  if (cnt > tb) ids_next = load_ids(tb);
+  for (int s2 = 0; s2 < slots && s2 < cnt; ++s2) gathers(ring + s2 * sb, &bar[s2], ids, s2);   // slots <= tb
+  // counters instead of 64-bit divisions: slot s and its phase for token i; batch position of the
+  // refill token i + slots
+  int s = 0, nbp = slots == tb ? 0 : slots;
+  uint32_t ph = 0;
+  for (int64_t i = 0; i < cnt; ++i) {
+    const int64_t t = gw + i * nw;
+    float gwv[kKMax];
+#pragma unroll
+    for (int s2 = 0; s2 < kKMax; ++s2) gwv[s2] = g && s2 < k ? __ldg(g + t * k + s2) : 1.0f;
+    mbar_wait(&bar[s], ph);
+    const uint8_t* sx = ring + s * sb;
+    for (int c = lane; c < cpr; c += 32) {
+      float xv[VN], acc[VN];
+      Vec<T>::load(sx + 16 * c, xv);
+#pragma unroll
+      for (int s2 = 0; s2 < kKMax; ++s2) {
+        if (s2 >= k) break;
+        float cv[VN], rv[VN];
+        Vec<T>::load(sx + (1 + 2 * s2) * rb + 16 * c, cv);
+        Vec<T>::load(sx + (2 + 2 * s2) * rb + 16 * c, rv);
+#pragma unroll
+        for (int v = 0; v < VN; ++v) {
+          float term = rv[v] + (xv[v] - cv[v]);       // E(c~) + Delta  (Eq. 5)
+          if (g) term = gwv[s2] * term;
+          acc[v] = (s2 == 0) ? term : acc[v] + term;   // Eq. 2 sum over the k experts
+        }
+      }
+      Vec<T>::store(y + t * d + c * VN, acc);
+    }
+    __syncwarp();                            // every lane has read the slot: refill it
+    const int64_t nx = i + slots;
+    if (nx < cnt) {
+      if (nbp == 0) {                        // next batch of ids (loaded one batch ahead)
+        ids = ids_next;
+        ids_next = nx + tb < cnt ? load_ids(nx + tb) : 0;
+      }
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bar[s], sb);
+        bulk(ring + s * sb, x + (gw + nx * nw) * d, &bar[s]);
+      }
+      prefetch_x(nx + pf);
+      gathers(ring + s * sb, &bar[s], ids, nbp);
+    }
+    if (++nbp == tb) nbp = 0;
+    if (++s == slots) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) unpermute_kernel(const T* __restrict__ ret, int64_t n, int d,
                                                         const int32_t* __restrict__ slot, int k,
@@ -340,6 +467,11 @@ int restore_variant() {   // -1: the measured default (see restore_row_kernel)
   return v ? atoi(v) : -1;
 }
 
+int restore_prefetch() {   // LSHMOE_RESTORE_PF: x rows prefetched to L2 beyond the staged ring
+  const char* v = getenv("LSHMOE_RESTORE_PF");
+  return v ? std::max(0, std::min(8, atoi(v))) : 0;
+}
+
 template <typename T>
 int launch_restore_pdl(const void* x, const void* ct, const void* ret, int64_t n, int d, const int32_t* bucket, int k,
                        const float* g, void* y, cudaStream_t st) {
@@ -370,7 +502,27 @@ int launch_restore_pdl(const void* x, const void* ct, const void* ret, int64_t n
   // C4 (d = 1024) 64.1 vs 75.4 us for the flat kernel); k > 1 keeps the flat kernel (C3 50.1 us vs
   // 59-69 for the row kernels)
   int var = restore_variant();
-  if (var < 0) var = (k == 1 && cpr >= 32 && cpr <= 128) ? 12 : 0;
+  const bool stage_ok = k <= kStageMaxK && cpr <= 128 && kStageSmem / (kStageWarps * (1 + 2 * k) * cpr * 16) >= 1;
+  if (var < 0) var = stage_ok ? 20 : (k == 1 && cpr >= 32 && cpr <= 128) ? 12 : 0;
+  if (var == 20 && stage_ok) {                  // staged: slots per warp from the smem budget
+    static bool staged_cfg = [] {
+      cudaFuncSetAttribute(restore_stage_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageSmem);
+      cudaFuncSetAttribute(restore_stage_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageSmem);
+      return true;
+    }();
+    (void)staged_cfg;
+    const int rb = cpr * 16;
+    const int slots = std::min(8, kStageSmem / (kStageWarps * (1 + 2 * k) * rb));
+    const int64_t warps_needed = (n + 1) / 2;
+    cfg.gridDim = dim3(static_cast<unsigned>(std::max<int64_t>(
+        1, std::min<int64_t>(device_sm_count(), (warps_needed + kStageWarps - 1) / kStageWarps))));
+    cfg.blockDim = dim3(kStageWarps * 32);
+    cfg.dynamicSmemBytes = static_cast<size_t>(kStageWarps) * slots * (1 + 2 * k) * rb;
+    return cudaLaunchKernelEx(&cfg, k == 1 ? restore_stage_kernel<T, 1> : restore_stage_kernel<T, 0>,
+                              static_cast<const T*>(x), static_cast<const T*>(ct),
+                              static_cast<const T*>(ret), n, d, cpr, k, slots, restore_prefetch(), bucket, g,
+                              static_cast<T*>(y));
+  }
   if (var >= 12 && k == 1 && cpr >= 32 && cpr <= 128) {   // 10 + CTAs per SM, two rows per warp
     const int64_t pairs = (n + 1) / 2;
     const int warps = static_cast<int>(std::min<int64_t>(pairs, int64_t(var - 10) * 8 * device_sm_count()));

@@ -33,7 +33,7 @@ done
 if [ -z "$SKIP_NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
      python bench.py --profile --steps 2 --warmup 3 > gpurun_out/ncu_launch_${TAG}.log 2>&1; echo "ncu launches rc=$?"
-  for K in ${KERNELS:-HashSched group_kernel centroid_kernel FfnSched restore_row2_kernel}; do
+  for K in ${KERNELS:-HashSched group_kernel centroid_kernel FfnSched restore_stage_kernel}; do
     timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:$K -s 2 -c 1 \
        -o gpurun_out/prof_${TAG}_${K} python bench.py --profile --steps 1 --warmup 3 > gpurun_out/ncu_${TAG}_${K}.log 2>&1; echo "ncu $K rc=$?"
   done
