@@ -97,8 +97,8 @@ lshmoe_status lshmoe_rotation(int d, int q, uint64_t rotation_seed, lshmoe_dtype
    x [n, d] dtype, rotation [q, d, d] dtype (from lshmoe_rotation) -> codes int16 [n, q]:
    code_tj = sign(y_i*) * (i*+1), i* = argmax_i |y_i|, y = R_j x_t (reading R1); ties to the
    smallest i, a zero winner is '+' (reading R2).  bf16: tcgen05 tensor cores, bf16 x bf16
-   products, fp32 accumulation; f32: SIMT fp32 FMA (reading R19).  Hashed once per token, shared
-   by its k routed copies (reading R6).  n == 0 is a no-op.
+   products, fp32 accumulation; f32: SIMT fp32 FMA (reading R19), d <= 352 (else EUNSUPPORTED).
+   Hashed once per token, shared by its k routed copies (reading R6).  n == 0 is a no-op.
    workspace: device buffer of lshmoe_hash_workspace() bytes (0 for f32 or d <= 256: may be NULL).
    It must be zero-filled before its first use and not written by anyone else afterwards: it holds
    per-tile arrival counters that every call leaves at zero, plus scratch.  A caller allocates it

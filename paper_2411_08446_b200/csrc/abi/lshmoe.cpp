@@ -96,7 +96,7 @@ lshmoe_status lshmoe_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d, c
   REQUIRE(aligned16(x) && aligned16(rotation), LSHMOE_EINVAL, "x / rotation must be 16-byte aligned");
   int err;
   if (dtype == LSHMOE_F32) {
-    REQUIRE(d <= 384, LSHMOE_EUNSUPPORTED, "f32 (SIMT) hash supports d <= 384");
+    REQUIRE(d <= 352, LSHMOE_EUNSUPPORTED, "f32 (SIMT) hash supports d <= 352 (the x tile is staged in shared memory)");
     err = launch_hash_f32(static_cast<const float*>(x), n, d, static_cast<const float*>(rotation), q, codes, stream);
   } else {
     const size_t need = hash_workspace_bytes(n, d, q);
@@ -189,7 +189,7 @@ lshmoe_status lshmoe_sp_hash(const void* x, lshmoe_dtype dtype, int64_t n, int d
   REQUIRE(aligned16(x) && aligned16(normals), LSHMOE_EINVAL, "x / normals must be 16-byte aligned");
   int err;
   if (dtype == LSHMOE_F32) {
-    REQUIRE(d <= 384, LSHMOE_EUNSUPPORTED, "f32 (SIMT) SP hash supports d <= 384");
+    REQUIRE(d <= 352, LSHMOE_EUNSUPPORTED, "f32 (SIMT) SP hash supports d <= 352 (the x tile is staged in shared memory)");
     err = launch_sp_hash_f32(static_cast<const float*>(x), n, d, static_cast<const float*>(normals), q, b, codes, stream);
   } else {
     err = launch_sp_hash_bf16(x, n, d, normals, q, b, codes, stream);

@@ -15,17 +15,24 @@ constexpr int kTok = 128;     // tokens per CTA (one per thread)
 constexpr int kRowsR = 32;    // rotation rows staged per step
 constexpr int kXs = kTok + 1; // padded smem pitch of the transposed x tile (no bank conflicts)
 
-// grid (ceil(n / 128), q).  smem: x tile transposed [d][128] + R rows [32][d].
-__global__ void __launch_bounds__(kTok) hash_f32_kernel(const float* __restrict__ x, int n, int d,
-                                                        const float* __restrict__ R, int q,
-                                                        int16_t* __restrict__ codes) {
+// grid (ceil(n / 128), q), 128 x kRG threads: thread (g, t) scans rotation rows i = g (mod kRG) for
+// token t in ascending i, then the kRG partial winners meet in shared memory (larger |y|, ties to
+// the smaller index: the same winner as one ascending scan).  smem: x tile transposed [d][128] +
+// R rows [32][d] + the partial winners.
+constexpr int kRG = 4;
+__global__ void __launch_bounds__(kTok * kRG) hash_f32_kernel(const float* __restrict__ x, int n, int d,
+                                                              const float* __restrict__ R, int q,
+                                                              int16_t* __restrict__ codes) {
   extern __shared__ float sm[];
   float* xs = sm;                      // [d][kXs]
   float* rs = sm + d * kXs;            // [kRowsR][d]
+  __shared__ float s_best[kRG][kTok];
+  __shared__ int s_idx[kRG][kTok];
+  const int tl = threadIdx.x % kTok, grp = threadIdx.x / kTok;
   const int t0 = blockIdx.x * kTok;
   const int j = blockIdx.y;
   const float* Rj = R + static_cast<int64_t>(j) * d * d;
-  for (int i = threadIdx.x; i < d * kTok; i += kTok) {
+  for (int i = threadIdx.x; i < d * kTok; i += kTok * kRG) {
     const int tt = i / d, k = i - tt * d;                // coalesced read of x rows
     const int t = t0 + tt;
     xs[k * kXs + tt] = t < n ? x[static_cast<int64_t>(t) * d + k] : 0.0f;
@@ -36,12 +43,12 @@ __global__ void __launch_bounds__(kTok) hash_f32_kernel(const float* __restrict_
   for (int i0 = 0; i0 < d; i0 += kRowsR) {
     const int rows = min(kRowsR, d - i0);
     __syncthreads();
-    for (int i = threadIdx.x; i < rows * d; i += kTok) rs[i] = Rj[static_cast<int64_t>(i0) * d + i];
+    for (int i = threadIdx.x; i < rows * d; i += kTok * kRG) rs[i] = Rj[static_cast<int64_t>(i0) * d + i];
     __syncthreads();
-    for (int ii = 0; ii < rows; ++ii) {
+    for (int ii = grp; ii < rows; ii += kRG) {
       const float* rrow = rs + ii * d;
       float y = 0.0f;
-      for (int k = 0; k < d; ++k) y = fmaf(rrow[k], xs[k * kXs + threadIdx.x], y);
+      for (int k = 0; k < d; ++k) y = fmaf(rrow[k], xs[k * kXs + tl], y);
       const float a = fabsf(y);
       if (a > best) {          // ties keep the smaller index; a zero winner is '+' (R2)
         best = a;
@@ -50,8 +57,23 @@ __global__ void __launch_bounds__(kTok) hash_f32_kernel(const float* __restrict_
       }
     }
   }
-  const int t = t0 + threadIdx.x;
-  if (t < n) codes[static_cast<int64_t>(t) * q + j] = static_cast<int16_t>(bneg ? -(bidx + 1) : (bidx + 1));
+  s_best[grp][tl] = best;
+  s_idx[grp][tl] = bneg ? -(bidx + 1) : (bidx + 1);
+  __syncthreads();
+  const int t = t0 + tl;
+  if (grp == 0 && t < n) {
+    float b = s_best[0][tl];
+    int c = s_idx[0][tl];
+    for (int g2 = 1; g2 < kRG; ++g2) {
+      const float a = s_best[g2][tl];
+      const int c2 = s_idx[g2][tl];
+      if (a > b || (a == b && abs(c2) < abs(c))) {
+        b = a;
+        c = c2;
+      }
+    }
+    codes[static_cast<int64_t>(t) * q + j] = static_cast<int16_t>(c);
+  }
 }
 
 // NEXT-3 SP hash, fp32: grid ceil(n / 128) CTAs, one token per thread, the q*b normals staged 32
@@ -156,7 +178,8 @@ int launch_hash_f32(const float* x, int64_t n, int d, const float* R, int q, int
     configured_smem = static_cast<int>(smem);
   }
   dim3 grid(static_cast<unsigned>((n + kTok - 1) / kTok), q);
-  hash_f32_kernel<<<grid, kTok, smem, static_cast<cudaStream_t>(stream)>>>(x, static_cast<int>(n), d, R, q, codes);
+  hash_f32_kernel<<<grid, kTok * kRG, smem, static_cast<cudaStream_t>(stream)>>>(x, static_cast<int>(n), d, R, q,
+                                                                                 codes);
   count_launches(1);
   return cudaGetLastError();
 }

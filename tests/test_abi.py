@@ -79,6 +79,7 @@ def test_validation_errors(L):
     assert lib.lshmoe_rotation(4, 0, 1, 0, v) == L.EINVAL
     assert lib.lshmoe_hash(v, 1, 10, 96, v, 2, v, None, 0, None) == L.EUNSUPPORTED       # bf16, d % 64
     assert lib.lshmoe_hash(v, 0, 10, 6, v, 2, v, None, 0, None) == L.EUNSUPPORTED        # f32, d % 4
+    assert lib.lshmoe_hash(v, 0, 10, 356, v, 2, v, None, 0, None) == L.EUNSUPPORTED      # f32 SIMT, d > 352
     assert lib.lshmoe_hash(v, 1, -1, 64, v, 2, v, None, 0, None) == L.EINVAL
     assert lib.lshmoe_hash(v, 1, 10, 64, v, 17, v, None, 0, None) == L.EUNSUPPORTED      # q > LSHMOE_MAX_Q
     assert b"q > LSHMOE_MAX_Q" in lib.lshmoe_last_error()

@@ -49,7 +49,7 @@ def test_hash_bf16_shapes(L, n, d, q):
     _check_codes(L, case, f"bf16 n={n} d={d}")
 
 
-@pytest.mark.parametrize("n,d,q", [(300, 64, 2), (50, 8, 3)])
+@pytest.mark.parametrize("n,d,q", [(300, 64, 2), (50, 8, 3), (257, 256, 3), (130, 352, 2)])
 def test_hash_f32_shapes(L, n, d, q):
     cfg = small_cfg(n=n, d=d, q=q, dtype="f32")
     case = make_case(L, cfg, seed=2, sanitize=False)

@@ -1,5 +1,7 @@
 """GPU parity of a6-a9 (dispatch, expert FFN, combine, restore) and of the whole layer
 (Alg. 1) against the oracle, plus the uncompressed baseline (Eq. 2)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -59,6 +61,57 @@ def test_restore_identity_expert_exact(L, k):
     assert np.array_equal(y[exact], want[exact])
     assert np.all(np.abs(y - want) <= O.ulp_bf16(want) + 1e-30)
     print(f"[restore identity k={k}] exact-eligible fraction {exact.mean():.6f}")
+
+
+@pytest.mark.parametrize("dtype,d,k,n", [("bf16", 64, 1, 100_000), ("bf16", 768, 2, 50_000), ("bf16", 128, 3, 30_001),
+                                          ("bf16", 1024, 4, 20_000), ("f32", 64, 2, 40_000), ("bf16", 256, 5, 3_000),
+                                          ("bf16", 1536, 1, 5_000), ("bf16", 768, 1, 1)])
+def test_restore_kernels_agree(L, dtype, d, k, n):
+    """Every restore kernel (LSHMOE_RESTORE_VAR: 0 flat, 12 two-row, 20 staged by cp.async.bulk; the
+    default picks one by k and row size) gives the same bits, and the flat one matches the oracle.
+    Sizes give the staged kernel's warps more tokens than one bucket-id batch (32 / k), its k <= 4
+    cases, and the fallbacks (k = 5, rows > 2 KB)."""
+    rng = np.random.default_rng(11)
+    m = max(1, n // 5)
+    dt = _tdt(dtype)
+    X = torch.from_numpy(rng.standard_normal((n, d)).astype(np.float32)).to(dt).cuda()
+    Ct = torch.from_numpy(rng.standard_normal((m, d)).astype(np.float32)).to(dt).cuda()
+    ret = torch.from_numpy(rng.standard_normal((m, d)).astype(np.float32)).to(dt).cuda()
+    bucket = torch.from_numpy(rng.integers(0, m, (n, k)).astype(np.int32)).cuda()
+    g = torch.from_numpy(rng.random((n, k)).astype(np.float32)).cuda()
+    outs = {}
+    old = os.environ.get("LSHMOE_RESTORE_VAR")
+    try:
+        for var in ("0", "12", "20", None):
+            if var is None:
+                os.environ.pop("LSHMOE_RESTORE_VAR", None)
+            else:
+                os.environ["LSHMOE_RESTORE_VAR"] = var
+            outs[var] = (L.restore(X, Ct, ret, bucket), L.restore(X, Ct, ret, bucket, g))
+        torch.cuda.synchronize()
+    finally:
+        if old is None:
+            os.environ.pop("LSHMOE_RESTORE_VAR", None)
+        else:
+            os.environ["LSHMOE_RESTORE_VAR"] = old
+    for var in ("12", "20", None):
+        for a, b in zip(outs["0"], outs[var]):
+            assert torch.equal(a, b), f"variant {var} differs from the flat kernel"
+    sel = np.unique(rng.integers(0, n, 512))          # the flat kernel against the oracle on sampled tokens
+    bs = bucket.cpu().numpy()[sel]
+    xs, cs, rs = f64(X.cpu()[sel]), f64(Ct.cpu()), f64(ret.cpu())
+    for gw, y in ((None, outs["0"][0]), (g.cpu().numpy()[sel], outs["0"][1])):
+        gw64 = None if gw is None else gw.astype(np.float64)
+        ref = O.restore(xs, cs, rs, bs, gw64)
+        got = f64(y.cpu()[sel])
+        if dtype == "bf16":
+            # RNE of the fp32 result: 1 bf16 ulp of the exact value plus the fp32 evaluation's own
+            # error, <= 3 roundings of 2^-24 per term of sum_s g (|r| + |x| + |c|) (cancellation)
+            w = np.ones(bs.shape) if gw64 is None else gw64
+            mag = sum(w[:, s2, None] * (np.abs(rs[bs[:, s2]]) + np.abs(xs) + np.abs(cs[bs[:, s2]])) for s2 in range(k))
+            assert np.all(np.abs(got - ref) <= O.ulp_bf16(ref) + 3 * k * 2.0 ** -24 * mag)
+        else:
+            assert row_rel_err(got, ref) <= 1e-5
 
 
 def test_restore_in_place(L):
