@@ -727,6 +727,7 @@ __device__ void group_body(const Params& P, int e, int n_e, int goff, int T, int
   // kGB members per thread per batch, all their code loads issued before any is used.
   if (KW <= 4) group_keys<kS, 4, 4>(P, n_e, KW, mem, key, aux);   // q <= 8: 4 members' loads in flight
   else group_keys<kS, 2, kMaxQ / 2>(P, n_e, KW, mem, key, aux);
+  dstamp(P, 1, 6);                          // diagnostics: thread 0's keys stored
   __syncthreads();                          // every key is stored before any slot is claimed
   dstamp(P, 1, 1);
   // insert: a slot's value converges (atomicMin) to the smallest member index with its key (a
@@ -998,6 +999,10 @@ constexpr int kCPL = kBlkChunks / 32;    // chunks per lane per block
 #endif
 static_assert(LSHMOE_CWARPS == 8 || LSHMOE_CWARPS == 16, "centroid warps: 8 or 16");
 constexpr int kCWarps = LSHMOE_CWARPS;
+#ifndef LSHMOE_CGRID
+#define LSHMOE_CGRID 1   // experiment: centroid CTAs per SM (2 with 8 warps and 8 KB rings)
+#endif
+constexpr int kCPerSM = LSHMOE_CGRID;
 constexpr int kCThreads = 32 * kCWarps;
 constexpr int kRingSlot = 16 * kBlkChunks;
 constexpr int kWpartFloats = kBlkChunks * 8;   // one warp partial slot (fp32, up to 8 per chunk)
@@ -1612,7 +1617,7 @@ __device__ void fused_close(const Params& P, uint32_t ep) {
 // kF: the fused dispatch (lshmoe_compress_p2p) — compiled separately, so the plain kernel's
 // reduction loop carries no remote-store code.
 template <bool kF>
-__global__ void __launch_bounds__(kCThreads, 1) centroid_kernel(Params P) {
+__global__ void __launch_bounds__(kCThreads, kCPerSM) centroid_kernel(Params P) {
   __shared__ int s_goff[kRadix + 1];         // perm offset of each expert group
   __shared__ int s_roff[kRadix + 1];         // first global row of each expert
   __shared__ int s_mrow[kRadix];             // m_e
@@ -1757,7 +1762,7 @@ __global__ void __launch_bounds__(kCThreads, 1) grad_centroid_kernel(Params P) {
 
 constexpr int kCentroidSmemMax = 216 * 1024;   // K3 dynamic smem + static <= 227 KB
 constexpr int kBucketSmem = 200 * 1024;        // K2 dynamic smem (+ 8 KB static)
-int centroid_grid() { return std::min(device_sm_count(), kMaxGrid); }
+int centroid_grid() { return std::min(kCPerSM * device_sm_count(), kMaxGrid); }
 int centroid_max_range(int nk) {
   const int G = centroid_grid();
   return (nk + G - 1) / G + 1;

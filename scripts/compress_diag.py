@@ -55,6 +55,9 @@ L.set_diagnostics(False)
 print("kernel spans", L.compress_phase_times(ws))
 m = int(out.num_rows.item())
 print(f"m={m} expert_rows max={int(out.expert_rows.max())}")
+gsz = torch.bincount(zd.flatten().long(), minlength=cfg.E).cpu().numpy()
+print(f"group sizes: max {int(gsz.max())} (expert {int(gsz.argmax())}), median {int(np.median(gsz))}; "
+      f"rows of the largest group {int(out.expert_rows[int(gsz.argmax())])}")
 for kern, st in L.compress_diag(ws).items():
     D = {k: np.array(v) for k, v in st.items()}
     if np.all(np.isnan(D["end"])):
