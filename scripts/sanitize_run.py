@@ -56,6 +56,14 @@ L.hash_e4m3(L.quantize_e4m3(Xd), L.rotation_e4m3(768, 6, 3).cuda())
 L.hash_hd3(Xd, L.hd3_signs(6, 3).cuda())
 torch.cuda.synchronize()
 print("sp / e4m3 / hd3 hashes ok", flush=True)
+# NEXT-2 gate + hash, then compress on the same stream (the gate map is read after the dependency
+# wait here; the plain compress calls above read it before)
+Wg = (torch.randn((small.E, 768)) / 768 ** 0.5).to(torch.bfloat16)
+RG = L.rotation_gate(L.rotation(768, 6, 3, torch.bfloat16), Wg).cuda()
+gcodes, gzeta, _ = L.gate_hash(Xd, RG, 6, small.E, 2)
+L.compress(Xd, gcodes, gzeta, small.E)
+torch.cuda.synchronize()
+print("gate_hash -> compress ok", flush=True)
 # phase 2: local group of 2 virtual ranks (each on its own stream), then the fused compress at world 1
 E, d = 8, 768
 comms = L.Comm.local_group(2, 4000, 4000, d, torch.bfloat16, E)
