@@ -232,6 +232,7 @@ struct FfnSched {
   }
   int order;        // 0: units expert-major (e, mt, nt); 1: N-tile-major (nt, e, mt)
   int b_evict_first = 0;   // 1: weight loads carry an L2 evict-first policy (LSHMOE_FFN_EVICT)
+  int pre_kb = 0;          // weight k-blocks warmed into L2 before the dependency wait (LSHMOE_FFN_PREKB)
   __device__ int units() const { return tiles_pre[E_local]; }
   __device__ WorkItem get(int u, int rank, int /*group*/) const {
     int e = 0, mt, nt;
@@ -270,6 +271,23 @@ struct FfnSched {
 template <class Sched>
 __device__ __forceinline__ bool sched_b_evict_first(const Sched&) { return false; }
 __device__ __forceinline__ bool sched_b_evict_first(const FfnSched& s) { return s.b_evict_first != 0; }
+
+// Before the dependency wait (the weights are inputs no predecessor writes): cluster g warms L2
+// with the first pre_kb k-blocks of this CTA's half of every (expert, N-tile) weight tile
+// i = g, g + G, ..., so the first TMA loads after the wait hit L2 while the predecessor's last CTAs
+// finish (the centroid kernel before GEMM 1 gathers from L2 and leaves HBM idle).
+template <class Sched>
+__device__ __forceinline__ void sched_prefetch_static(const Sched&, const CUtensorMap*, int, int, int, int, int) {}
+__device__ __forceinline__ void sched_prefetch_static(const FfnSched& s, const CUtensorMap* tmB, int cluster,
+                                                      int nclusters, int rank, int brows, int kbe) {
+  if (s.pre_kb <= 0) return;
+  const int ntn = s.N / s.bn;
+  for (int i = cluster; i < s.E_local * ntn; i += nclusters) {
+    const int e = i / ntn, nt = i - e * ntn;
+    const int brow = e * s.N + nt * s.bn + rank * brows;
+    for (int kb = 0; kb < s.pre_kb; ++kb) tma_prefetch_l2_2d(tmB, kb * kbe, brow);
+  }
+}
 
 // ---- epilogues -------------------------------------------------------------------------------
 constexpr int kMaxGateK = 8;
@@ -702,6 +720,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (kCta == 2) tmem_alloc_2cta<C::kTmemCols>(tmem_slot);
     else tmem_alloc<C::kTmemCols>(tmem_slot);
   }
+  if (warp == 0 && lane == 0)   // static operands only (FFN weights): an L2 warm-up before the wait
+    sched_prefetch_static(sched, &tmB, blockIdx.x / static_cast<int>(cluster_nctarank()),
+                          static_cast<int>(gridDim.x / cluster_nctarank()), static_cast<int>(cluster_ctarank()) % kCta,
+                          C::kBRows, 128 / kEB);
   // PDL: everything above (barriers, TMEM, descriptor prefetch) overlaps the previous kernel's
   // tail; nothing a predecessor writes is read before this wait.  Then let the next kernel launch.
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1050,6 +1072,11 @@ int ffn_evict_first() {
   return env && env[0] == '0' ? 0 : 1;
 }
 
+int ffn_pre_kb() {   // LSHMOE_FFN_PREKB: weight k-blocks warmed into L2 before the dependency wait
+  const char* env = getenv("LSHMOE_FFN_PREKB");
+  return env ? atoi(env) : 4;
+}
+
 int ffn_prefetch() {   // experiment override LSHMOE_FFN_PF (k-blocks); default 0 (measured: no gain)
   const char* env = getenv("LSHMOE_FFN_PF");
   return env ? atoi(env) : 0;
@@ -1318,6 +1345,7 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
   const int exp = experiment_mode("LSHMOE_FFN_EXP");     // experiment: 1 = no output stores, 2 = no MMAs
   FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, ffn_prefetch(), nullptr, nullptr, ffn_order()};
   s1.b_evict_first = ffn_evict_first();
+  s1.pre_kb = ffn_pre_kb();
   const int bn1 = env_bn("LSHMOE_FFN_BN1", d_ffn, pick_bn(d_ffn));
   int err = 0;
   if (only == 2) {
@@ -1334,6 +1362,7 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
   if (err || only == 1) return err;
   FfnSched s2{recv_rows, E_local, world, d, 0, 0, ffn_prefetch(), nullptr, nullptr, ffn_order()};
   s2.b_evict_first = ffn_evict_first();
+  s2.pre_kb = ffn_pre_kb();
   const int bn2 = env_bn("LSHMOE_FFN_BN2", d, pick_bn(d));
   if (bn2 == 256) {
     BiasActEpi<256> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false}; e2.exp = exp;
