@@ -719,7 +719,11 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
     kernels.append(kern("compress: group + centroid (2 launches)" if group_path else
                         "compress: tile + bucket + centroid (3 launches)", "hbm", comp_bytes, t_comp))
     if span.get("centroid"):
-        kernels.append(kern("centroid_kernel (span, diagnostics stamps)", "hbm", cent_bytes, span["centroid"]))
+        kc = kern("centroid_kernel (span, diagnostics stamps)", "hbm", cent_bytes, span["centroid"])
+        kc["note"] = ("the gathered token rows are L2-resident (read by the hash just before; application-replay "
+                      "ncu: ~1.4 MB of DRAM reads per launch at C2, profiles/l2_residency_r2g.md): the fraction "
+                      "of HBM is a latency figure (ring rounds of L2 latency per warp, index and cut-row phases)")
+        kernels.append(kc)
     for nm_ in ("tiles", "bucket"):
         if span.get(nm_):
             label = "group_kernel" if group_path and nm_ == "bucket" else f"{nm_} kernel"
