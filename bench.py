@@ -827,6 +827,21 @@ def run_bench(args, cfg, L, world, rank, local_rank, dev, comm, E_local, X_cpu, 
                 # the measured cuBLAS figure is not the hardware ceiling: the kernel can exceed it (frac > 1);
                 # against NVIDIA's nominal dense bf16 figure it stays below 1
                 "frac_of_nominal": achieved / 2250.0, "nominal_tflops": 2250.0}
+        # the binding resource: TMA ingest from L2.  Each CTA-pair chunk (256 tokens x hash j x 256-column
+        # slice) stages its CTAs' 128 x d token rows and 128 x d rotation rows: 4 * 128 * d bytes per CTA
+        # chunk, d / 256 slices x q hashes per 256-token pair tile.  The chip's TMA / L2 (LTS) throughput
+        # cap is ~6300 B/cycle (B300_MICROARCH.md, measured on B300; the same per-SM figure the FFN's TMA
+        # streams reach here), times the SM clock of the run.
+        if d % 256 == 0:
+            chunks = 2 * ((n + 255) // 256) * cfg.q * (d // 256)
+            ingest = chunks * 4.0 * 128 * d
+            clk_ghz = pk_clock_ghz()
+            l2_peak = 6300.0 * clk_ghz * 1e9 / 1e12
+            roof["l2_ingest"] = {"bytes": ingest, "achieved_tbs": ingest / (hash_dev_ms / 1e3) / 1e12,
+                                 "peak_tbs": l2_peak, "frac": ingest / (hash_dev_ms / 1e3) / 1e12 / l2_peak,
+                                 "peak_source": "B300_MICROARCH.md TMA chip throughput ~6300 B/cycle (LTS cap) x "
+                                                "sm_max_mhz: the hash's binding roof (it re-stages each token "
+                                                "tile once per (hash, slice))"}
 
     cpu = None
     parity = None
