@@ -204,7 +204,10 @@ __global__ void __launch_bounds__(256) restore_row2_kernel(const T* x, const T* 
 // bf16, k = 1, three tokens per warp (13.5 KB) are in flight without holding registers, against two
 // rows in registers for restore_row2_kernel.  The arithmetic is restore_kernel's, term by term in
 // slot order (same bits as every other restore kernel).
-constexpr int kStageWarps = 16;
+#ifndef LSHMOE_RSTAGE_WARPS
+#define LSHMOE_RSTAGE_WARPS 16   // experiment knob (compile-time): warps per CTA of the staged restore
+#endif
+constexpr int kStageWarps = LSHMOE_RSTAGE_WARPS;
 constexpr int kStageSmem = 216 * 1024;
 constexpr int kStageMaxK = 4;
 
