@@ -2,9 +2,11 @@
 // P:L536-538) summed over the k gated experts as in Eq. 2:
 //     y_t = sum_s g_ts * (E(c~)[b_ts] + (x_t - c~[b_ts]))
 // The residual x - c~ is never materialised: it is recomputed here from x and the transmitted
-// centroid (reading R11), saving a write + read of n*k*d elements.  Flat 128-bit streaming: one
-// thread per 16-byte chunk of an output row; c~ / E(c~) rows are gathers (mostly L2 hits).
-// Also: the baseline un-permute and the world == 1 local exchange.
+// centroid (reading R11), saving a write + read of n*k*d elements.  Default kernel (k <= 4, rows
+// <= 2 KB): restore_stage_kernel, each token's x row and its c~ / E(c~) rows staged in shared memory
+// by cp.async.bulk into per-warp mbarrier rings; the two-row warp kernel and the flat thread-per-
+// 16-byte-chunk kernel cover the rest.  All variants evaluate the same expression in the same order
+// (bit-identical outputs).  Also: the baseline un-permute and the world == 1 local exchange.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
