@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(kTok * kRG) hash_f32_kernel(const float* __res
   const int t0 = blockIdx.x * kTok;
   const int j = blockIdx.y;
   const float* Rj = R + static_cast<int64_t>(j) * d * d;
+#pragma unroll 8   // several loads in flight per thread (the tile is one dependent round trip, not 16)
   for (int i = threadIdx.x; i < d * kTok; i += kTok * kRG) {
     const int tt = i / d, k = i - tt * d;                // coalesced read of x rows
     const int t = t0 + tt;
@@ -43,11 +44,13 @@ __global__ void __launch_bounds__(kTok * kRG) hash_f32_kernel(const float* __res
   for (int i0 = 0; i0 < d; i0 += kRowsR) {
     const int rows = min(kRowsR, d - i0);
     __syncthreads();
+#pragma unroll 8
     for (int i = threadIdx.x; i < rows * d; i += kTok * kRG) rs[i] = Rj[static_cast<int64_t>(i0) * d + i];
     __syncthreads();
     for (int ii = grp; ii < rows; ii += kRG) {
       const float* rrow = rs + ii * d;
       float y = 0.0f;
+#pragma unroll 8   // the shared-memory loads of 8 steps issue together; the FMA chain keeps ascending k
       for (int k = 0; k < d; ++k) y = fmaf(rrow[k], xs[k * kXs + tl], y);
       const float a = fabsf(y);
       if (a > best) {          // ties keep the smaller index; a zero winner is '+' (R2)
