@@ -606,7 +606,10 @@ __global__ void __launch_bounds__(kBThreads, 1) bucket_kernel(Params P) {
 // global hash table, no cross-CTA round trip, no cluster barrier: the dependent global accesses
 // are the gate-map reads, the code gathers and the output stores.  A group whose arrays do not fit
 // in shared memory runs the same code on per-group regions of the workspace (global mode).
-constexpr int kGThreads = 1024;
+#ifndef LSHMOE_GTHREADS
+#define LSHMOE_GTHREADS 1024   // experiment knob (compile-time): threads of the group kernel's CTA
+#endif
+constexpr int kGThreads = LSHMOE_GTHREADS;
 constexpr int kGWarps = kGThreads / 32;
 constexpr int kGRound = 16;              // gate-map entries per thread per compaction round
 constexpr int kGroupSmem = 222 * 1024;   // dynamic shared memory of group_kernel (+ 2.2 KB static)
