@@ -1083,9 +1083,15 @@ int ffn_evict_first() {
   return env && env[0] == '0' ? 0 : 1;
 }
 
-int ffn_pre_kb() {   // LSHMOE_FFN_PREKB: weight k-blocks warmed into L2 before the dependency wait
+// LSHMOE_FFN_PREKB: weight k-blocks warmed into L2 before the dependency wait (default 4), capped so
+// that the warm-up stays a small fraction of L2: at most 32 MB over all E_local x N weight rows
+// (C2: 4 k-blocks = 25 MB; C4's first GEMM, 134 MB per k-block: none).
+int ffn_pre_kb(int E_local, int N) {
   const char* env = getenv("LSHMOE_FFN_PREKB");
-  return env ? atoi(env) : 4;
+  const int want = env ? atoi(env) : 4;
+  const int64_t per_kb = static_cast<int64_t>(E_local) * N * 128;   // bytes of one k-block of every row
+  const int64_t cap = per_kb > 0 ? (32ll << 20) / per_kb : 0;
+  return static_cast<int>(std::min<int64_t>(want, cap));
 }
 
 int ffn_prefetch() {   // experiment override LSHMOE_FFN_PF (k-blocks); default 0 (measured: no gain)
@@ -1360,7 +1366,7 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
   const int exp = experiment_mode("LSHMOE_FFN_EXP");     // experiment: 1 = no output stores, 2 = no MMAs
   FfnSched s1{recv_rows, E_local, world, d_ffn, 0, 0, ffn_prefetch(), nullptr, nullptr, ffn_order()};
   s1.b_evict_first = ffn_evict_first();
-  s1.pre_kb = ffn_pre_kb();
+  s1.pre_kb = ffn_pre_kb(E_local, d_ffn);
   const int bn1 = env_bn("LSHMOE_FFN_BN1", d_ffn, pick_bn(d_ffn));
   int err = 0;
   if (only == 2) {
@@ -1377,7 +1383,7 @@ int launch_ffn_bf16(const void* in, int d, int d_ffn, const int32_t* recv_rows, 
   if (err || only == 1) return err;
   FfnSched s2{recv_rows, E_local, world, d, 0, 0, ffn_prefetch(), nullptr, nullptr, ffn_order()};
   s2.b_evict_first = ffn_evict_first();
-  s2.pre_kb = ffn_pre_kb();
+  s2.pre_kb = ffn_pre_kb(E_local, d);
   const int bn2 = env_bn("LSHMOE_FFN_BN2", d, pick_bn(d));
   if (bn2 == 256) {
     BiasActEpi<256> e2{static_cast<const __nv_bfloat16*>(b2), static_cast<__nv_bfloat16*>(out), d, false}; e2.exp = exp;
