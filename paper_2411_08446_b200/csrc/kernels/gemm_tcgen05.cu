@@ -96,7 +96,6 @@ struct HashSched {
                     // the cluster tile, all walking the same (j, slice) chunk sequence (same B loads)
   int G;            // clusters (contig)
   int max_pieces;   // units per cluster (contig)
-  int pre_a = 0;    // k-blocks of the first unit's token tile warmed into L2 before the dependency wait
   __device__ void init(void*) {}
   int split;   // 1: one unit per BN slice; 0: one unit covers all d / BN slices (no merge)
   __device__ int units() const {
@@ -278,21 +277,9 @@ __device__ __forceinline__ bool sched_b_evict_first(const FfnSched& s) { return 
 // i = g, g + G, ..., so the first TMA loads after the wait hit L2 while the predecessor's last CTAs
 // finish (the centroid kernel before GEMM 1 gathers from L2 and leaves HBM idle).
 template <class Sched>
-__device__ __forceinline__ void sched_prefetch_static(const Sched&, const CUtensorMap*, const CUtensorMap*, int, int,
-                                                      int, int, int, int, int) {}
-// The hash: the token tile of this CTA's first unit (x is an input of the step; an L2 prefetch is
-// only a hint, so it is safe even if a predecessor were still writing x).
-__device__ __forceinline__ void sched_prefetch_static(const HashSched& s, const CUtensorMap* tmA, const CUtensorMap*,
-                                                      int cluster, int, int rank, int group, int, int kbe,
-                                                      int kblocks) {
-  if (s.pre_a <= 0 || cluster >= s.units()) return;
-  const WorkItem w = s.get(cluster, rank, group);
-  if (w.nchunks <= 0 || w.valid_rows <= 0) return;
-  for (int kb = 0; kb < s.pre_a && kb < kblocks; ++kb) tma_prefetch_l2_2d(tmA, kb * kbe, w.a_row);
-}
-__device__ __forceinline__ void sched_prefetch_static(const FfnSched& s, const CUtensorMap*, const CUtensorMap* tmB,
-                                                      int cluster, int nclusters, int rank, int, int brows, int kbe,
-                                                      int) {
+__device__ __forceinline__ void sched_prefetch_static(const Sched&, const CUtensorMap*, int, int, int, int, int) {}
+__device__ __forceinline__ void sched_prefetch_static(const FfnSched& s, const CUtensorMap* tmB, int cluster,
+                                                      int nclusters, int rank, int brows, int kbe) {
   if (s.pre_kb <= 0) return;
   const int ntn = s.N / s.bn;
   for (int i = cluster; i < s.E_local * ntn; i += nclusters) {
@@ -733,8 +720,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (kCta == 2) tmem_alloc_2cta<C::kTmemCols>(tmem_slot);
     else tmem_alloc<C::kTmemCols>(tmem_slot);
   }
-  if (warp == 0 && lane == 0)   // inputs only (FFN weights, hash tokens): an L2 warm-up before the wait
-    sched_prefetch_static(sched, &tmA, &tmB, cluster, nclusters, rank, group, C::kBRows, kBKe, kblocks);
+  if (warp == 0 && lane == 0)   // static operands only (FFN weights): an L2 warm-up before the wait
+    sched_prefetch_static(sched, &tmB, blockIdx.x / static_cast<int>(cluster_nctarank()),
+                          static_cast<int>(gridDim.x / cluster_nctarank()), static_cast<int>(cluster_ctarank()) % kCta,
+                          C::kBRows, 128 / kEB);
   // PDL: everything above (barriers, TMEM, descriptor prefetch) overlaps the previous kernel's
   // tail; nothing a predecessor writes is read before this wait.  Then let the next kernel launch.
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1147,10 +1136,6 @@ int launch_hash_bf16(const void* x, int64_t n, int d, const void* R, int q, int1
   s.q = q;
   s.d = d;
   s.m_tiles = static_cast<int>((n + BM * cta - 1) / (BM * cta));
-  {
-    const char* pa = getenv("LSHMOE_HASH_PREA");   // k-blocks of the first token tile warmed into L2
-    s.pre_a = pa ? atoi(pa) : 0;     // measured neutral at C2 (default off)
-  }
   const int bn = pick_bn(d);
   ArgmaxEpi e{};
   e.codes = codes;
